@@ -1,0 +1,240 @@
+/*
+ * psb.h -- C ABI of the B200-native data-parallel gradient path
+ *          (compress -> aggregate -> apply) of arXiv 2506.17551.
+ *
+ * Drop-in boundary.  The reference (parsim, header-only C++20) has no C ABI;
+ * its interface is the C++ API in namespace parsim.  Each entry
+ * point below names the reference function it replaces (file:line under
+ * /root/reference/proj/include/parsim).  A host binding (ctypes, the C++
+ * facade in include/parsim_b200.hpp, or a cgo/JNI stub)
+ * calls these with plain device pointers and sizes; no torch types appear.
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers unless marked (host).
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream) and returns immediately.  Argument errors are reported
+ *     synchronously (PSB_EINVAL, text in psb_last_error(), same wording as the
+ *     reference's detail::require messages).  Data-dependent errors (a
+ *     non-finite residual or parameter, parsim/numerics.hpp:57-61) raise a
+ *     device flag that psb_check() turns into PSB_ENONFINITE.
+ *   - The caller owns g, r (error-feedback residual), theta and all outputs;
+ *     the ctx owns every scratch buffer (allocated once in psb_ctx_create,
+ *     none per call) and the NCCL communicator.
+ *   - A ctx is bound to one device and one stream at a time; not thread-safe.
+ *   - Index type is u32: n must be < 2^32.
+ *   - f32 is the production type; f64 instantiations exist for bit-exact
+ *     parity with the f64 reference.
+ */
+#ifndef PSB_H_
+#define PSB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSB_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define PSB_API __attribute__((visibility("default")))
+#else
+#define PSB_API
+#endif
+
+typedef struct psb_ctx psb_ctx;
+typedef struct CUstream_st* psb_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  PSB_OK = 0,
+  PSB_EINVAL = 1,     /* precondition failed (reference: std::invalid_argument) */
+  PSB_ENONFINITE = 2, /* non-finite residual/parameter (reference: check_finite) */
+  PSB_ECUDA = 3,
+  PSB_ENCCL = 4,
+  PSB_ENOMEM = 5,
+  PSB_ESTATE = 6 /* ctx misuse (e.g. collective without psb_comm_init) */
+} psb_status;
+
+typedef enum { PSB_F32 = 0, PSB_F64 = 1 } psb_dtype;
+
+/* CollectiveAlgorithm fold orders, parsim/collectives.hpp:41, 68-128.
+ * pipelined_ring folds like ring (collectives.hpp:142-143). */
+typedef enum { PSB_ORDER_NAIVE = 0, PSB_ORDER_RING = 1, PSB_ORDER_HIER = 2 } psb_order;
+
+/* CompressorKind, parsim/compression.hpp:20 (none/onebit/topk), plus the
+ * north-star additions with no reference code: top-k with int8
+ * values and the dense 8-bit block quantizer. */
+typedef enum {
+  PSB_COMP_NONE = 0,
+  PSB_COMP_ONEBIT = 1,
+  PSB_COMP_TOPK = 2,
+  PSB_COMP_TOPK_Q8 = 3,
+  PSB_COMP_Q8 = 4
+} psb_compressor;
+
+typedef enum { PSB_DIST_UNIFORM = 0, PSB_DIST_LLMREC = 1, PSB_DIST_TIES = 2 } psb_dist;
+
+/* Topology grouping used by the hierarchical fold, parsim/collectives.hpp:18-39. */
+typedef struct {
+  uint32_t racks;
+  uint32_t nodes_per_rack;
+  uint32_t devices_per_node;
+} psb_topology;
+
+/* ------------------------------------------------------------ context */
+PSB_API int psb_abi_version(void);
+PSB_API const char* psb_status_string(psb_status s);
+
+/* Allocates all workspace for gradients up to max_n elements, top-k up to
+ * max_k, and up to max_workers payloads per step (P = local workers x ranks). */
+PSB_API psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, size_t max_k, int max_workers);
+PSB_API void psb_ctx_destroy(psb_ctx* ctx);
+PSB_API const char* psb_last_error(const psb_ctx* ctx);
+
+/* Synchronizes `stream` and converts device error flags raised since the
+ * last check into a status (PSB_ENONFINITE), clearing them. */
+PSB_API psb_status psb_check(psb_ctx* ctx, psb_stream_t stream);
+
+/* Number of the ctx's own kernels launched so far (for launch accounting). */
+PSB_API uint64_t psb_launch_count(const psb_ctx* ctx);
+
+/* Bytes of one worker's top-k payload block: u32 idx[k] | pad16 | val[k] | pad16
+ * (TOPK, val of dtype) or u32 idx[k] | pad16 | i8 code[k] | pad16 |
+ * f32 scale[ceil(k/128)] | pad16 (TOPK_Q8). */
+PSB_API size_t psb_payload_bytes(psb_compressor c, psb_dtype dt, size_t k);
+
+/* -------------------------------------------------------- communicator
+ * One rank per GPU, NCCL over NVLink/NVSwitch.  uid is 128 bytes (host). */
+PSB_API psb_status psb_comm_unique_id(void* uid_out);
+PSB_API psb_status psb_comm_init(psb_ctx* ctx, int rank, int nranks, const void* uid);
+PSB_API int psb_comm_rank(const psb_ctx* ctx);
+PSB_API int psb_comm_size(const psb_ctx* ctx);
+/* In-place allgather: buf holds nranks blocks of bytes_per_rank; this rank's
+ * block is at buf + rank*bytes_per_rank. */
+PSB_API psb_status psb_allgather(psb_ctx* ctx, void* buf, size_t bytes_per_rank, psb_stream_t stream);
+
+/* ---------------------------------------------------------- generator
+ * Counter-based synthetic gradients, identical bits to
+ * oracle/psb_oracle.c:orc_generate.  Input generation only. */
+PSB_API psb_status psb_generate(psb_dist dist, uint64_t seed, uint32_t rank, uint32_t step, size_t n,
+                        float* out, psb_stream_t stream);
+
+/* -------------------------------------------------------- compressors */
+
+/* K1: ef_compress_step with the top-k compressor (compression.hpp:146-157 ->
+ * compress_topk :81-99).  p = r + g; the k entries of largest |p| (ties to
+ * the lower index) are emitted with indices ascending; r := (selected ? +0 : p).
+ * r == NULL: transient zero residual (strategies.hpp:97-102), p = g, nothing
+ * written back -- with g as input this is compress_topk itself.
+ * `worker` in [0, max_workers) keys the per-worker selection history used to
+ * predict the threshold (results never depend on it).  idx_out: u32[k];
+ * val_out: dtype[k]. */
+PSB_API psb_status psb_ef_topk(psb_ctx* ctx, psb_dtype dt, int worker, const void* g, void* r, size_t n,
+                       size_t k, uint32_t* idx_out, void* val_out, psb_stream_t stream);
+
+/* K1 + int8 values (north-star, unpinned): the selected values p[idx] are
+ * quantized in blocks of 128 consecutive payload entries with the 8-bit rule
+ * of psb_q8_quantize; r := (selected ? p - code*scale : p). */
+PSB_API psb_status psb_ef_topk_q8(psb_ctx* ctx, int worker, const float* g, float* r, size_t n, size_t k,
+                          uint32_t* idx_out, int8_t* codes_out, float* scales_out,
+                          psb_stream_t stream);
+
+/* 1-bit sign compressor with EF: compress_onebit (compression.hpp:67-77) on
+ * p = r + g.  words_out: u32[ceil(n/32)], bit i%32 of word i/32 = (p_i >= 0)
+ * (little-endian identical to the reference sign_bytes); scale_out: one f64
+ * (device) = sum|p_i| / n (fixed-shape deterministic reduction); r := p -
+ * (+-scale) in dtype. */
+PSB_API psb_status psb_ef_onebit(psb_ctx* ctx, psb_dtype dt, const void* g, void* r, size_t n,
+                         uint32_t* words_out, double* scale_out, psb_stream_t stream);
+
+/* 8-bit block quantizer (north-star, no reference code; spec in
+ * oracle/psb_oracle.c:orc_q8_quant): per block of `block` elements scale =
+ * absmax/127, code = rint(p/scale) in [-127,127]; r (nullable) := p - code*scale. */
+PSB_API psb_status psb_q8_quantize(psb_ctx* ctx, const float* x, float* r, size_t n, uint32_t block,
+                           int8_t* codes, float* scales, psb_stream_t stream);
+PSB_API psb_status psb_q8_dequantize(psb_ctx* ctx, const int8_t* codes, const float* scales, size_t n,
+                             uint32_t block, float* out, psb_stream_t stream);
+
+/* decompress of one top-k payload into a dense vector (compression.hpp:113-142):
+ * out (n, pre-zeroed by the caller) receives val at idx.  Index validation
+ * (idx < n, strictly increasing) raises a device flag reported by psb_check as
+ * PSB_EINVAL ("decompress: index out of range" / "indices not strictly increasing"). */
+PSB_API psb_status psb_decompress_topk(psb_ctx* ctx, psb_dtype dt, const uint32_t* idx, const void* val,
+                               size_t k, size_t n, void* out, psb_stream_t stream);
+
+/* ------------------------------------------------- aggregate + apply */
+
+/* decompress + allreduce_mean + vec_axpy(-lr, mean, theta) for P top-k
+ * payload blocks (strategies.hpp:105-112, collectives.hpp:135-148,
+ * numerics.hpp:70-78), without materializing dense messages.  payloads: P
+ * blocks of psb_payload_bytes(PSB_COMP_TOPK or TOPK_Q8, dt, k) in worker order.
+ * The mean at each touched index is folded over the P dense values (+0 where a
+ * worker did not select the index) in the configured order, so results are
+ * bit-identical to the reference's dense fold; theta is updated in place with
+ * a separate multiply and add (no FMA).  Untouched entries are unchanged
+ * (bitwise, as (-lr)*(+0) + theta == theta).  mean_out (nullable, dense n,
+ * pre-zeroed by the caller) receives the mean at touched indices.
+ * theta == NULL computes the mean only (allreduce_mean without the update);
+ * the same holds for psb_dense_mean_sgd and psb_onebit_mean_sgd. */
+PSB_API psb_status psb_sparse_mean_sgd(psb_ctx* ctx, psb_compressor c, psb_dtype dt, int P,
+                               const void* payloads, size_t k, psb_order order,
+                               const psb_topology* topo, double lr, void* theta, size_t n,
+                               void* mean_out, psb_stream_t stream);
+
+/* Eq. 12 async application of P payloads in worker order: theta :=
+ * (-eta_p/(1+tau_p)) * decompress(msg_p) + theta for p = 0..P-1
+ * (strategies.hpp:125-129 applied as in trainer.hpp:245-254).
+ * scale_per_worker (host, P doubles) = eta/(1+tau_p). */
+PSB_API psb_status psb_sparse_async_apply(psb_ctx* ctx, psb_compressor c, psb_dtype dt, int P,
+                                  const void* payloads, size_t k, const double* scale_per_worker,
+                                  void* theta, size_t n, psb_stream_t stream);
+
+/* compressor none: allreduce_mean over P dense buffers [P][n] + SGD. */
+PSB_API psb_status psb_dense_mean_sgd(psb_ctx* ctx, psb_dtype dt, int P, const void* bufs, psb_order order,
+                              const psb_topology* topo, double lr, void* theta, size_t n,
+                              void* mean_out, psb_stream_t stream);
+
+/* 1-bit: words [P][ceil(n/32)], scales (device, P doubles) -> mean + SGD. */
+PSB_API psb_status psb_onebit_mean_sgd(psb_ctx* ctx, psb_dtype dt, int P, const uint32_t* words,
+                               const double* scales, psb_order order, const psb_topology* topo,
+                               double lr, void* theta, size_t n, void* mean_out,
+                               psb_stream_t stream);
+
+/* ------------------------------------------------------- step drivers */
+typedef struct {
+  psb_compressor compressor;
+  psb_dtype dtype;
+  size_t n;          /* gradient length */
+  size_t k;          /* top-k per worker (TOPK, TOPK_Q8) */
+  uint32_t q8_block; /* block size for PSB_COMP_Q8 (e.g. 256) */
+  int workers;       /* local virtual workers W: g and r hold W rows of n */
+  const void* g;     /* [W][n] this rank's gradients */
+  void* r;           /* [W][n] EF residuals, or NULL (no error feedback) */
+  void* theta;       /* [n] replica of the parameters (identical on all ranks) */
+  double lr;
+  psb_order order;
+  psb_topology topo; /* for PSB_ORDER_HIER; zeros = flat (devices_per_node = P) */
+  void* mean_out;    /* optional dense [n] aggregated mean (parity/debug) */
+} psb_step_desc;
+
+/* sync_data_parallel_step (strategies.hpp:86-121) across W local workers x
+ * nranks ranks (P = W * nranks, worker id = rank*W + w): per-worker EF
+ * compression, one exchange (NCCL allgather of payloads, or the dense 8-bit
+ * all-to-all + allgather for PSB_COMP_Q8), then the fused mean + SGD apply.
+ * theta is updated in place identically on every rank. */
+PSB_API psb_status psb_sync_step(psb_ctx* ctx, const psb_step_desc* d, psb_stream_t stream);
+
+/* One round of the bounded-staleness async loop (trainer.hpp:244-255) for the
+ * P workers: each worker's EF-compressed message is applied in worker order
+ * with scale lr/(1+tau_p), tau_p = min(*global_updates + p, p mod (s+1))
+ * where s = staleness_bound (s = 3 reproduces the reference's fixed pattern).
+ * *global_updates (host, in/out) advances by P. */
+PSB_API psb_status psb_async_round(psb_ctx* ctx, const psb_step_desc* d, uint32_t staleness_bound,
+                           uint64_t* global_updates, psb_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSB_H_ */

@@ -1,0 +1,280 @@
+// ref_shim.cpp -- extern "C" entry points into the UNMODIFIED reference headers.
+//
+// TEST INFRASTRUCTURE ONLY (see oracle/psb_oracle.c header).  This file holds
+// no reference source: it #includes the reference's own headers from the path
+// given on the command line (oracle/Makefile, REF_INCLUDE, default
+// /root/reference/proj/include) and exposes the hot-path functions over plain
+// pointers so tests/ and bench.py (reference arm, cpu_baseline) can call the
+// reference implementation itself.  Output: oracle/_ref/libparsim_ref.so.
+//
+// Functions wrapped (all in namespace parsim):
+//   compress_topk        parsim/compression.hpp:81-99
+//   compress_onebit      parsim/compression.hpp:67-77
+//   ef_compress_step     parsim/compression.hpp:146-157
+//   decompress           parsim/compression.hpp:113-142
+//   allreduce_mean       parsim/collectives.hpp:135-154
+//   sync_data_parallel_step  parsim/strategies.hpp:86-113
+//   async_step           parsim/strategies.hpp:125-129
+//   vec_axpy             parsim/numerics.hpp:70-78
+//   SeededRng            parsim/numerics.hpp:152-178
+
+#include <cstring>
+#include <exception>
+#include <thread>
+#include <vector>
+
+#include "parsim/collectives.hpp"
+#include "parsim/compression.hpp"
+#include "parsim/numerics.hpp"
+#include "parsim/strategies.hpp"
+
+using namespace parsim;
+
+namespace {
+thread_local char g_err[512];
+
+int fail_with(const std::exception& e) {
+  std::strncpy(g_err, e.what(), sizeof(g_err) - 1);
+  g_err[sizeof(g_err) - 1] = 0;
+  return 1;
+}
+
+CompressorConfig make_cfg(int kind, std::size_t k) {
+  CompressorConfig c;
+  c.kind = kind == 0 ? CompressorKind::none : (kind == 1 ? CompressorKind::onebit : CompressorKind::topk);
+  c.top_k = k;
+  return c;
+}
+
+CollectiveAlgorithm make_algo(int a) {
+  switch (a) {
+    case 0: return CollectiveAlgorithm::naive;
+    case 1: return CollectiveAlgorithm::ring;
+    case 2: return CollectiveAlgorithm::hierarchical;
+    default: return CollectiveAlgorithm::pipelined_ring;
+  }
+}
+
+Topology make_topo(std::size_t racks, std::size_t npr, std::size_t dpn) {
+  Topology t;
+  t.racks = racks;
+  t.nodes_per_rack = npr;
+  t.devices_per_node = dpn;
+  return t;
+}
+
+// Message -> flat outputs.  For top-k: idx/val arrays of length k.  For
+// onebit: sign bytes + scale.  For none: dense values in val.
+void export_msg(const CompressedGradient& m, std::uint64_t* idx, double* val, std::uint8_t* sign_bytes,
+                double* scale, std::size_t* count) {
+  if (auto* t = std::get_if<TopKPayload>(&m.payload)) {
+    for (std::size_t j = 0; j < t->indices.size(); ++j) {
+      if (idx) idx[j] = t->indices[j];
+      if (val) val[j] = t->values[j];
+    }
+    if (count) *count = t->indices.size();
+  } else if (auto* s = std::get_if<SignBitPayload>(&m.payload)) {
+    if (sign_bytes) std::memcpy(sign_bytes, s->sign_bytes.data(), s->sign_bytes.size());
+    if (scale) *scale = s->scale;
+    if (count) *count = s->sign_bytes.size();
+  } else {
+    auto& d = std::get<DensePayload>(m.payload);
+    if (val) std::memcpy(val, d.values.data(), d.values.size() * sizeof(double));
+    if (count) *count = d.values.size();
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err; }
+
+int ref_splitmix_stream(std::uint64_t seed, std::size_t n, std::uint64_t* out) {
+  SeededRng r(seed);
+  for (std::size_t i = 0; i < n; ++i) out[i] = r.next_u64();
+  return 0;
+}
+
+// SeededRng::uniform(lo, hi) stream, used to regenerate the reference tests'
+// own inputs (e.g. acceptance.cpp:133-170, test_compression.cpp:118-135).
+int ref_uniform_stream(std::uint64_t seed, std::size_t n, double lo, double hi, double* out) {
+  SeededRng r(seed);
+  for (std::size_t i = 0; i < n; ++i) out[i] = r.uniform(lo, hi);
+  return 0;
+}
+
+int ref_compress_topk(const double* g, std::size_t n, std::size_t k, std::uint64_t* idx, double* val) {
+  try {
+    DenseVector v(g, g + n);
+    export_msg(compress_topk(v, k), idx, val, nullptr, nullptr, nullptr);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
+}
+
+int ref_compress_onebit(const double* g, std::size_t n, std::uint8_t* sign_bytes, double* scale) {
+  try {
+    DenseVector v(g, g + n);
+    export_msg(compress_onebit(v), nullptr, nullptr, sign_bytes, scale, nullptr);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
+}
+
+// One ef_compress_step; residual is in/out.  kind: 0 none, 1 onebit, 2 topk.
+// Outputs: topk -> idx/val (k entries); onebit -> sign_bytes/scale; none -> val (n).
+int ref_ef_compress_step(int kind, std::size_t k, double* residual, const double* g, std::size_t n,
+                         std::uint64_t* idx, double* val, std::uint8_t* sign_bytes, double* scale) {
+  try {
+    ErrorFeedbackState st{DenseVector(residual, residual + n)};
+    DenseVector v(g, g + n);
+    auto msg = ef_compress_step(st, v, make_cfg(kind, k));
+    std::memcpy(residual, st.residual.data(), n * sizeof(double));
+    export_msg(msg, idx, val, sign_bytes, scale, nullptr);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
+}
+
+// bufs: P rows of n.  algo: 0 naive 1 ring 2 hierarchical 3 pipelined_ring.
+int ref_allreduce_mean(int algo, std::size_t P, const double* bufs, std::size_t n, std::size_t racks,
+                       std::size_t npr, std::size_t dpn, double* out) {
+  try {
+    WorkerGroup wg;
+    for (std::size_t p = 0; p < P; ++p) wg.buffers.emplace_back(bufs + p * n, bufs + (p + 1) * n);
+    DenseVector m = dpn == 0 ? allreduce_mean(wg, make_algo(algo))
+                             : allreduce_mean(wg, make_algo(algo), make_topo(racks, npr, dpn));
+    std::memcpy(out, m.data(), n * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
+}
+
+// sync_data_parallel_step.  params in/out.  residuals: P rows of n (in/out),
+// or nullptr for "no error-feedback state" (strategies.hpp:97-102).
+// dpn == 0 selects the no-topology overload (strategies.hpp:115-121).
+// threads > 1 runs the per-worker ef_compress_step calls of the step on
+// worker threads (SPEC.md:238 allows it; the fold stays serial), used only by
+// bench.py's reference arm as the "P cores" variant.
+int ref_sync_step(int kind, std::size_t k, int algo, std::size_t P, const double* grads, double* params,
+                  std::size_t n, double lr, double* residuals, std::size_t racks, std::size_t npr,
+                  std::size_t dpn) {
+  try {
+    WorkerGroup wg;
+    for (std::size_t p = 0; p < P; ++p) wg.buffers.emplace_back(grads + p * n, grads + (p + 1) * n);
+    DenseVector theta(params, params + n);
+    HyperParams h;
+    h.learning_rate = lr;
+    StrategyConfig cfg;
+    cfg.data_degree = P;
+    cfg.collective = make_algo(algo);
+    cfg.compressor = make_cfg(kind, k);
+    std::vector<ErrorFeedbackState> ef;
+    if (residuals) {
+      for (std::size_t p = 0; p < P; ++p)
+        ef.push_back(ErrorFeedbackState{DenseVector(residuals + p * n, residuals + (p + 1) * n)});
+    }
+    DenseVector out = dpn == 0
+                          ? sync_data_parallel_step(wg, theta, h, cfg, residuals ? &ef : nullptr)
+                          : sync_data_parallel_step(wg, theta, h, cfg, make_topo(racks, npr, dpn),
+                                                    residuals ? &ef : nullptr);
+    std::memcpy(params, out.data(), n * sizeof(double));
+    if (residuals) {
+      for (std::size_t p = 0; p < P; ++p)
+        std::memcpy(residuals + p * n, ef[p].residual.data(), n * sizeof(double));
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
+}
+
+// Same step with the P ef_compress_step calls spread over `threads` host
+// threads, then the reference's own decompress + allreduce_mean + vec_axpy,
+// serially, in the reference order (strategies.hpp:105-112).  Reference
+// functions only; this is the "all host threads" reference arm.
+int ref_sync_step_threaded(int kind, std::size_t k, int algo, std::size_t P, const double* grads,
+                           double* params, std::size_t n, double lr, double* residuals, int threads) {
+  try {
+    std::vector<ErrorFeedbackState> ef(P);
+    std::vector<CompressedGradient> msgs(P);
+    for (std::size_t p = 0; p < P; ++p)
+      ef[p].residual.assign(residuals + p * n, residuals + (p + 1) * n);
+    CompressorConfig cc = make_cfg(kind, k);
+    std::vector<std::thread> pool;
+    std::vector<std::string> errs(P);
+    int T = threads < 1 ? 1 : threads;
+    for (int t = 0; t < T; ++t) {
+      pool.emplace_back([&, t]() {
+        for (std::size_t p = (std::size_t)t; p < P; p += (std::size_t)T) {
+          try {
+            DenseVector g(grads + p * n, grads + (p + 1) * n);
+            msgs[p] = ef_compress_step(ef[p], g, cc);
+          } catch (const std::exception& e) {
+            errs[p] = e.what();
+          }
+        }
+      });
+    }
+    for (auto& th : pool) th.join();
+    for (auto& e : errs)
+      if (!e.empty()) throw std::invalid_argument(e);
+    WorkerGroup dec;
+    for (std::size_t p = 0; p < P; ++p) dec.buffers.push_back(decompress(msgs[p]));
+    DenseVector mean = allreduce_mean(dec, make_algo(algo));
+    DenseVector theta(params, params + n);
+    DenseVector out = vec_axpy(-lr, mean, theta);
+    std::memcpy(params, out.data(), n * sizeof(double));
+    for (std::size_t p = 0; p < P; ++p)
+      std::memcpy(residuals + p * n, ef[p].residual.data(), n * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
+}
+
+int ref_async_step(const double* params, const double* g, std::size_t n, std::size_t tau, double eta,
+                   double* out) {
+  try {
+    DenseVector t(params, params + n), gg(g, g + n);
+    DenseVector o = async_step(t, gg, tau, eta);
+    std::memcpy(out, o.data(), n * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
+}
+
+int ref_vec_axpy(double a, const double* x, const double* y, std::size_t n, double* out) {
+  try {
+    DenseVector xx(x, x + n), yy(y, y + n);
+    DenseVector o = vec_axpy(a, xx, yy);
+    std::memcpy(out, o.data(), n * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
+}
+
+// decompress of a top-k payload (compression.hpp:113-142), including its
+// validation (out-of-range / unsorted indices -> invalid_argument).
+int ref_decompress_topk(std::size_t dim, const std::uint64_t* idx, const double* val, std::size_t k,
+                        double* out) {
+  try {
+    TopKPayload t;
+    t.dim = dim;
+    t.indices.assign(idx, idx + k);
+    t.values.assign(val, val + k);
+    DenseVector o = decompress(CompressedGradient{t});
+    std::memcpy(out, o.data(), dim * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
+}
+
+}  // extern "C"

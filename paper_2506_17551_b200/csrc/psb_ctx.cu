@@ -1,0 +1,465 @@
+// psb_ctx.cu -- context, communicator, argument checks and step drivers.
+//
+// Step drivers replace the reference's data-parallel step functions:
+//   psb_sync_step   <- sync_data_parallel_step  parsim/strategies.hpp:86-121
+//   psb_async_round <- async branch of train     parsim/trainer.hpp:244-255
+//                      (+ async_step             parsim/strategies.hpp:125-129)
+// P = W local virtual workers x R ranks (one process per GPU, NCCL over
+// NVLink/NVSwitch).  Worker id = rank*W + w, so the reference's canonical
+// worker order is preserved across ranks.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "psb_internal.cuh"
+
+psb_status psb_q8_quant_launch(psb_ctx* c, const float* x, float* r, size_t n, uint32_t B,
+                               int8_t* codes, float* scales, cudaStream_t st);
+psb_status psb_q8_reduce_launch(psb_ctx* c, const int8_t* wcodes, size_t wstride,
+                                const float* wscales, size_t sstride, int P, size_t blk_lo,
+                                size_t blk_hi, size_t n, uint32_t B, psb_order order, uint32_t dpn,
+                                uint32_t npr, int8_t* mcodes, float* mscales, double lr,
+                                float* theta, float* mean_out, cudaStream_t st);
+psb_status psb_q8_apply_launch(psb_ctx* c, const int8_t* mcodes, const float* mscales, size_t n,
+                               uint32_t B, double lr, float* theta, float* mean_out,
+                               cudaStream_t st);
+
+psb_status psb_set_err(psb_ctx* c, psb_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+psb_status psb_cuda_err(psb_ctx* c, cudaError_t e, const char* where) {
+  if (c) c->err = std::string(where) + ": " + cudaGetErrorString(e);
+  return PSB_ECUDA;
+}
+
+#define CUDA_TRY(c, expr, where)                                  \
+  do {                                                            \
+    cudaError_t e__ = (expr);                                     \
+    if (e__ != cudaSuccess) return psb_cuda_err((c), e__, where); \
+  } while (0)
+
+#define NCCL_TRY(c, expr, where)                                                        \
+  do {                                                                                  \
+    ncclResult_t r__ = (expr);                                                          \
+    if (r__ != ncclSuccess)                                                             \
+      return psb_set_err((c), PSB_ENCCL, std::string(where) + ": " + ncclGetErrorString(r__)); \
+  } while (0)
+
+extern "C" int psb_abi_version(void) { return PSB_ABI_VERSION; }
+
+extern "C" const char* psb_status_string(psb_status s) {
+  switch (s) {
+    case PSB_OK: return "ok";
+    case PSB_EINVAL: return "invalid argument";
+    case PSB_ENONFINITE: return "non-finite entry";
+    case PSB_ECUDA: return "cuda error";
+    case PSB_ENCCL: return "nccl error";
+    case PSB_ENOMEM: return "out of device memory";
+    case PSB_ESTATE: return "invalid ctx state";
+  }
+  return "unknown";
+}
+
+extern "C" size_t psb_payload_bytes(psb_compressor c, psb_dtype dt, size_t k) {
+  if (c == PSB_COMP_TOPK) return psb_align16(k * 4) + psb_align16(k * (dt == PSB_F64 ? 8 : 4));
+  if (c == PSB_COMP_TOPK_Q8) return psb_align16(k * 4) + psb_align16(k) + psb_align16(((k + 127) / 128) * 4);
+  return 0;
+}
+
+static size_t tile_f64() { return (size_t)PSB_SCAN_THREADS * 4 * 2; }
+
+extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, size_t max_k,
+                                     int max_workers) {
+  if (!out) return PSB_EINVAL;
+  *out = nullptr;
+  if (max_n < 1 || max_n >= (1ull << 32) || max_k > max_n || max_workers < 1 ||
+      max_workers > PSB_MAX_P)
+    return PSB_EINVAL;
+  psb_ctx* c = new psb_ctx();
+  c->device = device;
+  c->max_n = max_n;
+  c->max_k = max_k < 1 ? 1 : max_k;
+  c->max_workers = max_workers;
+  auto fail = [&](cudaError_t e) {
+    psb_ctx_destroy(c);
+    return e == cudaErrorMemoryAllocation ? PSB_ENOMEM : PSB_ECUDA;
+  };
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(e);
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  // f32 tiles are 4096 elements, f64 tiles 2048: size for the larger count.
+  const size_t ntiles = (max_n + tile_f64() - 1) / tile_f64() + 1;
+  const size_t stage_cap = ntiles * tile_f64();
+#define ALLOC(ptr, bytes)                                   \
+  do {                                                      \
+    e = cudaMalloc((void**)&(ptr), (bytes));                \
+    if (e != cudaSuccess) return fail(e);                   \
+    e = cudaMemset((ptr), 0, (bytes));                      \
+    if (e != cudaSuccess) return fail(e);                   \
+  } while (0)
+  ALLOC(c->d_flags, 64);
+  ALLOC(c->d_tk, sizeof(TopkScratch));
+  ALLOC(c->d_tw, sizeof(TopkWorker) * max_workers);
+  ALLOC(c->d_hist1, sizeof(uint32_t) * PSB_HIST_BINS);
+  ALLOC(c->d_histr, sizeof(uint32_t) * PSB_HIST_BINS);
+  ALLOC(c->d_tile_cnt, sizeof(uint32_t) * ntiles);
+  ALLOC(c->d_tile_gt, sizeof(uint32_t) * ntiles);
+  ALLOC(c->d_tile_eq, sizeof(uint32_t) * ntiles);
+  ALLOC(c->d_stage_idx, sizeof(uint32_t) * stage_cap);
+  c->stage_val_bytes = sizeof(double) * stage_cap;
+  ALLOC(c->d_stage_val, c->stage_val_bytes);
+  // segment table: smallest segment is 64 entries (P*S*8 + 4S <= 96 KB, P <= 32)
+  c->seg_cap = (size_t)max_workers * (max_n / 64 + 2);
+  ALLOC(c->d_seg_off, sizeof(uint32_t) * c->seg_cap);
+  c->partials_cap = (size_t)c->num_sms * 4 + 64;
+  ALLOC(c->d_partials, sizeof(double) * (c->partials_cap + 1));
+#undef ALLOC
+  *out = c;
+  return PSB_OK;
+}
+
+extern "C" void psb_ctx_destroy(psb_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  void* ptrs[] = {c->d_flags,    c->d_tk,        c->d_tw,        c->d_hist1,   c->d_histr,
+                  c->d_tile_cnt, c->d_tile_gt,   c->d_tile_eq,   c->d_stage_idx, c->d_stage_val,
+                  c->d_seg_off,  c->d_partials,  c->d_gather,    c->d_work,    c->d_qmean};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+}
+
+extern "C" const char* psb_last_error(const psb_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
+
+extern "C" uint64_t psb_launch_count(const psb_ctx* c) { return c ? c->launches : 0; }
+
+extern "C" psb_status psb_check(psb_ctx* c, psb_stream_t stream) {
+  if (!c) return PSB_EINVAL;
+  CUDA_TRY(c, cudaStreamSynchronize((cudaStream_t)stream), "psb_check");
+  uint32_t flags = 0;
+  CUDA_TRY(c, cudaMemcpy(&flags, c->d_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost), "psb_check");
+  if (c->comm) {
+    ncclResult_t ae = ncclSuccess;
+    ncclCommGetAsyncError(c->comm, &ae);
+    if (ae != ncclSuccess && ae != ncclInProgress)
+      return psb_set_err(c, PSB_ENCCL, std::string("nccl async: ") + ncclGetErrorString(ae));
+  }
+  if (flags) {
+    CUDA_TRY(c, cudaMemset(c->d_flags, 0, sizeof(uint32_t)), "psb_check");
+    if (flags & 2u) return psb_set_err(c, PSB_EINVAL, "decompress: index out of range for dim");
+    if (flags & 4u) return psb_set_err(c, PSB_EINVAL, "decompress: indices not strictly increasing");
+    return psb_set_err(c, PSB_ENONFINITE, "ef_compress_step residual: non-finite entry");
+  }
+  return PSB_OK;
+}
+
+// -------------------------------------------------------------- communicator
+extern "C" psb_status psb_comm_unique_id(void* uid_out) {
+  if (!uid_out) return PSB_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return PSB_ENCCL;
+  std::memcpy(uid_out, &id, sizeof(id));
+  return PSB_OK;
+}
+
+extern "C" psb_status psb_comm_init(psb_ctx* c, int rank, int nranks, const void* uid) {
+  PSB_REQUIRE(c, c != nullptr, "null ctx");
+  PSB_REQUIRE(c, nranks >= 1 && rank >= 0 && rank < nranks, "psb_comm_init: bad rank/size");
+  c->rank = rank;
+  c->nranks = nranks;
+  if (nranks == 1) return PSB_OK;
+  PSB_REQUIRE(c, uid != nullptr, "psb_comm_init: null unique id");
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  CUDA_TRY(c, cudaSetDevice(c->device), "psb_comm_init");
+  NCCL_TRY(c, ncclCommInitRank(&c->comm, nranks, id, rank), "ncclCommInitRank");
+  return PSB_OK;
+}
+
+extern "C" int psb_comm_rank(const psb_ctx* c) { return c ? c->rank : -1; }
+extern "C" int psb_comm_size(const psb_ctx* c) { return c ? c->nranks : -1; }
+
+extern "C" psb_status psb_allgather(psb_ctx* c, void* buf, size_t bytes_per_rank, psb_stream_t stream) {
+  PSB_REQUIRE(c, c != nullptr, "null ctx");
+  if (c->nranks == 1) return PSB_OK;
+  if (!c->comm) return psb_set_err(c, PSB_ESTATE, "psb_allgather: communicator not initialised");
+  uint8_t* b = reinterpret_cast<uint8_t*>(buf);
+  NCCL_TRY(c, ncclAllGather(b + (size_t)c->rank * bytes_per_rank, b, bytes_per_rank, ncclUint8, c->comm,
+                            (cudaStream_t)stream),
+           "ncclAllGather");
+  return PSB_OK;
+}
+
+// ------------------------------------------------------------ compressors
+static psb_status ensure(psb_ctx* c, void** p, size_t* have, size_t need, const char* what) {
+  if (*have >= need) return PSB_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *have = 0;
+  cudaError_t e = cudaMalloc(p, need);
+  if (e != cudaSuccess) return psb_set_err(c, PSB_ENOMEM, std::string(what) + ": out of device memory");
+  *have = need;
+  return PSB_OK;
+}
+
+extern "C" psb_status psb_ef_topk(psb_ctx* c, psb_dtype dt, int worker, const void* g, void* r,
+                                  size_t n, size_t k, uint32_t* idx_out, void* val_out,
+                                  psb_stream_t stream) {
+  PSB_REQUIRE(c, c != nullptr, "null ctx");
+  PSB_REQUIRE(c, dt == PSB_F32 || dt == PSB_F64, "psb_ef_topk: bad dtype");
+  PSB_REQUIRE(c, k >= 1 && k <= n,
+              "compress_topk: k out of range (k=" + std::to_string(k) + ", dim=" + std::to_string(n) + ")");
+  PSB_REQUIRE(c, n <= c->max_n, "ef_compress_step: n exceeds ctx max_n");
+  PSB_REQUIRE(c, worker >= 0 && worker < c->max_workers, "psb_ef_topk: worker out of range");
+  PSB_REQUIRE(c, g && idx_out && val_out, "psb_ef_topk: null pointer");
+  return psb_topk_run(c, dt, worker, g, r, n, k, idx_out, val_out, (cudaStream_t)stream);
+}
+
+extern "C" psb_status psb_ef_topk_q8(psb_ctx* c, int worker, const float* g, float* r, size_t n,
+                                     size_t k, uint32_t* idx_out, int8_t* codes_out,
+                                     float* scales_out, psb_stream_t stream) {
+  PSB_REQUIRE(c, c != nullptr, "null ctx");
+  PSB_REQUIRE(c, k >= 1 && k <= n,
+              "compress_topk: k out of range (k=" + std::to_string(k) + ", dim=" + std::to_string(n) + ")");
+  PSB_REQUIRE(c, n <= c->max_n && k <= c->max_k, "psb_ef_topk_q8: size exceeds ctx capacity");
+  PSB_REQUIRE(c, g && idx_out && codes_out && scales_out, "psb_ef_topk_q8: null pointer");
+  psb_status s = ensure(c, &c->d_work, &c->work_bytes, sizeof(float) * c->max_k, "topk_q8 values");
+  if (s) return s;
+  float* vals = reinterpret_cast<float*>(c->d_work);
+  s = psb_topk_run(c, PSB_F32, worker, g, r, n, k, idx_out, vals, (cudaStream_t)stream);
+  if (s) return s;
+  return psb_topk_q8_fix(c, nullptr, k, idx_out, vals, r, codes_out, scales_out, (cudaStream_t)stream);
+}
+
+// --------------------------------------------------------------- drivers
+static psb_status check_desc(psb_ctx* c, const psb_step_desc* d) {
+  PSB_REQUIRE(c, c != nullptr, "null ctx");
+  PSB_REQUIRE(c, d != nullptr, "null step descriptor");
+  PSB_REQUIRE(c, d->workers >= 1, "WorkerGroup: no workers");
+  PSB_REQUIRE(c, (size_t)d->workers * c->nranks <= (size_t)c->max_workers,
+              "sync_data_parallel_step: P exceeds ctx max_workers");
+  PSB_REQUIRE(c, d->n >= 1 && d->n <= c->max_n, "sync_data_parallel_step: n out of range for ctx");
+  PSB_REQUIRE(c, d->lr > 0.0, "HyperParams: learning_rate must be > 0");
+  PSB_REQUIRE(c, d->g && d->theta, "sync_data_parallel_step: null buffer");
+  if (d->compressor == PSB_COMP_TOPK || d->compressor == PSB_COMP_TOPK_Q8) {
+    PSB_REQUIRE(c, d->k >= 1 && d->k <= d->n,
+                "compress_topk: k out of range (k=" + std::to_string(d->k) + ", dim=" + std::to_string(d->n) + ")");
+    PSB_REQUIRE(c, d->k <= c->max_k, "sync_data_parallel_step: k exceeds ctx max_k");
+  }
+  if (d->compressor == PSB_COMP_TOPK_Q8 || d->compressor == PSB_COMP_Q8)
+    PSB_REQUIRE(c, d->dtype == PSB_F32, "8-bit compressors are f32 only");
+  if (d->topo.devices_per_node)
+    PSB_REQUIRE(c, d->topo.racks >= 1 && d->topo.nodes_per_rack >= 1, "Topology: counts must be >= 1");
+  return PSB_OK;
+}
+
+// Compress this rank's W workers into their payload slots of the gather
+// buffer and exchange; on return the gather buffer holds all P payloads.
+static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaStream_t st,
+                                      uint8_t** payloads_out) {
+  const int W = d->workers, P = W * c->nranks;
+  const size_t es = d->dtype == PSB_F64 ? 8 : 4;
+  const size_t blk = psb_payload_bytes(d->compressor, d->dtype, d->k);
+  psb_status s = ensure(c, &c->d_gather, &c->gather_bytes, blk * P, "payload gather buffer");
+  if (s) return s;
+  uint8_t* gb = reinterpret_cast<uint8_t*>(c->d_gather);
+  for (int w = 0; w < W; ++w) {
+    const int gid = c->rank * W + w;
+    uint8_t* slot = gb + (size_t)gid * blk;
+    const void* g = reinterpret_cast<const uint8_t*>(d->g) + (size_t)w * d->n * es;
+    void* r = d->r ? reinterpret_cast<uint8_t*>(d->r) + (size_t)w * d->n * es : nullptr;
+    uint32_t* idx = reinterpret_cast<uint32_t*>(slot);
+    if (d->compressor == PSB_COMP_TOPK) {
+      s = psb_topk_run(c, d->dtype, w, g, r, d->n, d->k, idx, slot + psb_align16(d->k * 4), st);
+    } else {
+      int8_t* codes = reinterpret_cast<int8_t*>(slot + psb_align16(d->k * 4));
+      float* scales = reinterpret_cast<float*>(slot + psb_align16(d->k * 4) + psb_align16(d->k));
+      s = psb_ef_topk_q8(c, w, (const float*)g, (float*)r, d->n, d->k, idx, codes, scales,
+                         (psb_stream_t)st);
+    }
+    if (s) return s;
+  }
+  if (c->nranks > 1) {
+    if (!c->comm) return psb_set_err(c, PSB_ESTATE, "sync step: communicator not initialised");
+    NCCL_TRY(c, ncclAllGather(gb + (size_t)c->rank * W * blk, gb, (size_t)W * blk, ncclUint8, c->comm, st),
+             "ncclAllGather(payloads)");
+  }
+  *payloads_out = gb;
+  return PSB_OK;
+}
+
+static psb_status q8_step(psb_ctx* c, const psb_step_desc* d, cudaStream_t st) {
+  const int W = d->workers, R = c->nranks, P = W * R;
+  const uint32_t B = d->q8_block ? d->q8_block : 256;
+  PSB_REQUIRE(c, B == 128 || B == 256 || B == 512 || B == 1024, "q8: block must be 128, 256, 512 or 1024");
+  const size_t n = d->n;
+  const size_t nb = (n + B - 1) / B;
+  const size_t nbs = (nb + R - 1) / R;           // blocks per shard
+  const size_t shard_elems = nbs * B;
+  const size_t n_pad = (size_t)R * shard_elems;  // >= n
+  // workspace: local codes W*n_pad | local scales W*R*nbs | recv codes P*shard | recv scales P*nbs
+  //            | mean codes n_pad | mean scales R*nbs   (each region 256-aligned)
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t o_lc = 0;
+  const size_t o_ls = o_lc + al((size_t)W * n_pad);
+  const size_t o_rc = o_ls + al(sizeof(float) * W * R * nbs);
+  const size_t o_rs = o_rc + al((size_t)P * shard_elems);
+  const size_t o_mc = o_rs + al(sizeof(float) * P * nbs);
+  const size_t o_ms = o_mc + al(n_pad);
+  const size_t total = o_ms + al(sizeof(float) * R * nbs);
+  psb_status s = ensure(c, &c->d_gather, &c->gather_bytes, total, "q8 workspace");
+  if (s) return s;
+  uint8_t* ws = reinterpret_cast<uint8_t*>(c->d_gather);
+  int8_t* lcodes = reinterpret_cast<int8_t*>(ws + o_lc);
+  float* lscales = reinterpret_cast<float*>(ws + o_ls);
+  int8_t* rcodes = reinterpret_cast<int8_t*>(ws + o_rc);
+  float* rscales = reinterpret_cast<float*>(ws + o_rs);
+  int8_t* mcodes = reinterpret_cast<int8_t*>(ws + o_mc);
+  float* mscales = reinterpret_cast<float*>(ws + o_ms);
+  uint32_t dpn, npr;
+  if (d->topo.devices_per_node == 0) {
+    dpn = (uint32_t)P;
+    npr = 1;
+  } else {
+    dpn = d->topo.devices_per_node;
+    npr = d->topo.nodes_per_rack;
+  }
+  for (int w = 0; w < W; ++w) {
+    const float* g = reinterpret_cast<const float*>(d->g) + (size_t)w * n;
+    float* r = d->r ? reinterpret_cast<float*>(d->r) + (size_t)w * n : nullptr;
+    s = psb_q8_quant_launch(c, g, r, n, B, lcodes + (size_t)w * n_pad, lscales + (size_t)w * R * nbs, st);
+    if (s) return s;
+  }
+  float* theta = reinterpret_cast<float*>(d->theta);
+  float* mean_out = reinterpret_cast<float*>(d->mean_out);
+  if (R == 1) {
+    return psb_q8_reduce_launch(c, lcodes, n_pad, lscales, (size_t)R * nbs, P, 0, nb, n, B, d->order,
+                                dpn, npr, mcodes, mscales, d->lr, theta, mean_out, st);
+  }
+  if (!c->comm) return psb_set_err(c, PSB_ESTATE, "q8 step: communicator not initialised");
+  // all-to-all of block shards: worker gid's shard q goes to rank q, slot gid
+  NCCL_TRY(c, ncclGroupStart(), "ncclGroupStart");
+  for (int peer = 0; peer < R; ++peer) {
+    for (int w = 0; w < W; ++w) {
+      const int gid_src = c->rank * W + w;  // my worker, sent to peer
+      NCCL_TRY(c, ncclSend(lcodes + (size_t)w * n_pad + (size_t)peer * shard_elems, shard_elems, ncclInt8,
+                           peer, c->comm, st), "ncclSend(codes)");
+      NCCL_TRY(c, ncclSend(lscales + (size_t)w * R * nbs + (size_t)peer * nbs, nbs, ncclFloat32, peer,
+                           c->comm, st), "ncclSend(scales)");
+      (void)gid_src;
+    }
+    for (int w = 0; w < W; ++w) {
+      const int gid = peer * W + w;  // peer's worker w, my shard
+      NCCL_TRY(c, ncclRecv(rcodes + (size_t)gid * shard_elems, shard_elems, ncclInt8, peer, c->comm, st),
+               "ncclRecv(codes)");
+      NCCL_TRY(c, ncclRecv(rscales + (size_t)gid * nbs, nbs, ncclFloat32, peer, c->comm, st),
+               "ncclRecv(scales)");
+    }
+  }
+  NCCL_TRY(c, ncclGroupEnd(), "ncclGroupEnd");
+  const size_t blk_lo = (size_t)c->rank * nbs;
+  const size_t blk_hi = std::min(nb, blk_lo + nbs);
+  s = psb_q8_reduce_launch(c, rcodes, shard_elems, rscales, nbs, P, blk_lo, blk_hi, n, B, d->order, dpn,
+                           npr, mcodes, mscales, d->lr, nullptr, nullptr, st);
+  if (s) return s;
+  NCCL_TRY(c, ncclGroupStart(), "ncclGroupStart");
+  NCCL_TRY(c, ncclAllGather(mcodes + blk_lo * B, mcodes, shard_elems, ncclInt8, c->comm, st),
+           "ncclAllGather(codes)");
+  NCCL_TRY(c, ncclAllGather(mscales + blk_lo, mscales, nbs, ncclFloat32, c->comm, st),
+           "ncclAllGather(scales)");
+  NCCL_TRY(c, ncclGroupEnd(), "ncclGroupEnd");
+  return psb_q8_apply_launch(c, mcodes, mscales, n, B, d->lr, theta, mean_out, st);
+}
+
+extern "C" psb_status psb_sync_step(psb_ctx* c, const psb_step_desc* d, psb_stream_t stream) {
+  psb_status s = check_desc(c, d);
+  if (s) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int W = d->workers, P = W * c->nranks;
+  const size_t es = d->dtype == PSB_F64 ? 8 : 4;
+  switch (d->compressor) {
+    case PSB_COMP_TOPK:
+    case PSB_COMP_TOPK_Q8: {
+      uint8_t* pl = nullptr;
+      s = compress_and_gather(c, d, st, &pl);
+      if (s) return s;
+      return psb_sparse_mean_sgd(c, d->compressor, d->dtype, P, pl, d->k, d->order, &d->topo, d->lr,
+                                 d->theta, d->n, d->mean_out, stream);
+    }
+    case PSB_COMP_ONEBIT: {
+      const size_t nw = (d->n + 31) / 32;
+      const size_t words_bytes = (sizeof(uint32_t) * nw * P + 255) & ~(size_t)255;
+      s = ensure(c, &c->d_gather, &c->gather_bytes, words_bytes + sizeof(double) * P, "onebit buffers");
+      if (s) return s;
+      uint32_t* words = reinterpret_cast<uint32_t*>(c->d_gather);
+      double* scales = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(c->d_gather) + words_bytes);
+      for (int w = 0; w < W; ++w) {
+        const int gid = c->rank * W + w;
+        const void* g = reinterpret_cast<const uint8_t*>(d->g) + (size_t)w * d->n * es;
+        void* r = d->r ? reinterpret_cast<uint8_t*>(d->r) + (size_t)w * d->n * es : nullptr;
+        s = psb_ef_onebit(c, d->dtype, g, r, d->n, words + (size_t)gid * nw, scales + gid, stream);
+        if (s) return s;
+      }
+      if (c->nranks > 1) {
+        if (!c->comm) return psb_set_err(c, PSB_ESTATE, "sync step: communicator not initialised");
+        NCCL_TRY(c, ncclGroupStart(), "ncclGroupStart");
+        NCCL_TRY(c, ncclAllGather(words + (size_t)c->rank * W * nw, words, (size_t)W * nw, ncclUint32,
+                                  c->comm, st), "ncclAllGather(sign words)");
+        NCCL_TRY(c, ncclAllGather(scales + (size_t)c->rank * W, scales, (size_t)W, ncclFloat64, c->comm, st),
+                 "ncclAllGather(scales)");
+        NCCL_TRY(c, ncclGroupEnd(), "ncclGroupEnd");
+      }
+      return psb_onebit_mean_sgd(c, d->dtype, P, words, scales, d->order, &d->topo, d->lr, d->theta,
+                                 d->n, d->mean_out, stream);
+    }
+    case PSB_COMP_NONE: {
+      // no compression: allreduce_mean of the raw buffers (strategies.hpp:94-95);
+      // exact reference order requires all P dense buffers -> allgather them.
+      const void* bufs = d->g;
+      if (c->nranks > 1) {
+        s = ensure(c, &c->d_gather, &c->gather_bytes, es * d->n * P, "dense gather buffer");
+        if (s) return s;
+        uint8_t* gb = reinterpret_cast<uint8_t*>(c->d_gather);
+        CUDA_TRY(c, cudaMemcpyAsync(gb + (size_t)c->rank * W * d->n * es, d->g, (size_t)W * d->n * es,
+                                    cudaMemcpyDeviceToDevice, st), "dense copy");
+        if (!c->comm) return psb_set_err(c, PSB_ESTATE, "sync step: communicator not initialised");
+        NCCL_TRY(c, ncclAllGather(gb + (size_t)c->rank * W * d->n * es, gb, (size_t)W * d->n * es, ncclUint8,
+                                  c->comm, st), "ncclAllGather(dense)");
+        bufs = gb;
+      }
+      return psb_dense_mean_sgd(c, d->dtype, P, bufs, d->order, &d->topo, d->lr, d->theta, d->n,
+                                d->mean_out, stream);
+    }
+    case PSB_COMP_Q8:
+      return q8_step(c, d, st);
+  }
+  return psb_set_err(c, PSB_EINVAL, "compress: unknown compressor kind");
+}
+
+extern "C" psb_status psb_async_round(psb_ctx* c, const psb_step_desc* d, uint32_t staleness_bound,
+                                      uint64_t* global_updates, psb_stream_t stream) {
+  psb_status s = check_desc(c, d);
+  if (s) return s;
+  PSB_REQUIRE(c, global_updates != nullptr, "psb_async_round: null global_updates");
+  PSB_REQUIRE(c, d->compressor == PSB_COMP_TOPK || d->compressor == PSB_COMP_TOPK_Q8,
+              "psb_async_round: sparse compressors only");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int P = d->workers * c->nranks;
+  uint8_t* pl = nullptr;
+  s = compress_and_gather(c, d, st, &pl);
+  if (s) return s;
+  std::vector<double> scale(P);
+  const uint64_t g0 = *global_updates;
+  for (int p = 0; p < P; ++p) {
+    const uint64_t bound = (uint64_t)staleness_bound + 1;
+    const uint64_t tau = std::min<uint64_t>(g0 + (uint64_t)p, (uint64_t)p % bound);
+    scale[p] = d->lr / (1.0 + (double)tau);  // strategies.hpp:127
+  }
+  s = psb_sparse_async_apply(c, d->compressor, d->dtype, P, pl, d->k, scale.data(), d->theta, d->n, stream);
+  if (s) return s;
+  *global_updates = g0 + (uint64_t)P;
+  return PSB_OK;
+}

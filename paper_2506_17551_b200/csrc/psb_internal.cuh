@@ -1,0 +1,174 @@
+// psb_internal.cuh -- shared definitions for the sm_100a gradient-path kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+
+#include "psb.h"
+
+#define PSB_MAX_P 32          // payloads folded per apply (worker mask is u32)
+#define PSB_HIST_BINS 4096    // widest radix digit (12 bits)
+#define PSB_SCAN_THREADS 256  // K1 scan CTA size
+#define PSB_ITEMS 16          // elements per thread per K1 tile (f32)
+
+// ------------------------------------------------------------------ K1 state
+// Per-call scratch of the top-k selection (reset by k_topk_begin every call).
+struct TopkScratch {
+  uint32_t done[8];         // last-block counters (one per kernel role)
+  uint32_t b1;              // level-1 digit of the k-th largest key
+  uint32_t need_full_hist;  // predicted candidate set missed -> full histogram pass
+  uint32_t need_compact;    // candidates must be compacted by a separate pass
+  uint32_t nonfinite;
+  unsigned long long prefix;  // key digits resolved so far
+  unsigned long long need;    // entries still to take inside `prefix`
+  unsigned long long match;   // entries matching `prefix`
+  unsigned long long n;
+  unsigned long long k;
+  uint32_t g_used;            // predicted level-1 digit used by this call
+  uint32_t pad;
+};
+
+// Per-worker persistent selection history.
+struct TopkWorker {
+  uint32_t g_pred;  // level-1 digit predicted for the next call (0 = none)
+  uint32_t calls;
+};
+
+struct psb_ctx {
+  int device = 0;
+  int num_sms = 148;
+  size_t max_n = 0, max_k = 0;
+  int max_workers = 1;
+  std::string err;
+  uint64_t launches = 0;
+  // comm
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  // flags
+  uint32_t* d_flags = nullptr;  // [0] nonfinite
+  // K1 scratch
+  TopkScratch* d_tk = nullptr;
+  TopkWorker* d_tw = nullptr;
+  uint32_t* d_hist1 = nullptr;   // level-1 histogram
+  uint32_t* d_histr = nullptr;   // refine-level histogram
+  uint32_t* d_tile_cnt = nullptr;
+  uint32_t* d_tile_gt = nullptr;
+  uint32_t* d_tile_eq = nullptr;
+  uint32_t* d_stage_idx = nullptr;  // candidate staging, tile-segmented, capacity max_n
+  void* d_stage_val = nullptr;      // f64 capacity
+  size_t stage_val_bytes = 0;
+  // apply scratch
+  uint32_t* d_seg_off = nullptr;  // [max_workers][nseg_max + 1]
+  size_t seg_cap = 0;
+  // onebit / q8 scratch
+  double* d_partials = nullptr;
+  size_t partials_cap = 0;
+  // exchange buffers (payload gather, q8 shards)
+  void* d_gather = nullptr;
+  size_t gather_bytes = 0;
+  void* d_work = nullptr;  // generic workspace
+  size_t work_bytes = 0;
+  float* d_qmean = nullptr;
+};
+
+// ------------------------------------------------------------------- helpers
+psb_status psb_set_err(psb_ctx* c, psb_status s, const std::string& msg);
+psb_status psb_cuda_err(psb_ctx* c, cudaError_t e, const char* where);
+
+#define PSB_REQUIRE(ctx, cond, msg)                                      \
+  do {                                                                   \
+    if (!(cond)) return psb_set_err((ctx), PSB_EINVAL, (msg));           \
+  } while (0)
+
+#define PSB_LAUNCH_CHECK(ctx, where)                                     \
+  do {                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                 \
+    if (e_ != cudaSuccess) return psb_cuda_err((ctx), e_, (where));      \
+  } while (0)
+
+static inline size_t psb_align16(size_t b) { return (b + 15) & ~(size_t)15; }
+
+// Key of |x|: the magnitude bits, monotone in |x| for finite values and +-0
+// (SURVEY.md parity fact 1).
+template <class T>
+struct KeyOf;
+template <>
+struct KeyOf<float> {
+  typedef uint32_t K;
+  static constexpr int kLevels = 3;
+  __device__ __forceinline__ static K key(float x) { return __float_as_uint(x) & 0x7fffffffu; }
+  __host__ __device__ static constexpr int shift(int l) { return l == 0 ? 19 : (l == 1 ? 8 : 0); }
+  __host__ __device__ static constexpr int width(int l) { return l == 0 ? 12 : (l == 1 ? 11 : 8); }
+  static constexpr K kInf = 0x7f800000u;
+};
+template <>
+struct KeyOf<double> {
+  typedef unsigned long long K;
+  static constexpr int kLevels = 6;
+  __device__ __forceinline__ static K key(double x) {
+    return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffULL;
+  }
+  __host__ __device__ static constexpr int shift(int l) {
+    return l == 0 ? 51 : (l == 1 ? 39 : (l == 2 ? 27 : (l == 3 ? 15 : (l == 4 ? 3 : 0))));
+  }
+  __host__ __device__ static constexpr int width(int l) { return l == 5 ? 3 : 12; }
+  static constexpr K kInf = 0x7ff0000000000000ULL;
+};
+
+// IEEE round-to-nearest arithmetic without contraction, per type.
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ bool is_finite(float x) {
+  return (__float_as_uint(x) & 0x7f800000u) != 0x7f800000u;
+}
+__device__ __forceinline__ bool is_finite(double x) {
+  return ((unsigned long long)__double_as_longlong(x) & 0x7ff0000000000000ULL) !=
+         0x7ff0000000000000ULL;
+}
+
+// Block-wide exclusive scan of u64 over PSB_SCAN_THREADS threads.  Returns the
+// exclusive prefix; *total receives the block total.
+__device__ __forceinline__ unsigned long long block_exscan_u64(unsigned long long v,
+                                                              unsigned long long* sh_warp,
+                                                              unsigned long long* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh_warp[wid] = x;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  if (wid == 0) {
+    unsigned long long w = lane < nw ? sh_warp[lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) sh_warp[lane] = w;  // inclusive warp-total prefix
+  }
+  __syncthreads();
+  unsigned long long warp_excl = wid ? sh_warp[wid - 1] : 0ull;
+  *total = sh_warp[nw - 1];
+  unsigned long long r = warp_excl + x - v;
+  __syncthreads();
+  return r;
+}
+
+// Launch helpers defined in the .cu files.
+psb_status psb_topk_run(psb_ctx* c, psb_dtype dt, int worker, const void* g, void* r, size_t n,
+                        size_t k, uint32_t* idx_out, void* val_out, cudaStream_t st);
+psb_status psb_topk_q8_fix(psb_ctx* c, const float* r_unused, size_t k, const uint32_t* idx,
+                           const float* vals, float* r, int8_t* codes, float* scales,
+                           cudaStream_t st);

@@ -1,0 +1,289 @@
+// psb_q8.cu -- 8-bit per-block quantizer and the dense 8-bit all-reduce.
+//
+// NO REFERENCE CODE: multi-bit quantization is a non-goal of the reference
+// (SPEC.md:182); the rule implemented here is specified, and restated on the
+// CPU, in oracle/psb_oracle.c:orc_q8_quant:
+//   per block of B consecutive elements: scale = absmax / 127  (IEEE f32 div)
+//   code = clamp(rint(p / scale), -127, 127)  (IEEE div, round-half-even), 0 if scale == 0
+//   xhat = code * scale;  error feedback r' = p - xhat (compression.hpp:153-154 shape)
+// One warp per block, float4 loads, char4 code stores (128-bit per 4 lanes).
+//
+// Dense 8-bit "hierarchical" all-reduce (cfg3), P = W local workers x R ranks:
+//   1. quantize each local worker's p = r + g          (k_q8_quant)
+//   2. all-to-all of int8 shards + scales (NCCL grouped send/recv): rank q
+//      receives block-shard q of every worker
+//   3. k_q8_reduce: fold the P dequantized values in the configured
+//      reference order (collectives.hpp:68-128), * (1/P), requantize the mean
+//      per block; with R == 1 also apply SGD in the same pass
+//   4. NCCL allgather of the requantized shards
+//   5. k_q8_apply: theta = (-lr) * (code*scale) + theta (no FMA)
+#include "psb_fold.cuh"
+
+namespace {
+
+__device__ __forceinline__ int q8_code(float p, float scale) {
+  if (!(scale > 0.f)) return 0;
+  int q = __float2int_rn(__fdiv_rn(p, scale));
+  return q > 127 ? 127 : (q < -127 ? -127 : q);
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(256) k_q8_quant(const float* __restrict__ x, float* __restrict__ r,
+                                                  size_t n, int8_t* __restrict__ codes,
+                                                  float* __restrict__ scales, uint32_t* flags) {
+  constexpr int B = VPL * 128;
+  const int lane = threadIdx.x & 31;
+  const size_t nb = (n + B - 1) / B;
+  const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  const bool vec_ok = ((((uintptr_t)x) | ((uintptr_t)r) | ((uintptr_t)codes)) & 15) == 0;
+  bool bad = false;
+  for (size_t blk = warp; blk < nb; blk += nwarps) {
+    const size_t lo = blk * B;
+    const bool full = vec_ok && lo + B <= n;
+    float p[VPL][4];
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+      const size_t e = lo + (size_t)it * 128 + lane * 4;
+      if (full) {
+        const float4 xv = __ldcs(reinterpret_cast<const float4*>(x + e));
+        if (r) {
+          const float4 rv = *reinterpret_cast<const float4*>(r + e);
+          p[it][0] = __fadd_rn(rv.x, xv.x);
+          p[it][1] = __fadd_rn(rv.y, xv.y);
+          p[it][2] = __fadd_rn(rv.z, xv.z);
+          p[it][3] = __fadd_rn(rv.w, xv.w);
+        } else {
+          p[it][0] = xv.x; p[it][1] = xv.y; p[it][2] = xv.z; p[it][3] = xv.w;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const size_t ei = e + c;
+          p[it][c] = ei < n ? (r ? __fadd_rn(r[ei], x[ei]) : x[ei]) : 0.f;
+        }
+      }
+    }
+    float amax = 0.f;
+#pragma unroll
+    for (int it = 0; it < VPL; ++it)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        amax = fmaxf(amax, fabsf(p[it][c]));
+        bad |= !is_finite(p[it][c]);
+      }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const float scale = __fdiv_rn(amax, 127.0f);
+    if (lane == 0) scales[blk] = scale;
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+      const size_t e = lo + (size_t)it * 128 + lane * 4;
+      int q[4];
+      float res[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        q[c] = q8_code(p[it][c], scale);
+        res[c] = __fsub_rn(p[it][c], __fmul_rn((float)q[c], scale));
+      }
+      if (full) {
+        char4 cv = make_char4((signed char)q[0], (signed char)q[1], (signed char)q[2], (signed char)q[3]);
+        *reinterpret_cast<char4*>(codes + e) = cv;
+        if (r) *reinterpret_cast<float4*>(r + e) = make_float4(res[0], res[1], res[2], res[3]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (e + c < n) {
+            codes[e + c] = (int8_t)q[c];
+            if (r) r[e + c] = res[c];
+          }
+        }
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1u);
+}
+
+__global__ void k_q8_dequant(const int8_t* __restrict__ codes, const float* __restrict__ scales,
+                             size_t n, uint32_t B, float* __restrict__ out) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    out[i] = __fmul_rn((float)codes[i], scales[i / B]);
+}
+
+// Fold P workers' dequantized values over blocks [blk_lo, blk_hi) (global block
+// ids), requantize the mean per block into (mcodes, mscales) at global offsets,
+// and, when theta != nullptr, apply SGD directly (single-rank path).
+// Worker q's codes for global element e live at wcodes + q*wstride + (e - e_base),
+// scales at wscales + q*sstride + (blk - blk_lo).
+template <int VPL>
+__global__ void __launch_bounds__(256) k_q8_reduce(
+    const int8_t* __restrict__ wcodes, size_t wstride, const float* __restrict__ wscales,
+    size_t sstride, int P, size_t blk_lo, size_t blk_hi, size_t n, int order, uint32_t dpn,
+    uint32_t npr, int8_t* __restrict__ mcodes, float* __restrict__ mscales, float coef,
+    float* __restrict__ theta, float* __restrict__ mean_out, uint32_t* flags) {
+  constexpr int B = VPL * 128;
+  const int lane = threadIdx.x & 31;
+  const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  const size_t e_base = blk_lo * B;
+  const float inv = (float)(1.0 / (double)P);
+  bool bad = false;
+  for (size_t blk = blk_lo + warp; blk < blk_hi; blk += nwarps) {
+    float m[VPL][4];
+    float amax = 0.f;
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const size_t e = blk * B + (size_t)it * 128 + lane * 4 + c;
+        float mean = 0.f;
+        if (e < n) {
+          auto get = [&](int q) -> float {
+            const int8_t code = wcodes[(size_t)q * wstride + (e - e_base)];
+            const float sc = wscales[(size_t)q * sstride + (blk - blk_lo)];
+            return __fmul_rn((float)code, sc);
+          };
+          mean = __fmul_rn(fold_sum<float>(get, P, order, e, n, dpn, npr), inv);
+        }
+        m[it][c] = mean;
+        amax = fmaxf(amax, fabsf(mean));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const float scale = __fdiv_rn(amax, 127.0f);
+    if (lane == 0) mscales[blk] = scale;
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const size_t e = blk * B + (size_t)it * 128 + lane * 4 + c;
+        if (e >= n) continue;
+        const int q = q8_code(m[it][c], scale);
+        mcodes[e] = (int8_t)q;
+        if (theta) {
+          const float mhat = __fmul_rn((float)q, scale);
+          const float th = __fadd_rn(__fmul_rn(coef, mhat), theta[e]);
+          theta[e] = th;
+          if (mean_out) mean_out[e] = mhat;
+          bad |= !is_finite(th);
+        }
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1u);
+}
+
+__global__ void __launch_bounds__(256) k_q8_apply(const int8_t* __restrict__ mcodes,
+                                                  const float* __restrict__ mscales, size_t n,
+                                                  uint32_t B, float coef, float* __restrict__ theta,
+                                                  float* __restrict__ mean_out, uint32_t* flags) {
+  bool bad = false;
+  const size_t nv = n / 4;
+  const bool vec_ok = ((((uintptr_t)mcodes) | ((uintptr_t)theta)) & 15) == 0 && !mean_out;
+  if (vec_ok) {
+    for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv;
+         v += (size_t)gridDim.x * blockDim.x) {
+      const size_t e = v * 4;
+      const char4 cv = *reinterpret_cast<const char4*>(mcodes + e);
+      const float sc = mscales[e / B];
+      float4 th = *reinterpret_cast<float4*>(theta + e);
+      th.x = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.x, sc)), th.x);
+      th.y = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.y, sc)), th.y);
+      th.z = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.z, sc)), th.z);
+      th.w = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.w, sc)), th.w);
+      *reinterpret_cast<float4*>(theta + e) = th;
+      bad |= !is_finite(th.x) || !is_finite(th.y) || !is_finite(th.z) || !is_finite(th.w);
+    }
+    for (size_t e = nv * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (size_t)gridDim.x * blockDim.x) {
+      const float th = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)mcodes[e], mscales[e / B])), theta[e]);
+      theta[e] = th;
+      bad |= !is_finite(th);
+    }
+  } else {
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (size_t)gridDim.x * blockDim.x) {
+      const float mhat = __fmul_rn((float)mcodes[e], mscales[e / B]);
+      const float th = __fadd_rn(__fmul_rn(coef, mhat), theta[e]);
+      theta[e] = th;
+      if (mean_out) mean_out[e] = mhat;
+      bad |= !is_finite(th);
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
+}
+
+}  // namespace
+
+psb_status psb_q8_quant_launch(psb_ctx* c, const float* x, float* r, size_t n, uint32_t B,
+                               int8_t* codes, float* scales, cudaStream_t st) {
+  const size_t nb = (n + B - 1) / B;
+  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((nb + 7) / 8, (size_t)c->num_sms * 8));
+  switch (B) {
+    case 128: k_q8_quant<1><<<grid, 256, 0, st>>>(x, r, n, codes, scales, c->d_flags); break;
+    case 256: k_q8_quant<2><<<grid, 256, 0, st>>>(x, r, n, codes, scales, c->d_flags); break;
+    case 512: k_q8_quant<4><<<grid, 256, 0, st>>>(x, r, n, codes, scales, c->d_flags); break;
+    case 1024: k_q8_quant<8><<<grid, 256, 0, st>>>(x, r, n, codes, scales, c->d_flags); break;
+    default: return psb_set_err(c, PSB_EINVAL, "q8: block must be 128, 256, 512 or 1024");
+  }
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "psb_q8_quantize");
+  return PSB_OK;
+}
+
+psb_status psb_q8_reduce_launch(psb_ctx* c, const int8_t* wcodes, size_t wstride,
+                                const float* wscales, size_t sstride, int P, size_t blk_lo,
+                                size_t blk_hi, size_t n, uint32_t B, psb_order order, uint32_t dpn,
+                                uint32_t npr, int8_t* mcodes, float* mscales, double lr,
+                                float* theta, float* mean_out, cudaStream_t st) {
+  if (blk_hi <= blk_lo) return PSB_OK;
+  const size_t nb = blk_hi - blk_lo;
+  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((nb + 7) / 8, (size_t)c->num_sms * 8));
+  const float coef = (float)(-lr);
+#define PSB_RED(V)                                                                                \
+  k_q8_reduce<V><<<grid, 256, 0, st>>>(wcodes, wstride, wscales, sstride, P, blk_lo, blk_hi, n,    \
+                                       (int)order, dpn, npr, mcodes, mscales, coef, theta, mean_out, \
+                                       c->d_flags)
+  switch (B) {
+    case 128: PSB_RED(1); break;
+    case 256: PSB_RED(2); break;
+    case 512: PSB_RED(4); break;
+    case 1024: PSB_RED(8); break;
+    default: return psb_set_err(c, PSB_EINVAL, "q8: block must be 128, 256, 512 or 1024");
+  }
+#undef PSB_RED
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "q8 reduce");
+  return PSB_OK;
+}
+
+psb_status psb_q8_apply_launch(psb_ctx* c, const int8_t* mcodes, const float* mscales, size_t n,
+                               uint32_t B, double lr, float* theta, float* mean_out,
+                               cudaStream_t st) {
+  const unsigned grid = (unsigned)std::min<size_t>((n / 4 + 255) / 256 + 1, (size_t)c->num_sms * 16);
+  k_q8_apply<<<grid, 256, 0, st>>>(mcodes, mscales, n, B, (float)(-lr), theta, mean_out, c->d_flags);
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "q8 apply");
+  return PSB_OK;
+}
+
+extern "C" psb_status psb_q8_quantize(psb_ctx* c, const float* x, float* r, size_t n,
+                                      uint32_t block, int8_t* codes, float* scales,
+                                      psb_stream_t stream) {
+  PSB_REQUIRE(c, c != nullptr, "null ctx");
+  PSB_REQUIRE(c, n >= 1 && x && codes && scales, "psb_q8_quantize: bad arguments");
+  return psb_q8_quant_launch(c, x, r, n, block, codes, scales, (cudaStream_t)stream);
+}
+
+extern "C" psb_status psb_q8_dequantize(psb_ctx* c, const int8_t* codes, const float* scales,
+                                        size_t n, uint32_t block, float* out, psb_stream_t stream) {
+  PSB_REQUIRE(c, c != nullptr, "null ctx");
+  PSB_REQUIRE(c, n >= 1 && block >= 1 && codes && scales && out, "psb_q8_dequantize: bad arguments");
+  const unsigned grid = (unsigned)std::min<size_t>((n + 255) / 256, (size_t)c->num_sms * 16);
+  k_q8_dequant<<<grid, 256, 0, (cudaStream_t)stream>>>(codes, scales, n, block, out);
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "psb_q8_dequantize");
+  return PSB_OK;
+}

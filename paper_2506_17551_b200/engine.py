@@ -1,0 +1,251 @@
+"""Device-level host API over the C ABI (include/psb.h).
+
+`Context` owns one psb_ctx (all scratch, the NCCL communicator) bound to one
+CUDA device.  Tensors are torch CUDA tensors used purely as device memory;
+every computation runs in libpsb.so kernels on the tensor's current stream.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence, Tuple
+
+import torch
+
+from . import _lib as L
+
+_DT = {torch.float32: L.PSB_F32, torch.float64: L.PSB_F64}
+ORDERS = {"naive": L.PSB_ORDER_NAIVE, "ring": L.PSB_ORDER_RING,
+          "pipelined_ring": L.PSB_ORDER_RING, "hierarchical": L.PSB_ORDER_HIER}
+DISTS = {"uniform": L.PSB_DIST_UNIFORM, "llmrec": L.PSB_DIST_LLMREC, "ties": L.PSB_DIST_TIES}
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise L.PsbInvalidArgument(f"unsupported dtype {t.dtype}; expected float32 or float64")
+
+
+def _need_cuda(*ts: Optional[torch.Tensor]) -> None:
+    for t in ts:
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise L.PsbInvalidArgument("libpsb operates on contiguous CUDA tensors")
+
+
+def topology(racks: int = 0, nodes_per_rack: int = 0, devices_per_node: int = 0) -> L.Topology:
+    """psb_topology; all-zero means the flat topology (devices_per_node = P)."""
+    return L.Topology(racks, nodes_per_rack, devices_per_node)
+
+
+def payload_bytes(compressor: int, dtype: torch.dtype, k: int) -> int:
+    return int(L.load().psb_payload_bytes(compressor, _DT[dtype], k))
+
+
+def generate(dist: str, seed: int, rank: int, step: int, n: int, out: torch.Tensor) -> torch.Tensor:
+    """Counter-based synthetic gradient (bit-identical to orc_generate)."""
+    _need_cuda(out)
+    lib = L.load()
+    st = torch.cuda.current_stream(out.device).cuda_stream
+    L.raise_for(lib.psb_generate(DISTS[dist], seed, rank, step, n, out.data_ptr(), st), None,
+                "psb_generate")
+    return out
+
+
+class Context:
+    """One psb_ctx: scratch for gradients up to max_n, top-k up to max_k and
+    max_workers payloads per step (P = local workers x ranks)."""
+
+    def __init__(self, max_n: int, max_k: int = 1, max_workers: int = 1,
+                 device: Optional[int] = None):
+        self.lib = L.load()
+        if not torch.cuda.is_available():
+            raise L.PsbError("libpsb needs a CUDA device (no CPU fallback)")
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.max_n, self.max_k, self.max_workers = int(max_n), int(max(1, max_k)), int(max_workers)
+        h = ctypes.c_void_p()
+        st = self.lib.psb_ctx_create(ctypes.byref(h), self.device, self.max_n, self.max_k,
+                                     self.max_workers)
+        if st != L.PSB_OK:
+            L.raise_for(st, None, "psb_ctx_create")
+        self.h = h
+        self.rank, self.nranks = 0, 1
+
+    # ----------------------------------------------------------- lifecycle
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.psb_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _ck(self, status: int, where: str) -> None:
+        if status != L.PSB_OK:
+            L.raise_for(status, self.h, where)
+
+    def check(self) -> None:
+        """Synchronize the current stream and raise on device-side errors."""
+        self._ck(self.lib.psb_check(self.h, self.stream()), "psb_check")
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.psb_launch_count(self.h))
+
+    # --------------------------------------------------------- communicator
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        L.raise_for(L.load().psb_comm_unique_id(buf), None, "psb_comm_unique_id")
+        return buf.raw
+
+    def comm_init(self, rank: int, nranks: int, uid: Optional[bytes]) -> None:
+        buf = ctypes.create_string_buffer(uid, 128) if uid is not None else None
+        self._ck(self.lib.psb_comm_init(self.h, rank, nranks, buf), "psb_comm_init")
+        self.rank, self.nranks = rank, nranks
+
+    def allgather_(self, buf: torch.Tensor, bytes_per_rank: int) -> None:
+        _need_cuda(buf)
+        self._ck(self.lib.psb_allgather(self.h, buf.data_ptr(), bytes_per_rank, self.stream()),
+                 "psb_allgather")
+
+    # ---------------------------------------------------------- compressors
+    def ef_topk(self, g: torch.Tensor, r: Optional[torch.Tensor], k: int, worker: int = 0,
+                idx_out: Optional[torch.Tensor] = None,
+                val_out: Optional[torch.Tensor] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+        """K1: p = r + g, top-k of |p| (ties -> lower index), r := sel ? +0 : p.
+        Returns (idx int32 [k] holding u32 indices, val [k])."""
+        _need_cuda(g, r)
+        n = g.numel()
+        if idx_out is None:
+            idx_out = torch.empty(max(k, 1), dtype=torch.int32, device=g.device)
+        if val_out is None:
+            val_out = torch.empty(max(k, 1), dtype=g.dtype, device=g.device)
+        self._ck(self.lib.psb_ef_topk(self.h, _dtype_code(g), worker, g.data_ptr(), _ptr(r), n, k,
+                                      idx_out.data_ptr(), val_out.data_ptr(), self.stream()),
+                 "ef_compress_step")
+        return idx_out[:k], val_out[:k]
+
+    def ef_topk_q8(self, g: torch.Tensor, r: Optional[torch.Tensor], k: int, worker: int = 0):
+        _need_cuda(g, r)
+        idx = torch.empty(k, dtype=torch.int32, device=g.device)
+        codes = torch.empty(k, dtype=torch.int8, device=g.device)
+        scales = torch.empty((k + 127) // 128, dtype=torch.float32, device=g.device)
+        self._ck(self.lib.psb_ef_topk_q8(self.h, worker, g.data_ptr(), _ptr(r), g.numel(), k,
+                                         idx.data_ptr(), codes.data_ptr(), scales.data_ptr(),
+                                         self.stream()), "ef_compress_step(topk_q8)")
+        return idx, codes, scales
+
+    def ef_onebit(self, g: torch.Tensor, r: Optional[torch.Tensor]):
+        """1-bit EF: returns (sign words int32 [ceil(n/32)], scale f64 device [1])."""
+        _need_cuda(g, r)
+        n = g.numel()
+        words = torch.empty((n + 31) // 32, dtype=torch.int32, device=g.device)
+        scale = torch.empty(1, dtype=torch.float64, device=g.device)
+        self._ck(self.lib.psb_ef_onebit(self.h, _dtype_code(g), g.data_ptr(), _ptr(r), n,
+                                        words.data_ptr(), scale.data_ptr(), self.stream()),
+                 "ef_compress_step(onebit)")
+        return words, scale
+
+    def q8_quantize(self, x: torch.Tensor, r: Optional[torch.Tensor], block: int = 256):
+        _need_cuda(x, r)
+        n = x.numel()
+        codes = torch.empty(n, dtype=torch.int8, device=x.device)
+        scales = torch.empty((n + block - 1) // block, dtype=torch.float32, device=x.device)
+        self._ck(self.lib.psb_q8_quantize(self.h, x.data_ptr(), _ptr(r), n, block,
+                                          codes.data_ptr(), scales.data_ptr(), self.stream()),
+                 "psb_q8_quantize")
+        return codes, scales
+
+    def q8_dequantize(self, codes: torch.Tensor, scales: torch.Tensor, block: int = 256):
+        out = torch.empty(codes.numel(), dtype=torch.float32, device=codes.device)
+        self._ck(self.lib.psb_q8_dequantize(self.h, codes.data_ptr(), scales.data_ptr(),
+                                            codes.numel(), block, out.data_ptr(), self.stream()),
+                 "psb_q8_dequantize")
+        return out
+
+    def decompress_topk(self, idx: torch.Tensor, val: torch.Tensor, n: int) -> torch.Tensor:
+        out = torch.zeros(n, dtype=val.dtype, device=val.device)
+        self._ck(self.lib.psb_decompress_topk(self.h, _dtype_code(val), _ptr(idx), _ptr(val),
+                                              val.numel(), n, out.data_ptr(), self.stream()),
+                 "decompress")
+        return out
+
+    # ------------------------------------------------------ aggregate+apply
+    def sparse_mean_sgd(self, payloads: torch.Tensor, P: int, k: int, dtype: torch.dtype,
+                        order: str, lr: float, theta: Optional[torch.Tensor], n: int,
+                        mean_out: Optional[torch.Tensor] = None,
+                        topo: Optional[L.Topology] = None,
+                        compressor: int = L.PSB_COMP_TOPK) -> None:
+        topo = topo or topology()
+        self._ck(self.lib.psb_sparse_mean_sgd(self.h, compressor, _DT[dtype], P,
+                                              payloads.data_ptr(), k, ORDERS[order],
+                                              ctypes.byref(topo), lr, _ptr(theta), n,
+                                              _ptr(mean_out), self.stream()), "sparse_mean_sgd")
+
+    def sparse_async_apply(self, payloads: torch.Tensor, P: int, k: int, dtype: torch.dtype,
+                           scales: Sequence[float], theta: torch.Tensor,
+                           compressor: int = L.PSB_COMP_TOPK) -> None:
+        arr = (ctypes.c_double * P)(*scales)
+        self._ck(self.lib.psb_sparse_async_apply(self.h, compressor, _DT[dtype], P,
+                                                 payloads.data_ptr(), k, arr, theta.data_ptr(),
+                                                 theta.numel(), self.stream()), "async_apply")
+
+    def dense_mean_sgd(self, bufs: torch.Tensor, order: str, lr: float,
+                       theta: Optional[torch.Tensor], mean_out: Optional[torch.Tensor] = None,
+                       topo: Optional[L.Topology] = None) -> None:
+        _need_cuda(bufs, theta, mean_out)
+        P, n = bufs.shape
+        topo = topo or topology()
+        self._ck(self.lib.psb_dense_mean_sgd(self.h, _dtype_code(bufs), P, bufs.data_ptr(),
+                                             ORDERS[order], ctypes.byref(topo), lr, _ptr(theta),
+                                             n, _ptr(mean_out), self.stream()), "allreduce_mean")
+
+    def onebit_mean_sgd(self, words: torch.Tensor, scales: torch.Tensor, n: int,
+                        dtype: torch.dtype, order: str, lr: float, theta: Optional[torch.Tensor],
+                        mean_out: Optional[torch.Tensor] = None,
+                        topo: Optional[L.Topology] = None) -> None:
+        P = scales.numel()
+        topo = topo or topology()
+        self._ck(self.lib.psb_onebit_mean_sgd(self.h, _DT[dtype], P, words.data_ptr(),
+                                              scales.data_ptr(), ORDERS[order], ctypes.byref(topo),
+                                              lr, _ptr(theta), n, _ptr(mean_out), self.stream()),
+                 "onebit_mean_sgd")
+
+    # ------------------------------------------------------------- drivers
+    def step_desc(self, compressor: int, g: torch.Tensor, r: Optional[torch.Tensor],
+                  theta: torch.Tensor, lr: float, k: int = 0, order: str = "naive",
+                  q8_block: int = 256, topo: Optional[L.Topology] = None,
+                  mean_out: Optional[torch.Tensor] = None) -> L.StepDesc:
+        _need_cuda(g, r, theta, mean_out)
+        W = g.shape[0] if g.dim() == 2 else 1
+        n = g.shape[-1]
+        d = L.StepDesc()
+        d.compressor = compressor
+        d.dtype = _dtype_code(g)
+        d.n, d.k, d.q8_block, d.workers = n, k, q8_block, W
+        d.g, d.r, d.theta = g.data_ptr(), _ptr(r), theta.data_ptr()
+        d.lr = lr
+        d.order = ORDERS[order]
+        d.topo = topo or topology()
+        d.mean_out = _ptr(mean_out)
+        return d
+
+    def sync_step(self, desc: L.StepDesc) -> None:
+        self._ck(self.lib.psb_sync_step(self.h, ctypes.byref(desc), self.stream()),
+                 "sync_data_parallel_step")
+
+    def async_round(self, desc: L.StepDesc, staleness_bound: int, global_updates: int) -> int:
+        gu = ctypes.c_uint64(global_updates)
+        self._ck(self.lib.psb_async_round(self.h, ctypes.byref(desc), staleness_bound,
+                                          ctypes.byref(gu), self.stream()), "async_round")
+        return int(gu.value)

@@ -1,0 +1,235 @@
+"""GPU parity of aggregate + apply, the other compressors and the step drivers.
+
+Bar: bit-exact against the oracle composite whenever the reference fold order
+is mirrored (all cases here); the 1-bit scale is a deterministic tree sum and
+is compared at 1e-12 relative (f64) -- see DESIGN.md "Parity".
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2506_17551_b200 import _lib as L
+from paper_2506_17551_b200.engine import payload_bytes, topology
+
+pytestmark = pytest.mark.gpu
+
+
+def tnp(t):
+    return t.detach().cpu().numpy()
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64 if a.dtype == np.float64 else np.uint32)
+
+
+def make_payloads(P, n, k, dtype, seed, overlap=True):
+    """P top-k payloads with heavy index overlap, +-0 values and collisions."""
+    rng = np.random.default_rng(seed)
+    idx = np.zeros((P, k), dtype=np.uint32)
+    val = np.zeros((P, k), dtype=dtype)
+    pool = rng.choice(n, size=min(n, 3 * k), replace=False)
+    for p in range(P):
+        src = pool if overlap else np.arange(n)
+        idx[p] = np.sort(rng.choice(src, size=k, replace=False))
+        v = rng.standard_normal(k).astype(dtype)
+        v[rng.random(k) < 0.05] = dtype(0.0)
+        v[rng.random(k) < 0.05] = -dtype(0.0)
+        val[p] = v
+    return idx, val
+
+
+def pack_payloads(idx, val, dtype_t):
+    P, k = idx.shape
+    blk = payload_bytes(L.PSB_COMP_TOPK, dtype_t, k)
+    buf = np.zeros(P * blk, dtype=np.uint8)
+    voff = (k * 4 + 15) // 16 * 16
+    for p in range(P):
+        buf[p * blk:p * blk + 4 * k] = idx[p].view(np.uint8)
+        vb = val[p].view(np.uint8)
+        buf[p * blk + voff:p * blk + voff + vb.size] = vb
+    return torch.from_numpy(buf).cuda()
+
+
+ORDERS = [("naive", 0, 1), ("ring", 0, 1), ("hierarchical", 2, 2), ("hierarchical", 3, 1),
+          ("pipelined_ring", 0, 1)]
+
+
+@pytest.mark.parametrize("dtype_t", [torch.float32, torch.float64])
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8, 16])
+@pytest.mark.parametrize("order,dpn,npr", ORDERS)
+def test_sparse_mean_sgd_bitwise(ctx, dtype_t, P, order, dpn, npr):
+    dt = np.float32 if dtype_t == torch.float32 else np.float64
+    n, k = 50_021, 1_500
+    idx, val = make_payloads(P, n, k, dt, seed=P * 7 + len(order))
+    theta_h = (O.generate("uniform", 5, 0, 0, n)).astype(dt)
+    theta_h[::11] = -0.0
+    dense = np.zeros((P, n), dtype=dt)
+    for p in range(P):
+        dense[p, idx[p].astype(np.int64)] = val[p]
+    mean_h = O.fold_mean(dense, order, dpn, npr)
+    want = theta_h.copy()
+    O.axpy_(-0.05, mean_h, want)
+    theta = torch.from_numpy(theta_h.copy()).cuda()
+    mean = torch.zeros(n, dtype=dtype_t, device="cuda")
+    pl = pack_payloads(idx, val, dtype_t)
+    topo = topology(1, npr, dpn) if dpn else None
+    ctx.sparse_mean_sgd(pl, P, k, dtype_t, order, 0.05, theta, n, mean, topo)
+    ctx.check()
+    assert np.array_equal(bits(tnp(theta)), bits(want))
+    touched = np.unique(idx.astype(np.int64))
+    assert np.array_equal(bits(tnp(mean)[touched]), bits(mean_h[touched]))
+
+
+@pytest.mark.parametrize("P", [1, 4, 8])
+def test_async_apply_bitwise(ctx, P):
+    n, k = 40_000, 800
+    idx, val = make_payloads(P, n, k, np.float32, seed=P)
+    theta_h = O.generate("llmrec", 2, 0, 0, n)
+    scales = [0.1 / (1 + (p % 3)) for p in range(P)]
+    want = theta_h.copy()
+    for p in range(P):
+        O.axpy_(-scales[p], O.decompress_topk(idx[p], val[p], n), want)
+    theta = torch.from_numpy(theta_h.copy()).cuda()
+    ctx.sparse_async_apply(pack_payloads(idx, val, torch.float32), P, k, torch.float32, scales, theta)
+    ctx.check()
+    assert np.array_equal(bits(tnp(theta)), bits(want))
+
+
+@pytest.mark.parametrize("dtype_t", [torch.float32, torch.float64])
+@pytest.mark.parametrize("order,dpn,npr", ORDERS)
+def test_dense_mean_bitwise(ctx, dtype_t, order, dpn, npr):
+    dt = np.float32 if dtype_t == torch.float32 else np.float64
+    for P in (1, 3, 8):
+        n = 10_007
+        bufs = np.stack([O.generate("uniform", 11, p, 0, n) for p in range(P)]).astype(dt)
+        theta_h = O.generate("uniform", 12, 0, 0, n).astype(dt)
+        mean_h = O.fold_mean(bufs, order, dpn, npr)
+        want = theta_h.copy()
+        O.axpy_(-0.25, mean_h, want)
+        theta = torch.from_numpy(theta_h.copy()).cuda()
+        mean = torch.empty(n, dtype=dtype_t, device="cuda")
+        topo = topology(1, npr, dpn) if dpn else None
+        ctx.dense_mean_sgd(torch.from_numpy(bufs).cuda(), order, 0.25, theta, mean, topo)
+        ctx.check()
+        assert np.array_equal(bits(tnp(mean)), bits(mean_h))
+        assert np.array_equal(bits(tnp(theta)), bits(want))
+
+
+@pytest.mark.parametrize("dtype_t", [torch.float32, torch.float64])
+def test_onebit_compress_and_mean(ctx, dtype_t):
+    dt = np.float32 if dtype_t == torch.float32 else np.float64
+    n = 100_003
+    g_h = O.generate("llmrec", 13, 0, 0, n).astype(dt)
+    r_h = (O.generate("uniform", 13, 1, 0, n) * 1e-3).astype(dt)
+    r = torch.from_numpy(r_h.copy()).cuda()
+    words, scale = ctx.ef_onebit(torch.from_numpy(g_h).cuda(), r)
+    ctx.check()
+    ow, osc, _ = O.ef_onebit(g_h, r_h)
+    assert np.array_equal(tnp(words).view(np.uint32), ow)
+    assert abs(float(scale.item()) - osc) <= 1e-12 * abs(osc)
+    # residual: bit-exact given the scale the device computed
+    s = dt(float(scale.item()))
+    pp = ((O.generate("uniform", 13, 1, 0, n) * 1e-3).astype(dt) + g_h).astype(dt)
+    want = (pp - np.where(pp >= 0, s, -s)).astype(dt)
+    assert np.array_equal(bits(tnp(r)), bits(want))
+    # 1-bit fold + SGD with the device scales
+    P = 4
+    ws = torch.stack([torch.from_numpy(ow.view(np.int32)).cuda()] * P)
+    scales = torch.tensor([osc * (1 + p) for p in range(P)], dtype=torch.float64, device="cuda")
+    theta = torch.zeros(n, dtype=dtype_t, device="cuda")
+    mean = torch.empty(n, dtype=dtype_t, device="cuda")
+    ctx.onebit_mean_sgd(ws, scales, n, dtype_t, "ring", 0.1, theta, mean)
+    ctx.check()
+    bitsv = ((ow.view(np.uint8)[:, None] >> np.arange(8, dtype=np.uint8)) & 1).reshape(-1)[:n].astype(bool)
+    dense = np.stack([np.where(bitsv, dt(osc * (1 + p)), -dt(osc * (1 + p))) for p in range(P)])
+    mean_h = O.fold_mean(dense, "ring")
+    want_t = np.zeros(n, dtype=dt)
+    O.axpy_(-0.1, mean_h, want_t)
+    assert np.array_equal(bits(tnp(mean)), bits(mean_h))
+    assert np.array_equal(bits(tnp(theta)), bits(want_t))
+
+
+@pytest.mark.parametrize("block", [128, 256, 512, 1024])
+def test_q8_quantize_bitwise(ctx, block):
+    for n in (1, 1000, 262_147):
+        g_h = O.generate("llmrec", 21, 0, 0, n)
+        r_h = O.generate("uniform", 21, 1, 0, n) * np.float32(1e-4)
+        r = torch.from_numpy(r_h.copy()).cuda()
+        codes, scales = ctx.q8_quantize(torch.from_numpy(g_h).cuda(), r, block)
+        oc, osc, _ = O.q8_quant(g_h, r_h, block)
+        ctx.check()
+        assert np.array_equal(tnp(codes), oc)
+        assert np.array_equal(bits(tnp(scales)), bits(osc))
+        assert np.array_equal(bits(tnp(r)), bits(r_h))
+        deq = ctx.q8_dequantize(codes, scales, block)
+        assert np.array_equal(bits(tnp(deq)), bits(O.q8_dequant(oc, osc, block)))
+
+
+COMPS = {"topk": L.PSB_COMP_TOPK, "onebit": L.PSB_COMP_ONEBIT, "none": L.PSB_COMP_NONE,
+         "q8": L.PSB_COMP_Q8, "topk_q8": L.PSB_COMP_TOPK_Q8}
+
+
+@pytest.mark.parametrize("comp", ["topk", "topk_q8", "none", "q8", "onebit"])
+@pytest.mark.parametrize("order", ["naive", "ring", "hierarchical"])
+@pytest.mark.parametrize("W", [1, 4])
+def test_sync_step_virtual_workers(ctx, comp, order, W):
+    """psb_sync_step with W virtual workers on one GPU (cfg1 shape) vs the
+    oracle composite of sync_data_parallel_step, 10 steps, EF carried."""
+    n, k, lr = 100_000, 1_000, 0.05
+    dpn, npr = (2, 2) if order == "hierarchical" and W == 4 else (0, 1)
+    topo = topology(1, npr, dpn) if dpn else None
+    theta_h = np.zeros(n, dtype=np.float32)
+    res_h = np.zeros((W, n), dtype=np.float32)
+    theta = torch.zeros(n, device="cuda")
+    res = torch.zeros(W, n, device="cuda")
+    for step in range(10):
+        g_h = np.stack([O.generate("llmrec", 42, w, step, n) for w in range(W)])
+        g = torch.from_numpy(g_h).cuda()
+        mean = torch.zeros(n, device="cuda")
+        d = ctx.step_desc(COMPS[comp], g, res, theta, lr, k, order, 256, topo, mean)
+        ctx.sync_step(d)
+        ctx.check()
+        O.sync_step(g_h, theta_h, lr, comp, k, order, res_h, dpn, npr, 256)
+        if comp == "onebit":
+            # scale = deterministic tree sum vs sequential fold: tolerance
+            np.testing.assert_allclose(tnp(theta), theta_h, rtol=1e-5, atol=1e-7)
+            theta.copy_(torch.from_numpy(theta_h))
+            res.copy_(torch.from_numpy(res_h))
+        else:
+            assert np.array_equal(bits(tnp(theta)), bits(theta_h)), step
+            assert np.array_equal(bits(tnp(res)), bits(res_h)), step
+
+
+@pytest.mark.parametrize("q8", [False, True])
+def test_async_round_bounded_staleness(ctx, q8):
+    """psb_async_round vs the trainer's async loop (trainer.hpp:244-255), s=3
+    (reference pattern) and s=2 (cfg4)."""
+    for s in (3, 2):
+        W, n, k, lr = 8, 60_000, 60, 0.1
+        theta_h = np.zeros(n, dtype=np.float32)
+        res_h = np.zeros((W, n), dtype=np.float32)
+        theta = torch.zeros(n, device="cuda")
+        res = torch.zeros(W, n, device="cuda")
+        gu = gu_h = 0
+        for step in range(5):
+            g_h = np.stack([O.generate("llmrec", 4, w, step, n) for w in range(W)])
+            comp = L.PSB_COMP_TOPK_Q8 if q8 else L.PSB_COMP_TOPK
+            d = ctx.step_desc(comp, torch.from_numpy(g_h).cuda(), res, theta, lr, k)
+            gu = ctx.async_round(d, s, gu)
+            ctx.check()
+            gu_h = O.async_round(g_h, theta_h, lr, k, res_h, s, gu_h, q8=q8)
+            assert gu == gu_h
+            assert np.array_equal(bits(tnp(theta)), bits(theta_h)), (s, step)
+            assert np.array_equal(bits(tnp(res)), bits(res_h)), (s, step)
+
+
+def test_step_rejects_bad_args(ctx):
+    from paper_2506_17551_b200 import PsbInvalidArgument
+    g = torch.zeros(2, 100, device="cuda")
+    theta = torch.zeros(100, device="cuda")
+    with pytest.raises(PsbInvalidArgument, match="learning_rate"):
+        ctx.sync_step(ctx.step_desc(L.PSB_COMP_TOPK, g, None, theta, 0.0, 5))
+    with pytest.raises(PsbInvalidArgument, match="k out of range"):
+        ctx.sync_step(ctx.step_desc(L.PSB_COMP_TOPK, g, None, theta, 0.1, 101))
