@@ -1,0 +1,368 @@
+"""bench.py -- dense-equiv gradient GB/s of the compress+aggregate+apply step.
+
+Default (no flags): N=1 GPU, BASELINE.json configs[1] shape at one rank:
+125M-param LLM-rec gradient, EF top-k 1%, sparse allgather (one rank: no
+exchange), sync SGD.  Under torchrun (N>1) every rank owns one worker (P = N),
+compresses its own 125M gradient, the payloads are allgathered over NCCL and
+every replica applies the same rank-ordered mean (weak scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config cfg2|cfg3|cfg4|cfg1] [--n N] [--rho R]
+
+One JSON line on rank 0 (contract in the task statement; fields explained in
+DESIGN.md "Measurement").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "dense-equiv gradient GB/s per step (compress+aggregate+apply) at 1/2/4/8 B200"
+
+CONFIGS = {
+    # name: (workload text, n, rho, compressor, order, dist, mode, extra)
+    "cfg2": ("cfg2: 125M-param LLM-rec gradient, top-k 1% + error feedback, sparse allgather, sync SGD",
+             125_000_000, 0.01, "topk", "ring", "llmrec", "sync", {}),
+    "cfg3": ("cfg3: 125M-param gradient, dense 8-bit block-quantized (B=256) hierarchical allreduce, sync SGD",
+             125_000_000, 0.0, "q8", "naive", "llmrec", "sync", {"q8_block": 256}),
+    "cfg4": ("cfg4: 350M-param gradient, top-k 0.1% + int8 values, async bounded staleness s=2",
+             350_000_000, 0.001, "topk_q8", "naive", "llmrec", "async", {"staleness": 2}),
+    "cfg1": ("cfg1: 1M-param gradient, top-k 1% + error feedback, sync SGD, 4 simulated workers",
+             1_000_000, 0.01, "topk", "ring", "uniform", "sync", {"workers": 4}),
+}
+
+CLOCK_REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+    0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                bits = int(parts[2], 16)
+            except ValueError:
+                continue
+            for b, name in CLOCK_REASONS.items():
+                if bits & b and name != "gpu_idle":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- CPU legs
+def cpu_reference_run(n_sample: int, P: int, k: int, threads: int, budget_s: float, min_steps: int,
+                      max_steps: int, dist: str, comp: str):
+    """Time the reference's own sync_data_parallel_step (oracle/_ref) on a
+    bounded sample; returns (GB/s dense-equiv, seconds per step, steps, kind)."""
+    import numpy as np
+
+    from oracle import oracle as O
+    kind = "reference" if O.ref_available() else "port"
+    grads = [np.stack([O.generate(dist, 42, p, s, n_sample) for p in range(P)]).astype(np.float64)
+             for s in range(2)]
+    theta = np.zeros(n_sample)
+    res = np.zeros((P, n_sample))
+    times = []
+    t_start = time.perf_counter()
+    for s in range(max_steps):
+        t0 = time.perf_counter()
+        if kind == "reference":
+            if comp == "topk":
+                O.ref_sync_step_threaded("topk", k, "ring", grads[s % 2], theta, 0.05, res, threads)
+            else:
+                O.ref_sync_step("none", 0, "naive", grads[s % 2], theta, 0.05, None)
+        else:
+            g32 = grads[s % 2].astype(np.float32)
+            O.sync_step(g32, theta.astype(np.float32), 0.05, comp if comp == "topk" else "none", k,
+                        "ring", res.astype(np.float32))
+        times.append(time.perf_counter() - t0)
+        if len(times) >= min_steps and time.perf_counter() - t_start > budget_s:
+            break
+    t = statistics.median(times)
+    return 4.0 * n_sample * P / t / 1e9, t, len(times), kind
+
+
+def reference_arm(args, cfg, world, rank):
+    name, n, rho, comp, order, dist, mode, extra = cfg
+    if rank != 0:
+        return
+    P = world * extra.get("workers", 1)
+    n_sample = min(n, 2_000_000)
+    k = max(1, int(round(rho * n_sample))) if comp.startswith("topk") else 0
+    threads = max(1, min(P, os.cpu_count() or 1))
+    ref_comp = "topk" if comp.startswith("topk") else "none"
+    steps = max(1, args.steps)
+    # warmup (untimed) then K timed steps, each a bounded sample of the workload
+    if args.warmup:
+        cpu_reference_run(n_sample, P, k, threads, 0.0, 1, 1, dist, ref_comp)
+    gbs, t, done, kind = cpu_reference_run(n_sample, P, k, threads, 0.0, steps, steps, dist, ref_comp)
+    sample = (f"N={n_sample} of {n} params per worker x P={P} workers, k={k} ({ref_comp}), "
+              f"{done} steps of the reference sync_data_parallel_step"
+              f"{' (per-worker ef_compress_step on ' + str(threads) + ' threads, serial fold)' if threads > 1 else ''}")
+    line = {
+        "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": done,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (same mix64 generator, widened to f64)",
+        "config": {"workload": name, "n_params": n, "P": P, "sample_n": n_sample},
+        "impl": "reference",
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU arm
+def ours(args, cfg, world, rank, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_17551_b200 import _lib as L
+    from paper_2506_17551_b200.engine import Context, generate
+
+    name, n, rho, comp, order, dist_name, mode, extra = cfg
+    if args.n:
+        n = args.n
+    if args.rho is not None:
+        rho = args.rho
+    W = extra.get("workers", 1)
+    P = W * world
+    k = max(1, int(round(rho * n))) if comp.startswith("topk") else 0
+    comp_code = {"topk": L.PSB_COMP_TOPK, "topk_q8": L.PSB_COMP_TOPK_Q8, "q8": L.PSB_COMP_Q8,
+                 "onebit": L.PSB_COMP_ONEBIT, "none": L.PSB_COMP_NONE}[comp]
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.Stream(dev)
+    ctx = Context(n, max(k, 1), P, device=local_rank)
+    if world > 1:
+        uid = [Context.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.comm_init(rank, world, uid[0])
+
+    NB = 3  # rotated gradient buffers (each > L2): inputs larger than L2
+    with torch.cuda.stream(stream):
+        grads = [torch.empty(W, n, device=dev) for _ in range(NB)]
+        for b in range(NB):
+            for w in range(W):
+                generate(dist_name, 42, rank * W + w, b, n, grads[b][w])
+        res = torch.zeros(W, n, device=dev)
+        theta = torch.zeros(n, device=dev)
+        descs = [ctx.step_desc(comp_code, grads[b], res, theta, 0.05, k, order,
+                               extra.get("q8_block", 256)) for b in range(NB)]
+    stream.synchronize()
+    gu = [0]
+
+    def step(i):
+        d = descs[i % NB]
+        if mode == "async":
+            gu[0] = ctx.async_round(d, extra.get("staleness", 2), gu[0])
+        else:
+            ctx.sync_step(d)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+        ctx.check()
+        # ---- timed region: K steps, device-timed with events on our stream
+        barrier()
+        torch.cuda.synchronize(dev)
+        ctx.profile_enable(True)
+        ctx.profile_read()
+        l0 = ctx.launches
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local_rank) as clk:
+            e0.record(stream)
+            for i in range(args.steps):
+                step(args.warmup + i)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+        barrier()
+        launches = ctx.launches - l0
+        ctx.profile_enable(False)
+        k1_ms, k1_count = ctx.profile_read()
+        ctx.check()
+        ms_local = e0.elapsed_time(e1) / args.steps
+        t = torch.tensor([ms_local, k1_ms / max(k1_count, 1)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step, k1_avg_ms = float(t[0]), float(t[1])
+
+        # ---- e2e through the public API: pinned host gradient in, theta out
+        host_g = [torch.empty(W, n, pin_memory=True) for _ in range(2)]
+        for b in range(2):
+            host_g[b].copy_(grads[b].cpu())
+        host_theta = torch.empty(n, pin_memory=True)
+        dev_g = torch.empty(W, n, device=dev)
+        d_e2e = ctx.step_desc(comp_code, dev_g, res, theta, 0.05, k, order, extra.get("q8_block", 256))
+        e_steps = max(3, min(args.steps, 10))
+        barrier()
+        torch.cuda.synchronize(dev)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for i in range(e_steps):
+            dev_g.copy_(host_g[i % 2], non_blocking=True)
+            if mode == "async":
+                gu[0] = ctx.async_round(d_e2e, extra.get("staleness", 2), gu[0])
+            else:
+                ctx.sync_step(d_e2e)
+            host_theta.copy_(theta, non_blocking=True)
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+        ctx.check()
+        te = torch.tensor([f0.elapsed_time(f1) / e_steps], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = float(te[0])
+
+    if rank != 0:
+        ctx.close()
+        return
+    peak, peak_src = load_peaks()
+    dense_bytes = 4.0 * n * P
+    value = dense_bytes / (ms_step * 1e-3) / 1e9
+    e2e_value = dense_bytes / (e2e_ms * 1e-3) / 1e9
+    # roofline of the dominant kernel (K1 streaming pass): algorithmic bytes
+    # per launch = 12 bytes/element (read g, read r, write r) x n elements
+    k1_bytes = 12.0 * n
+    k1_gbs = k1_bytes / (k1_avg_ms * 1e-3) / 1e9 if k1_avg_ms > 0 else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
+            tr = json.load(f)
+        traffic = tr.get(f"{comp}:{n}")
+    except Exception:
+        pass
+    # whole-step algorithmic bytes per GPU: 12N + 8k + 8Pk + 8|U| (|U| <= Pk)
+    step_alg = 12.0 * n + 8.0 * k + 8.0 * P * k + 8.0 * min(P * k, n) if comp == "topk" else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (counter-based mix64 LLM-rec gradients generated on device before timing)",
+        "config": {"workload": name, "n_params": n, "k": k, "rho": rho, "workers_per_rank": W, "P": P,
+                   "compressor": comp, "order": order, "mode": mode,
+                   "l2": f"inputs larger than L2: {NB} rotated {4 * n * W / 1e6:.0f} MB gradient buffers"},
+        "roofline": {"bound": "hbm", "kernel": "k_scan<float,MODE_A> (EF add + level-1 histogram)",
+                     "achieved": k1_gbs, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": (k1_gbs / peak) if k1_gbs else None, "traffic": traffic,
+                     "alg_bytes_per_launch": k1_bytes, "avg_launch_ms": k1_avg_ms,
+                     "step_alg_bytes": step_alg,
+                     "step_frac": (step_alg / (ms_step * 1e-3) / 1e9 / peak) if step_alg else None},
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 4 * n * W,
+                "d2h_bytes_per_step": 4 * n, "ms_per_step": e2e_ms,
+                "path": "psb_sync_step via the Python host API; pinned host gradient H2D + theta D2H per step"},
+        "gpu_launches": launches,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        n_s = min(n, 2_000_000)
+        k_s = max(1, int(round(rho * n_s))) if comp.startswith("topk") else 0
+        gbs, t_s, done, kind = cpu_reference_run(n_s, P, k_s, 1, 12.0, 2, 20, dist_name,
+                                                 "topk" if comp.startswith("topk") else "none")
+        line["cpu_baseline"] = {
+            "value": gbs, "unit": "GB/s", "cores": 1, "kind": kind,
+            "sample": f"{done} steps of reference sync_data_parallel_step at N={n_s} (P={P}, k={k_s}), "
+                      f"median {t_s:.3f} s/step, 1 thread (the reference is single-threaded)"}
+    print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--rho", type=float, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        reference_arm(args, cfg, world, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        ours(args, cfg, world, rank, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

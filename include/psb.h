@@ -99,6 +99,14 @@ PSB_API psb_status psb_check(psb_ctx* ctx, psb_stream_t stream);
 /* Number of the ctx's own kernels launched so far (for launch accounting). */
 PSB_API uint64_t psb_launch_count(const psb_ctx* ctx);
 
+/* Kernel timing for roofline accounting: when enabled, every launch of the
+ * K1 streaming pass (the EF add + level-1 histogram kernel, the path's
+ * dominant kernel) is bracketed by CUDA events on its launching stream.
+ * psb_profile_read synchronizes, returns the summed duration (ms) and launch
+ * count since the last read, and clears them. */
+PSB_API psb_status psb_profile_enable(psb_ctx* ctx, int enable);
+PSB_API psb_status psb_profile_read(psb_ctx* ctx, double* total_ms, uint64_t* launches);
+
 /* Bytes of one worker's top-k payload block: u32 idx[k] | pad16 | val[k] | pad16
  * (TOPK, val of dtype) or u32 idx[k] | pad16 | i8 code[k] | pad16 |
  * f32 scale[ceil(k/128)] | pad16 (TOPK_Q8). */

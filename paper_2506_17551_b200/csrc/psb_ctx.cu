@@ -129,7 +129,39 @@ extern "C" void psb_ctx_destroy(psb_ctx* c) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->comm) ncclCommDestroy(c->comm);
+  for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
   delete c;
+}
+
+cudaEvent_t psb_prof_event(psb_ctx* c) {
+  if (c->prof_used == c->prof_ev.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->prof_ev.push_back(e);
+  }
+  return c->prof_ev[c->prof_used++];
+}
+
+extern "C" psb_status psb_profile_enable(psb_ctx* c, int enable) {
+  PSB_REQUIRE(c, c != nullptr, "null ctx");
+  c->prof = enable ? 1 : 0;
+  return PSB_OK;
+}
+
+extern "C" psb_status psb_profile_read(psb_ctx* c, double* total_ms, uint64_t* launches) {
+  PSB_REQUIRE(c, c != nullptr && total_ms && launches, "psb_profile_read: null argument");
+  double t = 0.0;
+  const size_t pairs = c->prof_used / 2;
+  for (size_t i = 0; i < pairs; ++i) {
+    CUDA_TRY(c, cudaEventSynchronize(c->prof_ev[2 * i + 1]), "psb_profile_read");
+    float ms = 0.f;
+    CUDA_TRY(c, cudaEventElapsedTime(&ms, c->prof_ev[2 * i], c->prof_ev[2 * i + 1]), "psb_profile_read");
+    t += ms;
+  }
+  *total_ms = t;
+  *launches = pairs;
+  c->prof_used = 0;
+  return PSB_OK;
 }
 
 extern "C" const char* psb_last_error(const psb_ctx* c) { return c ? c->err.c_str() : "null ctx"; }

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <string>
+#include <vector>
 
 #include "psb.h"
 
@@ -73,7 +74,14 @@ struct psb_ctx {
   void* d_work = nullptr;  // generic workspace
   size_t work_bytes = 0;
   float* d_qmean = nullptr;
+  // kernel timing (psb_profile_*)
+  int prof = 0;
+  std::vector<cudaEvent_t> prof_ev;  // pairs (start, stop)
+  size_t prof_used = 0;
 };
+
+// Record a profiling event pair around the dominant kernel (no-op unless enabled).
+cudaEvent_t psb_prof_event(psb_ctx* c);
 
 // ------------------------------------------------------------------- helpers
 psb_status psb_set_err(psb_ctx* c, psb_status s, const std::string& msg);

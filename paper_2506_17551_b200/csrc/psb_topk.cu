@@ -573,7 +573,9 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   a.stage_val = reinterpret_cast<T*>(c->d_stage_val);
   a.flags = c->d_flags;
   const uint32_t scan_grid = (uint32_t)std::min<size_t>(ntiles, (size_t)c->num_sms * 4);
+  if (c->prof) cudaEventRecord(psb_prof_event(c), st);
   k_scan<T, MODE_A><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
+  if (c->prof) cudaEventRecord(psb_prof_event(c), st);
   k_scan<T, MODE_A2><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
   k_scan<T, MODE_D><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
 

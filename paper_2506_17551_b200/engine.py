@@ -101,6 +101,16 @@ class Context:
     def launches(self) -> int:
         return int(self.lib.psb_launch_count(self.h))
 
+    def profile_enable(self, on: bool = True) -> None:
+        self._ck(self.lib.psb_profile_enable(self.h, 1 if on else 0), "psb_profile_enable")
+
+    def profile_read(self) -> Tuple[float, int]:
+        """(summed ms, launches) of the K1 streaming pass since the last read."""
+        ms, cnt = ctypes.c_double(), ctypes.c_uint64()
+        self._ck(self.lib.psb_profile_read(self.h, ctypes.byref(ms), ctypes.byref(cnt)),
+                 "psb_profile_read")
+        return float(ms.value), int(cnt.value)
+
     # --------------------------------------------------------- communicator
     @staticmethod
     def unique_id() -> bytes:
