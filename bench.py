@@ -57,57 +57,58 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi sampled every 200 ms during the timed region."""
+    """SM clock + clock-event reasons sampled through NVML every ~1 ms while
+    the timed region runs (the same counters nvidia-smi's clocks line reads;
+    the timed region is milliseconds long, below nvidia-smi -lms granularity)."""
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.stop = threading.Event()
+        self.err = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._run, daemon=True)
+            self.thread.start()
+        except Exception as e:  # NVML missing: report unsampled, never fake
+            self.err = str(e)
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self.nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop.is_set():
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM), int(get_r(self.h))))
+            except Exception as e:
+                self.err = str(e)
+                return
+            time.sleep(0.001)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.nv is not None:
+            self.thread.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 3:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-                bits = int(parts[2], 16)
-            except ValueError:
-                continue
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0,
+                    "note": self.err}
+        reasons = set()
+        for _, bits in self.samples:
             for b, name in CLOCK_REASONS.items():
                 if bits & b and name != "gpu_idle":
                     reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(self.samples), "source": "nvml"}
 
 
 # --------------------------------------------------------------- CPU legs
@@ -255,21 +256,45 @@ def ours(args, cfg, world, rank, local_rank):
         host_g = [torch.empty(W, n, pin_memory=True) for _ in range(2)]
         for b in range(2):
             host_g[b].copy_(grads[b].cpu())
-        host_theta = torch.empty(n, pin_memory=True)
-        dev_g = torch.empty(W, n, device=dev)
-        d_e2e = ctx.step_desc(comp_code, dev_g, res, theta, 0.05, k, order, extra.get("q8_block", 256))
-        e_steps = max(3, min(args.steps, 10))
+        # double-buffered: H2D of step i+1 and D2H of step i-1's theta snapshot
+        # overlap step i on separate streams (PCIe is full duplex)
+        host_theta = [torch.empty(n, pin_memory=True) for _ in range(2)]
+        dev_g = [torch.empty(W, n, device=dev) for _ in range(2)]
+        snap = [torch.empty(n, device=dev) for _ in range(2)]
+        d_e2e = [ctx.step_desc(comp_code, dev_g[b], res, theta, 0.05, k, order,
+                               extra.get("q8_block", 256)) for b in range(2)]
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        in_done = [ev(), ev()]
+        comp_done = [ev(), ev()]
+        out_done = [ev(), ev()]
+        e_steps = max(4, min(args.steps, 12))
         barrier()
         torch.cuda.synchronize(dev)
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
+        s_in.wait_stream(stream)
         for i in range(e_steps):
-            dev_g.copy_(host_g[i % 2], non_blocking=True)
+            b = i % 2
+            with torch.cuda.stream(s_in):
+                if i >= 2:
+                    s_in.wait_event(comp_done[b])  # step i-2 consumed dev_g[b]
+                dev_g[b].copy_(host_g[b], non_blocking=True)
+                in_done[b].record(s_in)
+            stream.wait_event(in_done[b])
             if mode == "async":
-                gu[0] = ctx.async_round(d_e2e, extra.get("staleness", 2), gu[0])
+                gu[0] = ctx.async_round(d_e2e[b], extra.get("staleness", 2), gu[0])
             else:
-                ctx.sync_step(d_e2e)
-            host_theta.copy_(theta, non_blocking=True)
+                ctx.sync_step(d_e2e[b])
+            if i >= 2:
+                stream.wait_event(out_done[b])  # snapshot b drained to the host
+            snap[b].copy_(theta)
+            comp_done[b].record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(comp_done[b])
+                host_theta[b].copy_(snap[b], non_blocking=True)
+                out_done[b].record(s_out)
+        stream.wait_stream(s_out)
         f1.record(stream)
         torch.cuda.synchronize(dev)
         ctx.check()
@@ -315,9 +340,14 @@ def ours(args, cfg, world, rank, local_rank):
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 4 * n * W,
                 "d2h_bytes_per_step": 4 * n, "ms_per_step": e2e_ms,
-                "path": "psb_sync_step via the Python host API; pinned host gradient H2D + theta D2H per step"},
+                "path": "psb_sync_step via the Python host API; per step: pinned host gradient H2D, "
+                        "step, theta snapshot D2H to pinned host (copies double-buffered on side streams)"},
         "gpu_launches": launches,
     }
+    if comp.startswith("topk"):
+        st = ctx.topk_stats(0)
+        line["config"]["k1_last_call"] = {kk: st[kk] for kk in ("candidates", "predicted_valid",
+                                                                "calls", "misses", "margin_f")}
     if world == 1 and not args.no_cpu_baseline:
         n_s = min(n, 2_000_000)
         k_s = max(1, int(round(rho * n_s))) if comp.startswith("topk") else 0

@@ -107,6 +107,13 @@ PSB_API uint64_t psb_launch_count(const psb_ctx* ctx);
 PSB_API psb_status psb_profile_enable(psb_ctx* ctx, int enable);
 PSB_API psb_status psb_profile_read(psb_ctx* ctx, double* total_ms, uint64_t* launches);
 
+/* Diagnostics of the last K1 call and of `worker`'s threshold prediction:
+ * out[0] candidates, [1] k, [2] threshold key T, [3] ties taken at T,
+ * [4] first radix level resolved over candidates (0 = prediction valid),
+ * [5] predicted key used (0 = cold), [6] misses << 32 | calls, [7] bits of
+ * the margin factor f.  Synchronous (copies from the device). */
+PSB_API psb_status psb_topk_stats(psb_ctx* ctx, int worker, uint64_t* out8);
+
 /* Bytes of one worker's top-k payload block: u32 idx[k] | pad16 | val[k] | pad16
  * (TOPK, val of dtype) or u32 idx[k] | pad16 | i8 code[k] | pad16 |
  * f32 scale[ceil(k/128)] | pad16 (TOPK_Q8). */

@@ -251,7 +251,7 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
   topo_fields(topo, P, &dpn, &npr);
   const T coef = (T)(-lr);
   if (P == 1) {
-    const unsigned grid = (unsigned)std::min<size_t>((k + 255) / 256, (size_t)c->num_sms * 8);
+    const unsigned grid = (unsigned)std::min<size_t>((k + 255) / 256, (size_t)c->num_sms * 32);
     if (async_mode)
       k_sparse_apply1<T, true><<<grid, 256, 0, st>>>(v, k, (T)(-wscale_host[0]), theta, nullptr,
                                                      c->d_flags);

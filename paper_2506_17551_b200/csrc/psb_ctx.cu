@@ -82,6 +82,7 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   c->max_n = max_n;
   c->max_k = max_k < 1 ? 1 : max_k;
   c->max_workers = max_workers;
+  if (const char* np = getenv("PSB_NO_PREDICT")) c->predict = np[0] == '0';
   auto fail = [&](cudaError_t e) {
     psb_ctx_destroy(c);
     return e == cudaErrorMemoryAllocation ? PSB_ENOMEM : PSB_ECUDA;
@@ -104,9 +105,9 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   ALLOC(c->d_tw, sizeof(TopkWorker) * max_workers);
   ALLOC(c->d_hist1, sizeof(uint32_t) * PSB_HIST_BINS);
   ALLOC(c->d_histr, sizeof(uint32_t) * PSB_HIST_BINS);
-  ALLOC(c->d_tile_cnt, sizeof(uint32_t) * ntiles);
-  ALLOC(c->d_tile_gt, sizeof(uint32_t) * ntiles);
-  ALLOC(c->d_tile_eq, sizeof(uint32_t) * ntiles);
+  ALLOC(c->d_seg_cnt, sizeof(uint32_t) * PSB_FINAL_TPC_MAX);
+  ALLOC(c->d_seg_pre, sizeof(uint32_t) * (PSB_FINAL_TPC_MAX + 1));
+  ALLOC(c->d_cta, sizeof(unsigned long long) * PSB_FINAL_TPC_MAX);
   ALLOC(c->d_stage_idx, sizeof(uint32_t) * stage_cap);
   c->stage_val_bytes = sizeof(double) * stage_cap;
   ALLOC(c->d_stage_val, c->stage_val_bytes);
@@ -124,7 +125,7 @@ extern "C" void psb_ctx_destroy(psb_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   void* ptrs[] = {c->d_flags,    c->d_tk,        c->d_tw,        c->d_hist1,   c->d_histr,
-                  c->d_tile_cnt, c->d_tile_gt,   c->d_tile_eq,   c->d_stage_idx, c->d_stage_val,
+                  c->d_seg_cnt,  c->d_seg_pre,   c->d_cta,       c->d_stage_idx, c->d_stage_val,
                   c->d_seg_off,  c->d_partials,  c->d_gather,    c->d_work,    c->d_qmean};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -290,8 +291,10 @@ static psb_status check_desc(psb_ctx* c, const psb_step_desc* d) {
 
 // Compress this rank's W workers into their payload slots of the gather
 // buffer and exchange; on return the gather buffer holds all P payloads.
+// fuse_apply (P == 1, sync, top-k): the SGD update of the single payload is
+// done inside K1's final write (psb_topk_run_fused), no separate apply pass.
 static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaStream_t st,
-                                      uint8_t** payloads_out) {
+                                      uint8_t** payloads_out, bool fuse_apply = false) {
   const int W = d->workers, P = W * c->nranks;
   const size_t es = d->dtype == PSB_F64 ? 8 : 4;
   const size_t blk = psb_payload_bytes(d->compressor, d->dtype, d->k);
@@ -305,7 +308,11 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
     void* r = d->r ? reinterpret_cast<uint8_t*>(d->r) + (size_t)w * d->n * es : nullptr;
     uint32_t* idx = reinterpret_cast<uint32_t*>(slot);
     if (d->compressor == PSB_COMP_TOPK) {
-      s = psb_topk_run(c, d->dtype, w, g, r, d->n, d->k, idx, slot + psb_align16(d->k * 4), st);
+      if (fuse_apply)
+        s = psb_topk_run_fused(c, d->dtype, w, g, r, d->n, d->k, idx, slot + psb_align16(d->k * 4),
+                               d->theta, d->lr, d->mean_out, st);
+      else
+        s = psb_topk_run(c, d->dtype, w, g, r, d->n, d->k, idx, slot + psb_align16(d->k * 4), st);
     } else {
       int8_t* codes = reinterpret_cast<int8_t*>(slot + psb_align16(d->k * 4));
       float* scales = reinterpret_cast<float*>(slot + psb_align16(d->k * 4) + psb_align16(d->k));
@@ -416,8 +423,9 @@ extern "C" psb_status psb_sync_step(psb_ctx* c, const psb_step_desc* d, psb_stre
     case PSB_COMP_TOPK:
     case PSB_COMP_TOPK_Q8: {
       uint8_t* pl = nullptr;
-      s = compress_and_gather(c, d, st, &pl);
-      if (s) return s;
+      const bool fuse = P == 1 && d->compressor == PSB_COMP_TOPK;
+      s = compress_and_gather(c, d, st, &pl, fuse);
+      if (s || fuse) return s;
       return psb_sparse_mean_sgd(c, d->compressor, d->dtype, P, pl, d->k, d->order, &d->topo, d->lr,
                                  d->theta, d->n, d->mean_out, stream);
     }

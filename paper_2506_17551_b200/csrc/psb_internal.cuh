@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -15,6 +16,7 @@
 #define PSB_HIST_BINS 4096    // widest radix digit (12 bits)
 #define PSB_SCAN_THREADS 256  // K1 scan CTA size
 #define PSB_ITEMS 16          // elements per thread per K1 tile (f32)
+#define PSB_FINAL_TPC_MAX 2048  // max tiles per CTA and CTAs of k_final_count
 
 // ------------------------------------------------------------------ K1 state
 // Per-call scratch of the top-k selection (reset by k_topk_begin every call).
@@ -29,14 +31,19 @@ struct TopkScratch {
   unsigned long long match;   // entries matching `prefix`
   unsigned long long n;
   unsigned long long k;
-  uint32_t g_used;            // predicted level-1 digit used by this call
+  unsigned long long cand_count;  // entries in the candidate list
+  unsigned long long g_key;       // predicted key threshold used by this call (0 = none)
+  uint32_t start_level;           // first radix level resolved over the candidates
   uint32_t pad;
 };
 
-// Per-worker persistent selection history.
+// Per-worker persistent selection history: the next call's candidate set is
+// {key >= key(T_prev * f)}; f adapts so the set stays a little above k.
 struct TopkWorker {
-  uint32_t g_pred;  // level-1 digit predicted for the next call (0 = none)
-  uint32_t calls;
+  unsigned long long g_key;  // predicted key threshold for the next call (0 = none)
+  float f;                   // margin factor (0 = uninitialised)
+  uint32_t calls, misses;
+  uint32_t pad;
 };
 
 struct psb_ctx {
@@ -56,9 +63,9 @@ struct psb_ctx {
   TopkWorker* d_tw = nullptr;
   uint32_t* d_hist1 = nullptr;   // level-1 histogram
   uint32_t* d_histr = nullptr;   // refine-level histogram
-  uint32_t* d_tile_cnt = nullptr;
-  uint32_t* d_tile_gt = nullptr;
-  uint32_t* d_tile_eq = nullptr;
+  uint32_t* d_seg_cnt = nullptr;          // candidates per k_scan CTA segment
+  uint32_t* d_seg_pre = nullptr;          // exclusive prefix of d_seg_cnt
+  unsigned long long* d_cta = nullptr;    // per-CTA totals / prefixes
   uint32_t* d_stage_idx = nullptr;  // candidate staging, tile-segmented, capacity max_n
   void* d_stage_val = nullptr;      // f64 capacity
   size_t stage_val_bytes = 0;
@@ -76,6 +83,7 @@ struct psb_ctx {
   float* d_qmean = nullptr;
   // kernel timing (psb_profile_*)
   int prof = 0;
+  int predict = 1;  // K1 threshold prediction (PSB_NO_PREDICT=1 disables)
   std::vector<cudaEvent_t> prof_ev;  // pairs (start, stop)
   size_t prof_used = 0;
 };
@@ -175,6 +183,11 @@ __device__ __forceinline__ unsigned long long block_exscan_u64(unsigned long lon
 }
 
 // Launch helpers defined in the .cu files.
+// K1 with the single-worker SGD update fused into its final write (theta,
+// lr, mean_out nullable): theta[idx] = (-lr) * (val * 1) + theta[idx].
+psb_status psb_topk_run_fused(psb_ctx* c, psb_dtype dt, int worker, const void* g, void* r,
+                              size_t n, size_t k, uint32_t* idx_out, void* val_out, void* theta,
+                              double lr, void* mean_out, cudaStream_t st);
 psb_status psb_topk_run(psb_ctx* c, psb_dtype dt, int worker, const void* g, void* r, size_t n,
                         size_t k, uint32_t* idx_out, void* val_out, cudaStream_t st);
 psb_status psb_topk_q8_fix(psb_ctx* c, const float* r_unused, size_t k, const uint32_t* idx,

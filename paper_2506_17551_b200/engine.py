@@ -101,6 +101,17 @@ class Context:
     def launches(self) -> int:
         return int(self.lib.psb_launch_count(self.h))
 
+    def topk_stats(self, worker: int = 0) -> dict:
+        """Diagnostics of the last K1 call (psb_topk_stats)."""
+        out = (ctypes.c_uint64 * 8)()
+        self._ck(self.lib.psb_topk_stats(self.h, worker, out), "psb_topk_stats")
+        import struct
+        return {"candidates": int(out[0]), "k": int(out[1]), "threshold_key": int(out[2]),
+                "ties_taken": int(out[3]), "predicted_valid": int(out[4]) == 0,
+                "predicted_key": int(out[5]), "calls": int(out[6]) & 0xFFFFFFFF,
+                "misses": int(out[6]) >> 32,
+                "margin_f": struct.unpack("<f", struct.pack("<I", int(out[7]) & 0xFFFFFFFF))[0]}
+
     def profile_enable(self, on: bool = True) -> None:
         self._ck(self.lib.psb_profile_enable(self.h, 1 if on else 0), "psb_profile_enable")
 

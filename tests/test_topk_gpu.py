@@ -189,3 +189,27 @@ def test_full_size_properties_125m(cuda):
         expect_r = torch.where(sel, torch.zeros_like(p), p)
         assert torch.equal(r.view(torch.int32), expect_r.view(torch.int32))
     c.close()
+
+
+def test_threshold_prediction_engages_and_stays_exact(cuda):
+    """After the first (cold) call the worker predicts its threshold; the
+    predicted candidate set must be valid in steady state and results exact."""
+    from paper_2506_17551_b200.engine import Context
+    n, k = 1_000_000, 10_000
+    c = Context(n, k, 1)
+    r_host = np.zeros(n, dtype=np.float32)
+    r_dev = torch.zeros(n, dtype=torch.float32, device="cuda")
+    valid = []
+    for step in range(8):
+        g_host = O.generate("llmrec", 11, 0, step, n)
+        idx, val = c.ef_topk(torch.from_numpy(g_host).cuda(), r_dev, k)
+        oi, ov, _ = O.ef_topk(g_host, r_host, k)
+        assert np.array_equal(tnp(idx).view(np.uint32), oi)
+        assert np.array_equal(tnp(r_dev).view(np.uint32), r_host.view(np.uint32))
+        st = c.topk_stats(0)
+        valid.append(st["predicted_valid"])
+        assert st["candidates"] >= k
+    c.check()
+    assert not valid[0]          # cold call
+    assert sum(valid[2:]) >= 5   # steady state predicted
+    c.close()
