@@ -228,17 +228,31 @@ def ours(args, cfg, world, rank, local_rank):
         for i in range(args.warmup):
             step(i)
         ctx.check()
-        # ---- timed region: K steps, device-timed with events on our stream
+        # ---- timed region: K steps, device-timed with events on our stream.
+        # The K steps are captured once into a CUDA graph and replayed (the
+        # step's launch sequence is fixed; all control flow is device-side),
+        # with the dominant kernel bracketed by event-record nodes.
         barrier()
         torch.cuda.synchronize(dev)
         ctx.profile_enable(True)
         ctx.profile_read()
         l0 = ctx.launches
+        graph = None
+        if not args.eager:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                for i in range(args.steps):
+                    step(args.warmup + i)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize(dev)
         with ClockSampler(local_rank) as clk:
             e0.record(stream)
-            for i in range(args.steps):
-                step(args.warmup + i)
+            if graph is not None:
+                graph.replay()
+            else:
+                for i in range(args.steps):
+                    step(args.warmup + i)
             e1.record(stream)
             torch.cuda.synchronize(dev)
         barrier()
@@ -329,6 +343,7 @@ def ours(args, cfg, world, rank, local_rank):
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (counter-based mix64 LLM-rec gradients generated on device before timing)",
         "config": {"workload": name, "n_params": n, "k": k, "rho": rho, "workers_per_rank": W, "P": P,
+                   "launch": "eager" if args.eager else "cuda-graph of the K timed steps",
                    "compressor": comp, "order": order, "mode": mode,
                    "l2": f"inputs larger than L2: {NB} rotated {4 * n * W / 1e6:.0f} MB gradient buffers"},
         "roofline": {"bound": "hbm", "kernel": "k_scan<float,MODE_A> (EF add + level-1 histogram)",
@@ -346,7 +361,7 @@ def ours(args, cfg, world, rank, local_rank):
     }
     if comp.startswith("topk"):
         st = ctx.topk_stats(0)
-        line["config"]["k1_last_call"] = {kk: st[kk] for kk in ("candidates", "predicted_valid",
+        line["config"]["k1_last_call"] = {kk: st[kk] for kk in ("candidates", "predicted_valid", "first_radix_level",
                                                                 "calls", "misses", "margin_f")}
     if world == 1 and not args.no_cpu_baseline:
         n_s = min(n, 2_000_000)
@@ -371,6 +386,7 @@ def main():
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--rho", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="launch the timed steps eagerly (no CUDA graph)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

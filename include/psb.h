@@ -113,6 +113,9 @@ PSB_API psb_status psb_profile_read(psb_ctx* ctx, double* total_ms, uint64_t* la
  * [5] predicted key used (0 = cold), [6] misses << 32 | calls, [7] bits of
  * the margin factor f.  Synchronous (copies from the device). */
 PSB_API psb_status psb_topk_stats(psb_ctx* ctx, int worker, uint64_t* out8);
+/* GPU timestamps (ns) of the candidate-phase milestones of the last K1 call
+ * (diagnostics; entries after the last milestone are stale). */
+PSB_API psb_status psb_topk_phases(psb_ctx* ctx, uint64_t* out16);
 
 /* Bytes of one worker's top-k payload block: u32 idx[k] | pad16 | val[k] | pad16
  * (TOPK, val of dtype) or u32 idx[k] | pad16 | i8 code[k] | pad16 |

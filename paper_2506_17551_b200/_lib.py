@@ -80,6 +80,7 @@ _SIGS = {
     "psb_launch_count": (_u64, [_vp]),
     "psb_payload_bytes": (_sz, [_i, _i, _sz]),
     "psb_topk_stats": (_i, [_vp, _i, ctypes.POINTER(_u64)]),
+    "psb_topk_phases": (_i, [_vp, ctypes.POINTER(_u64)]),
     "psb_profile_enable": (_i, [_vp, _i]),
     "psb_profile_read": (_i, [_vp, ctypes.POINTER(_d), ctypes.POINTER(_u64)]),
     "psb_comm_unique_id": (_i, [_vp]),

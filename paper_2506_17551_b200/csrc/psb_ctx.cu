@@ -105,6 +105,7 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   ALLOC(c->d_tw, sizeof(TopkWorker) * max_workers);
   ALLOC(c->d_hist1, sizeof(uint32_t) * PSB_HIST_BINS);
   ALLOC(c->d_histr, sizeof(uint32_t) * PSB_HIST_BINS);
+  ALLOC(c->d_histd, sizeof(uint32_t) * 16384);
   ALLOC(c->d_seg_cnt, sizeof(uint32_t) * PSB_FINAL_TPC_MAX);
   ALLOC(c->d_seg_pre, sizeof(uint32_t) * (PSB_FINAL_TPC_MAX + 1));
   ALLOC(c->d_cta, sizeof(unsigned long long) * PSB_FINAL_TPC_MAX);
@@ -125,7 +126,7 @@ extern "C" void psb_ctx_destroy(psb_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   void* ptrs[] = {c->d_flags,    c->d_tk,        c->d_tw,        c->d_hist1,   c->d_histr,
-                  c->d_seg_cnt,  c->d_seg_pre,   c->d_cta,       c->d_stage_idx, c->d_stage_val,
+                  c->d_seg_cnt,  c->d_seg_pre,   c->d_cta,       c->d_histd,       c->d_stage_idx, c->d_stage_val,
                   c->d_seg_off,  c->d_partials,  c->d_gather,    c->d_work,    c->d_qmean};
   for (void* p : ptrs)
     if (p) cudaFree(p);

@@ -34,15 +34,19 @@ struct TopkScratch {
   unsigned long long cand_count;  // entries in the candidate list
   unsigned long long g_key;       // predicted key threshold used by this call (0 = none)
   uint32_t start_level;           // first radix level resolved over the candidates
-  uint32_t pad;
+  uint32_t spec_ok;               // predicted mode may pre-zero candidate residuals
+  unsigned long long phase_ns[16];  // k_cand phase timestamps (globaltimer, CTA 0)
 };
 
 // Per-worker persistent selection history: the next call's candidate set is
 // {key >= key(T_prev * f)}; f adapts so the set stays a little above k.
 struct TopkWorker {
   unsigned long long g_key;  // predicted key threshold for the next call (0 = none)
+  unsigned long long t_prev; // threshold key T of the previous call
   float f;                   // margin factor (0 = uninitialised)
+  float rho;                 // smoothed step-to-step drift of T (0 = uninitialised)
   uint32_t calls, misses;
+  float last_ratio;          // candidates / k of the previous call
   uint32_t pad;
 };
 
@@ -63,6 +67,7 @@ struct psb_ctx {
   TopkWorker* d_tw = nullptr;
   uint32_t* d_hist1 = nullptr;   // level-1 histogram
   uint32_t* d_histr = nullptr;   // refine-level histogram
+  uint32_t* d_histd = nullptr;   // (key - G) histogram of the predicted mode
   uint32_t* d_seg_cnt = nullptr;          // candidates per k_scan CTA segment
   uint32_t* d_seg_pre = nullptr;          // exclusive prefix of d_seg_cnt
   unsigned long long* d_cta = nullptr;    // per-CTA totals / prefixes
@@ -84,6 +89,7 @@ struct psb_ctx {
   // kernel timing (psb_profile_*)
   int prof = 0;
   int predict = 1;  // K1 threshold prediction (PSB_NO_PREDICT=1 disables)
+  int cand_smem[2] = {0, 0};  // dynamic shared memory of the cooperative k_cand (f32, f64)
   std::vector<cudaEvent_t> prof_ev;  // pairs (start, stop)
   size_t prof_used = 0;
 };

@@ -12,31 +12,40 @@
 // bits(|p|) (monotone for finite values and +-0).  The lowest-index tie-break
 // is exact because every candidate list is kept in index order.
 //
-//   k_topk_begin   1 CTA: reset per-call scratch, zero histograms.
-//   k_scan<A>      THE streaming pass (12N bytes: read g, read r, write p->r).
-//                  Predicted mode (the worker's previous call left a key
-//                  threshold G = key(T_prev * f)): index-ordered compaction of
-//                  every element with key >= G -- CTA b streams a contiguous
-//                  index range and appends to its own segment (block scan per
-//                  tile, no cross-CTA waits, no histogram atomics).  The last
-//                  CTA validates the prediction (count >= k) and prefix-sums
-//                  the segment sizes into one logical index-ordered list.
-//                  Cold mode (no prediction): level-1 histogram of key>>19 in
-//                  shared memory; the last CTA resolves digit b1 of the k-th key.
-//   k_scan<A2>     only if the prediction missed: full histogram pass (reads p).
-//   k_scan<D>      only in cold/miss mode: compaction of digit >= b1.
-//   k_refine<L>    radix levels over the candidate list (all levels in
-//                  predicted mode, levels 2.. in cold mode).
-//   k_final_count  per-CTA (gt, eq) counts vs the exact threshold key T; the
-//                  last CTA scans the CTA totals and predicts the next G.
-//   k_final_write  one packed (gt, eq) block scan per 1024 candidates gives each
-//                  element's output slot gt_before + min(eq_before, need_eq);
-//                  writes idx/val, r[idx] = +0 and, for a single worker, the
-//                  fused SGD update of theta[idx] (no separate apply pass).
+//   k_topk_begin  1 CTA: reset per-call scratch, zero histograms.
+//   k_scan<A>     THE streaming pass (12N bytes: read g, read r, write r).
+//                 Predicted mode (the worker's previous call left a key
+//                 threshold G = key(T_prev * rho * f)): index-ordered
+//                 compaction of every element with key >= G -- CTA b streams a
+//                 contiguous index range and appends to its own segment (block
+//                 scan per tile, no cross-CTA waits, no histogram atomics) --
+//                 and the residual of those candidates is written as +0
+//                 speculatively (most of them are selected).  The last CTA
+//                 validates the prediction (count >= k, hence T >= G) and
+//                 prefix-sums the segment sizes into one logical list.
+//                 Cold mode (no prediction): level-1 histogram of key>>19;
+//                 the last CTA resolves digit b1 of the k-th key.
+//   k_restore     only on a prediction miss: put p back for pass A's candidates.
+//   k_scan<A2>    only on a miss: full level-1 histogram pass (reads p).
+//   k_scan<D>     only in cold/miss mode: compaction of digit >= b1.
+//   k_cand        ONE cooperative kernel for the whole candidate phase
+//                 (psb_cand.inl): slices staged in shared memory, grid-wide
+//                 barriers instead of kernel boundaries; the exact threshold T
+//                 (predicted mode: two levels on key - G, 2048-ulp coarse bins
+//                 then ulps; cold mode: the remaining key radix levels),
+//                 per-CTA (gt, eq) counts and their scan, then the ordered
+//                 write: slot = gt_before + min(eq_before, need_eq); idx/val
+//                 out, residual fix-up (+0 or restore p) and, for a single
+//                 worker, the fused SGD update of theta[idx].
 // Every kernel is launched unconditionally and exits early from device-side
-// flags, so the sequence is CUDA-graph capturable and never syncs the host.
-// Results never depend on the prediction: a miss only costs the fallback.
+// flags, so the sequence never syncs the host.  Results never depend on the
+// prediction: a miss only costs the fallback passes.
+#include <cooperative_groups.h>
+#include <cuda_pipeline.h>
+
 #include "psb_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -57,7 +66,8 @@ __host__ __device__ constexpr int tile_elems() {
 }
 
 enum { MODE_A = 0, MODE_A2 = 1, MODE_D = 2 };
-enum { DONE_A = 0, DONE_A2 = 1, DONE_R = 2, DONE_F = 3, DONE_D = 4 };
+enum { DONE_A = 0, DONE_A2 = 1, DONE_D = 4 };
+
 
 // key <-> magnitude value, for the predicted threshold key(T * f)
 __device__ __forceinline__ unsigned long long scale_key(unsigned long long key, float f, float) {
@@ -65,6 +75,12 @@ __device__ __forceinline__ unsigned long long scale_key(unsigned long long key, 
 }
 __device__ __forceinline__ unsigned long long scale_key(unsigned long long key, float f, double) {
   return (unsigned long long)__double_as_longlong(__dmul_rn(__longlong_as_double((long long)key), (double)f));
+}
+__device__ __forceinline__ double to_mag(unsigned long long key, float) {
+  return (double)__uint_as_float((uint32_t)key);
+}
+__device__ __forceinline__ double to_mag(unsigned long long key, double) {
+  return __longlong_as_double((long long)key);
 }
 
 template <class T>
@@ -108,30 +124,36 @@ __device__ __forceinline__ void st_vec(float* p, const float (&x)[4]) {
 __device__ __forceinline__ void st_vec(double* p, const double (&x)[2]) {
   *reinterpret_cast<double2*>(p) = make_double2(x[0], x[1]);
 }
+__device__ __forceinline__ void st_vec_stream(float* p, const float (&x)[4]) {
+  __stcs(reinterpret_cast<float4*>(p), make_float4(x[0], x[1], x[2], x[3]));
+}
+__device__ __forceinline__ void st_vec_stream(double* p, const double (&x)[2]) {
+  __stcs(reinterpret_cast<double2*>(p), make_double2(x[0], x[1]));
+}
 
-// Resolve one radix level from a histogram (run by one whole CTA of
-// PSB_SCAN_THREADS threads).  Bins [max(lo,1), nbins) hold exact counts.
-// Finds the bin b containing the need-th largest entry (found, bin, above =
-// count in bins > b, cnt = h[b]).
+// Result of resolving one radix level: the bin b holding the need-th largest
+// entry, the count above it and its own count.
 struct LevelResult {
   int found;
   uint32_t bin;
   unsigned long long above;
   unsigned long long cnt;
-  unsigned long long total;  // sum over bins >= max(lo,1)
+  unsigned long long total;  // sum over the explicit bins
 };
 
-// `sh` is a shared-memory staging area of >= nbins words: the histogram is
-// copied in with coalesced, independent loads, then scanned in shared memory.
+// Resolve a <= 4096-bin histogram (one whole CTA).  Bins [max(lo,1), nbins)
+// are explicit; bin 0 is implicit (the caller derives it from the matching
+// total).  `sh` (>= nbins words of shared memory) stages the histogram with
+// coalesced loads; all scanning happens in shared memory.
 __device__ void resolve_level(const uint32_t* hist, uint32_t nbins, uint32_t lo,
                               unsigned long long need, unsigned long long* sh_warp,
                               LevelResult* out, uint32_t* sh) {
   const uint32_t t = threadIdx.x;
-  for (uint32_t b = t; b < nbins; b += PSB_SCAN_THREADS)
+  for (uint32_t b = t; b < nbins; b += blockDim.x)
     sh[b] = (b >= lo && b >= 1) ? __ldcg(hist + b) : 0u;
   if (t == 0) out->found = 0;
   __syncthreads();
-  const uint32_t B = nbins >= PSB_SCAN_THREADS ? nbins / PSB_SCAN_THREADS : 1;
+  const uint32_t B = nbins >= blockDim.x ? nbins / blockDim.x : 1;
   const uint32_t b0 = t * B;
   unsigned long long sum = 0;
   if (b0 < nbins)
@@ -157,6 +179,17 @@ __device__ void resolve_level(const uint32_t* hist, uint32_t nbins, uint32_t lo,
   __syncthreads();
 }
 
+// Shared-memory histogram increment aggregated across the warp (call with the
+// full warp converged): lanes with the same bin elect one leader that adds the
+// group's count.  Candidate keys crowd into a few bins near the threshold, so
+// plain per-lane atomics would serialize on one address.
+__device__ __forceinline__ void hist_add_agg(uint32_t* sh, uint32_t bin, bool active) {
+  const uint32_t am = __ballot_sync(0xffffffffu, active);
+  if (!active) return;
+  const uint32_t grp = __match_any_sync(am, bin);
+  if ((int)(threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&sh[bin], (uint32_t)__popc(grp));
+}
+
 __device__ __forceinline__ bool last_block(uint32_t* counter) {
   __shared__ int am_last;
   __threadfence();
@@ -174,7 +207,7 @@ __device__ void seg_prefix(const uint32_t* cnt, uint32_t nseg, uint32_t* pre, ui
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < nseg; b += blockDim.x) sh[b] = __ldcg(cnt + b);
   __syncthreads();
-  const uint32_t q = (nseg + PSB_SCAN_THREADS - 1) / PSB_SCAN_THREADS;
+  const uint32_t q = (nseg + blockDim.x - 1) / blockDim.x;
   const uint32_t b0 = threadIdx.x * q, b1 = min(nseg, b0 + q);
   unsigned long long local = 0;
   for (uint32_t b = b0; b < b1; ++b) local += sh[b];
@@ -207,6 +240,9 @@ __global__ void k_topk_begin(TopkScratch* s, TopkWorker* w, uint32_t* hist1, uin
     s->cand_count = 0;
     s->start_level = 1;
     s->g_key = predict ? w->g_key : 0ull;
+    // pre-zeroing the candidates' residual pays off while most candidates are
+    // selected (restores C - k < zero-writes k)
+    s->spec_ok = w->last_ratio < 2.0f ? 1u : 0u;
   }
 }
 
@@ -241,6 +277,8 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
     compact = gk > 0;
     hist = !compact;
   }
+  // speculative +0 residual for candidates (predicted mode, EF pass only)
+  const bool spec = MODE == MODE_A && compact && a.s->spec_ok;
 
   if (hist)
     for (int b = threadIdx.x; b < PSB_HIST_BINS; b += blockDim.x) sh_hist[b] = 0;
@@ -270,14 +308,18 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
         for (int j = 0; j < 4; ++j) {
           const size_t e = base + (size_t)(j * PSB_SCAN_THREADS + threadIdx.x) * VW;
           ld_vec_stream(src + e, gv[j]);
-          ld_vec(rr + e, rv[j]);
+          ld_vec_stream(rr + e, rv[j]);  // evict-first: keep L2 for the candidate list
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
+          T out[VW];
 #pragma unroll
-          for (int c = 0; c < VW; ++c) x[j][c] = add_rn(rv[j][c], gv[j][c]);
+          for (int c = 0; c < VW; ++c) {
+            x[j][c] = add_rn(rv[j][c], gv[j][c]);
+            out[c] = (spec && KO::key(x[j][c]) >= gk) ? T(0) : x[j][c];
+          }
           const size_t e = base + (size_t)(j * PSB_SCAN_THREADS + threadIdx.x) * VW;
-          st_vec(rr + e, x[j]);
+          st_vec_stream(rr + e, out);
         }
       } else {
 #pragma unroll
@@ -297,7 +339,7 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
             valid |= 1u << (j * VW + c);
             if (MODE == MODE_A && rr != nullptr) {
               v = add_rn(rr[e], src[e]);
-              rr[e] = v;
+              rr[e] = (spec && KO::key(v) >= gk) ? T(0) : v;
             } else {
               v = src[e];
             }
@@ -313,13 +355,12 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
 #pragma unroll
       for (int c = 0; c < VW; ++c) {
         const int bit = j * VW + c;
-        if ((valid >> bit) & 1u) {
-          const K key = KO::key(x[j][c]);
+        const bool ok = (valid >> bit) & 1u;
+        const K key = KO::key(x[j][c]);
+        const uint32_t d = (uint32_t)(key >> SH1);
+        if (hist) hist_add_agg(sh_hist, d, ok && d != 0);  // digit 0 is implicit
+        if (ok) {
           if (key >= KO::kInf) nonfinite = 1;
-          if (hist) {
-            const uint32_t d = (uint32_t)(key >> SH1);
-            if (d) atomicAdd(&sh_hist[d], 1u);
-          }
           if (key >= gk) fl |= 1u << bit;
         }
       }
@@ -388,10 +429,10 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
       }
       seg_prefix(a.seg_cnt, gridDim.x, a.seg_pre, sh_hist, sh_warp);
     } else if (threadIdx.x == 0) {
-      a.s->need_full_hist = 1;  // miss: rerun level 1 on all of p, then compact
+      a.s->need_full_hist = 1;  // miss: restore, rerun level 1 on all of p, then compact
       a.s->cand_count = 0;
       a.w->misses += 1;
-      a.w->f = a.w->f > 0.f ? 1.f - (1.f - a.w->f) * 2.f : 0.98f;  // widen the margin
+      a.w->f = a.w->f > 0.f ? 1.f - (1.f - a.w->f) * 1.5f : 0.97f;  // widen the margin
       if (a.w->f < 0.5f) a.w->f = 0.5f;
     }
     if (threadIdx.x == 0) a.w->calls += 1;
@@ -420,270 +461,20 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
   }
 }
 
-// ---------------------------------------------------- candidate list
+// Prediction missed: pass A speculatively stored +0 for its candidates; put p
+// back (segment b holds exactly those written by k_scan CTA b) before the
+// cold path re-reads p from r.
 template <class T>
-struct CandArgs {
-  TopkScratch* s;
-  TopkWorker* w;
-  uint32_t* histr;
-  const uint32_t* cand_idx;
-  const T* cand_val;
-  const uint32_t* seg_pre;  // nseg + 1 exclusive prefixes of the k_scan CTA segments
-  uint32_t nseg;
-  size_t seg_cap;           // segment stride (= elements streamed by one k_scan CTA)
-  unsigned long long* cta;  // per-CTA (gt | eq << 32) totals, then exclusive prefixes
-  uint32_t* idx_out;
-  T* val_out;
-  T* r;
-  T* theta;     // fused single-worker SGD update (nullable)
-  T* mean_out;  // with theta: dense mean at touched indices (nullable)
-  T coef;       // (T)(-lr)
-  uint32_t* flags;
-};
-
-// Flat view of the segmented candidate list: logical entry e (index order)
-// lies in segment s with pre[s] <= e < pre[s+1], physically at
-// s*cap + (e - pre[s]).  Work is split evenly over the logical range, so the
-// candidate phase is balanced whatever the data's spatial distribution.
-struct FlatMap {
-  const uint32_t* pre;  // shared-memory copy
-  uint32_t nseg;
-  size_t cap;
-  __device__ __forceinline__ uint32_t seg_of(uint32_t e) const {
-    uint32_t lo = 0, hi = nseg;  // pre[lo] <= e < pre[hi]
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (pre[mid] <= e) lo = mid;
-      else hi = mid;
-    }
-    return lo;
-  }
-};
-
-// Loads the segment prefixes into shared memory and returns this CTA's
-// logical range (chunks are multiples of 1024 entries).
-template <class T>
-__device__ __forceinline__ FlatMap flat_begin(const CandArgs<T>& a, uint32_t* sh_pre, uint32_t* lo,
-                                              uint32_t* hi) {
-  for (uint32_t b = threadIdx.x; b <= a.nseg; b += blockDim.x) sh_pre[b] = a.seg_pre[b];
-  __syncthreads();
-  const uint32_t C = sh_pre[a.nseg];
-  uint32_t chunk = (C + gridDim.x - 1) / gridDim.x;
-  chunk = (chunk + 1023u) & ~1023u;
-  *lo = min(C, blockIdx.x * chunk);
-  *hi = min(C, *lo + chunk);
-  FlatMap m;
-  m.pre = sh_pre;
-  m.nseg = a.nseg;
-  m.cap = a.seg_cap;
-  return m;
+__global__ void __launch_bounds__(PSB_SCAN_THREADS) k_restore(ScanArgs<T> a) {
+  constexpr int TILE = tile_elems<T>();
+  if (!a.s->need_full_hist || !a.s->spec_ok || a.r == nullptr) return;
+  const size_t base = (size_t)blockIdx.x * a.tpc * TILE;
+  const uint32_t cnt = a.seg_cnt[blockIdx.x];
+  for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) a.r[a.cand_idx[base + j]] = a.cand_val[base + j];
 }
 
-// Physical positions of the 4 consecutive logical entries e0..e0+3 (< hi).
-__device__ __forceinline__ void flat_pos4(const FlatMap& m, uint32_t e0, uint32_t hi, size_t (&pos)[4]) {
-  uint32_t sg = e0 < hi ? m.seg_of(e0) : 0;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const uint32_t e = e0 + c;
-    pos[c] = 0;
-    if (e < hi) {
-      while (m.pre[sg + 1] <= e) ++sg;
-      pos[c] = (size_t)sg * m.cap + (e - m.pre[sg]);
-    }
-  }
-}
-
-template <class T>
-__global__ void __launch_bounds__(PSB_SCAN_THREADS) k_refine(CandArgs<T> a, int level) {
-  typedef KeyOf<T> KO;
-  typedef typename KO::K K;
-  __shared__ uint32_t sh_hist[PSB_HIST_BINS];
-  __shared__ uint32_t sh_pre[PSB_FINAL_TPC_MAX + 1];
-  __shared__ unsigned long long sh_warp[32];
-  __shared__ LevelResult sh_res;
-
-  if ((uint32_t)level < a.s->start_level) return;  // resolved by the streaming pass
-  const int pshift = level ? KO::shift(level - 1) : (int)(sizeof(K) * 8 - 1);
-  const int shift = KO::shift(level);
-  const uint32_t nbins = 1u << KO::width(level);
-  const K prefix = (K)a.s->prefix;
-
-  for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) sh_hist[b] = 0;
-  uint32_t lo, hi;
-  const FlatMap m = flat_begin(a, sh_pre, &lo, &hi);
-  for (uint32_t e0 = lo + 4 * threadIdx.x; e0 < hi; e0 += 4 * PSB_SCAN_THREADS) {
-    size_t pos[4];
-    flat_pos4(m, e0, hi, pos);
-    T v[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) v[c] = e0 + c < hi ? a.cand_val[pos[c]] : T(0);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const K key = KO::key(v[c]);
-      if (e0 + c < hi && (key >> pshift) == prefix) {
-        const uint32_t d = (uint32_t)(key >> shift) & (nbins - 1);
-        if (d) atomicAdd(&sh_hist[d], 1u);
-      }
-    }
-  }
-  __syncthreads();
-  for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) {
-    const uint32_t h = sh_hist[b];
-    if (h) atomicAdd(&a.histr[b], h);
-  }
-  if (!last_block(&a.s->done[DONE_R])) return;
-
-  const unsigned long long need = a.s->need, match = a.s->match;
-  __syncthreads();
-  resolve_level(a.histr, nbins, 1, need, sh_warp, &sh_res, sh_hist);
-  if (threadIdx.x == 0) {
-    const LevelResult& R = sh_res;
-    uint32_t bin;
-    unsigned long long above, cnt;
-    if (R.found) {
-      bin = R.bin;
-      above = R.above;
-      cnt = R.cnt;
-    } else {
-      bin = 0;
-      above = R.total;
-      cnt = match - R.total;
-    }
-    a.s->prefix = level ? ((a.s->prefix << KO::width(level)) | bin) : bin;
-    a.s->need = need - above;
-    a.s->match = cnt;
-    a.s->done[DONE_R] = 0;  // next level reuses the counter (stream-ordered)
-  }
-  __syncthreads();
-  for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) a.histr[b] = 0;
-}
-
-// Counts (key > T, key == T) per CTA chunk; the last CTA turns the totals
-// into exclusive prefixes (packed gt | eq << 32; each field < 2^32) -- offsets
-// depend only on counts, so the output order is deterministic -- and sets the
-// worker's next predicted threshold G = key(T * f), adapting f so the next
-// candidate set stays between ~1.1k and ~2k.
-template <class T>
-__global__ void __launch_bounds__(PSB_SCAN_THREADS) k_final_count(CandArgs<T> a) {
-  typedef KeyOf<T> KO;
-  typedef typename KO::K K;
-  __shared__ unsigned long long sh_c[PSB_FINAL_TPC_MAX];
-  __shared__ uint32_t sh_pre[PSB_FINAL_TPC_MAX + 1];
-  __shared__ unsigned long long sh_warp[32];
-  const K T_key = (K)a.s->prefix;
-  uint32_t lo, hi;
-  const FlatMap m = flat_begin(a, sh_pre, &lo, &hi);
-  uint32_t gt = 0, eq = 0;
-  for (uint32_t e0 = lo + 4 * threadIdx.x; e0 < hi; e0 += 4 * PSB_SCAN_THREADS) {
-    size_t pos[4];
-    flat_pos4(m, e0, hi, pos);
-    T v[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) v[c] = e0 + c < hi ? a.cand_val[pos[c]] : T(0);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const K key = KO::key(v[c]);
-      const bool ok = e0 + c < hi;
-      gt += ok && key > T_key;
-      eq += ok && key == T_key;
-    }
-  }
-  unsigned long long total;
-  block_exscan_u64((unsigned long long)gt | ((unsigned long long)eq << 32), sh_warp, &total);
-  if (threadIdx.x == 0) a.cta[blockIdx.x] = total;
-  if (!last_block(&a.s->done[DONE_F])) return;
-  for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) sh_c[b] = __ldcg(a.cta + b);
-  __syncthreads();
-  const uint32_t qb = (gridDim.x + PSB_SCAN_THREADS - 1) / PSB_SCAN_THREADS;
-  const uint32_t b0 = threadIdx.x * qb, b1 = min(gridDim.x, b0 + qb);
-  unsigned long long local = 0;
-  for (uint32_t b = b0; b < b1; ++b) local += sh_c[b];
-  unsigned long long run = block_exscan_u64(local, sh_warp, &total);
-  for (uint32_t b = b0; b < b1; ++b) {
-    const unsigned long long c = sh_c[b];
-    a.cta[b] = run;
-    run += c;
-  }
-  if (threadIdx.x == 0) {
-    // next call's prediction; candidates this call = a.s->cand_count
-    float f = a.w->f > 0.f ? a.w->f : 0.98f;
-    const double ratio = (double)__ldcg(&a.s->cand_count) / (double)a.s->k;
-    if (a.s->start_level == 0) {            // this call was predicted (and valid)
-      if (ratio > 2.0) f = 1.f - (1.f - f) * 0.5f;        // too many candidates: tighten
-      else if (ratio < 1.1) f = 1.f - (1.f - f) * 1.5f;   // thin margin: widen
-    }
-    f = fminf(fmaxf(f, 0.5f), 0.9995f);
-    a.w->f = f;
-    a.w->g_key = (T_key == 0 || T_key >= KO::kInf) ? 0ull : scale_key(T_key, f, T(0));
-  }
-}
-
-// One packed (gt, eq) block scan per 1024 candidates: element e is selected
-// iff key > T or (key == T and eq_before(e) < need_eq), and lands at slot
-// gt_before(e) + min(eq_before(e), need_eq) -- index order preserved.
-template <class T>
-__global__ void __launch_bounds__(PSB_SCAN_THREADS) k_final_write(CandArgs<T> a) {
-  typedef KeyOf<T> KO;
-  typedef typename KO::K K;
-  __shared__ uint32_t sh_pre[PSB_FINAL_TPC_MAX + 1];
-  __shared__ unsigned long long sh_warp[32];
-  __shared__ uint32_t sh_bad;
-  const K T_key = (K)a.s->prefix;
-  const unsigned long long need_eq = a.s->need;
-  if (threadIdx.x == 0) sh_bad = 0;
-  uint32_t lo, hi;
-  const FlatMap m = flat_begin(a, sh_pre, &lo, &hi);
-  unsigned long long run = a.cta[blockIdx.x];  // (gt | eq << 32) before this chunk
-  bool bad = false;
-  for (uint32_t base = lo; base < hi; base += 4 * PSB_SCAN_THREADS) {
-    const uint32_t e0 = base + 4 * threadIdx.x;
-    size_t pos[4];
-    flat_pos4(m, e0, hi, pos);
-    T v[4];
-    uint32_t id[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      v[c] = e0 + c < hi ? a.cand_val[pos[c]] : T(0);
-      id[c] = e0 + c < hi ? a.cand_idx[pos[c]] : 0u;
-    }
-    uint32_t gtm = 0, eqm = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if (e0 + c < hi) {
-        const K key = KO::key(v[c]);
-        gtm |= (key > T_key ? 1u : 0u) << c;
-        eqm |= (key == T_key ? 1u : 0u) << c;
-      }
-    }
-    const unsigned long long mine = (unsigned long long)__popc(gtm) | ((unsigned long long)__popc(eqm) << 32);
-    unsigned long long tot;
-    unsigned long long before = run + block_exscan_u64(mine, sh_warp, &tot);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const unsigned long long gt_b = before & 0xffffffffull, eq_b = before >> 32;
-      const bool gt = (gtm >> c) & 1u, eq = (eqm >> c) & 1u;
-      if (gt || (eq && eq_b < need_eq)) {
-        const unsigned long long slot = gt_b + (eq_b < need_eq ? eq_b : need_eq);
-        const uint32_t i = id[c];
-        a.idx_out[slot] = i;
-        a.val_out[slot] = v[c];
-        if (a.r) a.r[i] = T(0);
-        if (a.theta) {
-          const T mean = mul_rn(v[c], T(1));  // P = 1: mean = v * (1/1)
-          const T th = add_rn(mul_rn(a.coef, mean), a.theta[i]);
-          a.theta[i] = th;
-          if (a.mean_out) a.mean_out[i] = mean;
-          bad |= !is_finite(th);
-        }
-      }
-      before += (unsigned long long)gt | ((unsigned long long)eq << 32);
-    }
-    run += tot;
-  }
-  if (bad) sh_bad = 1;
-  __syncthreads();
-  if (threadIdx.x == 0 && sh_bad) atomicOr(a.flags, 1u);
-}
+// ---------------------------------------------------- candidate phase
+#include "psb_cand.inl"
 
 template <class T>
 psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k,
@@ -717,6 +508,7 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   if (c->prof) cudaEventRecord(psb_prof_event(c), st);
   k_scan<T, MODE_A><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
   if (c->prof) cudaEventRecord(psb_prof_event(c), st);
+  k_restore<T><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
   k_scan<T, MODE_A2><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
   k_scan<T, MODE_D><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
 
@@ -737,12 +529,25 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   b.mean_out = mean_out;
   b.coef = (T)(-lr);
   b.flags = c->d_flags;
-  const uint32_t cgrid = (uint32_t)std::max<size_t>(1, std::min<size_t>((n + 4095) / 4096, (size_t)c->num_sms * 4));
-  for (int level = 0; level < KeyOf<T>::kLevels; ++level)
-    k_refine<T><<<cgrid, PSB_SCAN_THREADS, 0, st>>>(b, level);
-  k_final_count<T><<<cgrid, PSB_SCAN_THREADS, 0, st>>>(b);
-  k_final_write<T><<<cgrid, PSB_SCAN_THREADS, 0, st>>>(b);
-  c->launches += 6 + KeyOf<T>::kLevels;
+  // cooperative grid: one CTA per SM, the rest of shared memory stages the slice
+  const int slot = sizeof(T) == 8;
+  if (c->cand_smem[slot] == 0) {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k_cand<T>);
+    const int dyn = optin - (int)fa.sharedSizeBytes - 1024;
+    cudaFuncSetAttribute(k_cand<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    c->cand_smem[slot] = dyn;
+  }
+  const int dyn = c->cand_smem[slot];
+  b.stage_cap = (uint32_t)(((size_t)dyn - kCoarseBins * 4) / (sizeof(T) + 4)) & ~3u;
+  const uint32_t cgrid = (uint32_t)std::max<size_t>(1, std::min<size_t>((n + 4095) / 4096, (size_t)c->num_sms));
+  void* kargs[] = {&b};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_cand<T>, dim3(cgrid), dim3(kCandThreads),
+                                              kargs, (size_t)dyn, st);
+  if (e != cudaSuccess) return psb_cuda_err(c, e, "psb_ef_topk (cooperative launch)");
+  c->launches += 6;
   PSB_LAUNCH_CHECK(c, "psb_ef_topk");
   return PSB_OK;
 }
@@ -818,6 +623,15 @@ psb_status psb_topk_q8_fix(psb_ctx* c, const float*, size_t k, const uint32_t* i
   return PSB_OK;
 }
 
+extern "C" psb_status psb_topk_phases(psb_ctx* c, uint64_t* out16) {
+  PSB_REQUIRE(c, c != nullptr && out16 != nullptr, "psb_topk_phases: null argument");
+  TopkScratch s;
+  cudaError_t e = cudaMemcpy(&s, c->d_tk, sizeof(s), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return psb_cuda_err(c, e, "psb_topk_phases");
+  for (int i = 0; i < 16; ++i) out16[i] = s.phase_ns[i];
+  return PSB_OK;
+}
+
 extern "C" psb_status psb_topk_stats(psb_ctx* c, int worker, uint64_t* out8) {
   PSB_REQUIRE(c, c != nullptr && out8 != nullptr, "psb_topk_stats: null argument");
   PSB_REQUIRE(c, worker >= 0 && worker < c->max_workers, "psb_topk_stats: worker out of range");
@@ -832,7 +646,8 @@ extern "C" psb_status psb_topk_stats(psb_ctx* c, int worker, uint64_t* out8) {
   out8[1] = s.k;
   out8[2] = s.prefix;       // exact threshold key T of the last call
   out8[3] = s.need;         // ties at T taken (lowest indices)
-  out8[4] = s.start_level;  // 0: predicted candidate set was valid
+  out8[4] = ((s.g_key != 0 && !s.need_full_hist) ? 0 : 1) |  // 0: predicted set was valid
+            ((uint64_t)s.start_level << 8);                  // 100+: T found on key - G
   out8[5] = s.g_key;        // predicted key used by the last call (0 = cold)
   out8[6] = ((uint64_t)w.misses << 32) | w.calls;
   out8[7] = fbits;          // margin factor f for the next call

@@ -107,10 +107,18 @@ class Context:
         self._ck(self.lib.psb_topk_stats(self.h, worker, out), "psb_topk_stats")
         import struct
         return {"candidates": int(out[0]), "k": int(out[1]), "threshold_key": int(out[2]),
-                "ties_taken": int(out[3]), "predicted_valid": int(out[4]) == 0,
+                "ties_taken": int(out[3]), "predicted_valid": (int(out[4]) & 0xFF) == 0,
+                "first_radix_level": int(out[4]) >> 8,
                 "predicted_key": int(out[5]), "calls": int(out[6]) & 0xFFFFFFFF,
                 "misses": int(out[6]) >> 32,
                 "margin_f": struct.unpack("<f", struct.pack("<I", int(out[7]) & 0xFFFFFFFF))[0]}
+
+    def topk_phases_us(self) -> list:
+        """Durations (us) between the candidate-phase milestones of the last K1 call."""
+        out = (ctypes.c_uint64 * 16)()
+        self._ck(self.lib.psb_topk_phases(self.h, out), "psb_topk_phases")
+        t = [int(x) for x in out]
+        return [(t[i + 1] - t[i]) / 1e3 for i in range(15) if t[i + 1] >= t[i] > 0]
 
     def profile_enable(self, on: bool = True) -> None:
         self._ck(self.lib.psb_profile_enable(self.h, 1 if on else 0), "psb_profile_enable")
