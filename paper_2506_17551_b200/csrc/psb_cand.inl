@@ -6,34 +6,40 @@
 // the slice fits (it does for top-k ratios up to a few percent), stages it in
 // shared memory once; every following pass -- the threshold levels, the
 // (gt, eq) counts and the ordered write -- then runs out of shared memory.
-// Grid-wide barriers replace kernel boundaries.
+// One grid-wide barrier per level replaces a kernel boundary: after it, EVERY
+// CTA resolves the level from the global histogram itself (same data, same
+// deterministic result), so no second barrier is needed to broadcast it.
 //
 // Threshold T:
 //   predicted mode (f32): coarse histogram of (key - G) >> kCoarseShift
-//     (4096 bins, the top one an implicit overflow), then the fine histogram
-//     of (key - G) & (2^kCoarseShift - 1) inside the chosen coarse bin.
+//     (4096 bins, the top one collecting everything an octave or more above
+//     G), then the fine histogram of (key - G) & (2^kCoarseShift - 1) inside
+//     the chosen coarse bin.
 //   otherwise: the remaining key radix levels (cold mode starts at level 1,
 //     f64 and the overflow case at level 0).
 // Write: slot = gt_before + min(eq_before, need_eq) from one packed (gt, eq)
-//   block scan per sub-tile, so the output keeps index order; residual
-//   fix-up and the fused single-worker SGD update of theta happen here.
+//   block scan per sub-tile, so the output keeps index order; then a
+//   barrier-free loop does the scattered part (residual fix-up, and the fused
+//   single-worker SGD update theta[idx] += (-lr) * (val * 1)).
 
 constexpr int kCandThreads = 512;
 constexpr uint32_t kCoarseBins = 4096;
 constexpr int kCoarseShift = 11;  // 2048-ulp coarse bins: 4095 of them span one octave above G
+constexpr uint32_t kLevelHist = 4096;  // words per level histogram buffer
+constexpr int kHistCoarse = 8, kHistFine = 9, kNumLevelHists = 10;  // radix levels use 0..7
 
 template <class T>
 struct CandArgs {
   TopkScratch* s;
   TopkWorker* w;
-  uint32_t* histr;  // <= 4096-bin global histogram (coarse, fine or radix level)
+  uint32_t* hlev;  // kNumLevelHists x kLevelHist global histograms (zero between calls)
   const uint32_t* cand_idx;
   const T* cand_val;
   const uint32_t* seg_pre;  // nseg + 1 exclusive prefixes of the k_scan CTA segments
   uint32_t nseg;
   size_t seg_cap;           // segment stride (= elements streamed by one k_scan CTA)
   uint32_t stage_cap;       // entries of the shared-memory staging area
-  unsigned long long* cta;  // per-CTA (gt | eq << 32) totals, then exclusive prefixes
+  unsigned long long* cta;  // per-CTA (gt | eq << 32) totals
   uint32_t* idx_out;
   T* val_out;
   T* r;
@@ -69,15 +75,18 @@ template <class T>
 __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   typedef KeyOf<T> KO;
   typedef typename KO::K K;
+  constexpr uint32_t kNoSlot = 0xffffffffu;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char dsm[];
-  uint32_t* sh_h = reinterpret_cast<uint32_t*>(dsm);                  // kCoarseBins words
-  T* st_val = reinterpret_cast<T*>(dsm + kCoarseBins * 4);             // stage_cap values
-  uint32_t* st_idx = reinterpret_cast<uint32_t*>(st_val + a.stage_cap);  // stage_cap indices
+  uint32_t* sh_h = reinterpret_cast<uint32_t*>(dsm);                      // kCoarseBins words
+  T* st_val = reinterpret_cast<T*>(dsm + kCoarseBins * 4);                 // stage_cap values
+  uint32_t* st_idx = reinterpret_cast<uint32_t*>(st_val + a.stage_cap);    // stage_cap indices
+  uint32_t* st_slot = st_idx + a.stage_cap;                                // stage_cap output slots
   __shared__ uint32_t sh_pre[PSB_FINAL_TPC_MAX + 1];
   __shared__ unsigned long long sh_warp[32];
   __shared__ LevelResult sh_res;
   __shared__ uint32_t sh_bad;
+  __shared__ unsigned long long sh_base;
 
   TopkScratch* s = a.s;
   const unsigned long long k = s->k;
@@ -149,8 +158,12 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       }
     }
   };
-  // One histogram pass over the slice: digit(key) for matching keys.
-  auto hist_pass = [&](uint32_t nbins, auto digit_of) {
+  // One histogram pass over the slice (digit(key) for matching keys), flushed
+  // into global histogram `g`; then the grid barrier; then every CTA resolves
+  // the level from `g`: bin holding the need-th largest (bin 0 implicit).
+  auto level_pass = [&](uint32_t* g, uint32_t nbins, unsigned long long need, unsigned long long match,
+                        auto digit_of, uint32_t* bin, unsigned long long* above,
+                        unsigned long long* bcnt) {
     for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) sh_h[b] = 0;
     __syncthreads();
     for (uint32_t base = 0; base < cnt; base += 4 * kCandThreads) {
@@ -168,105 +181,74 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
     __syncthreads();
     for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) {
       const uint32_t h = sh_h[b];
-      if (h) atomicAdd(&a.histr[b], h);
+      if (h) atomicAdd(&g[b], h);
     }
-  };
-  // CTA 0 resolves a level: bin holding the need-th largest (implicit bin 0).
-  auto resolve0 = [&](uint32_t nbins, unsigned long long need, unsigned long long match,
-                      uint32_t* bin, unsigned long long* above, unsigned long long* bcnt) {
-    resolve_level(a.histr, nbins, 1, need, sh_warp, &sh_res, sh_h);
+    grid.sync();
+    phase();
+    resolve_level(g, nbins, 1, need, sh_warp, &sh_res, sh_h);
     *bin = sh_res.found ? sh_res.bin : 0u;
     *above = sh_res.found ? sh_res.above : sh_res.total;
     *bcnt = sh_res.found ? sh_res.cnt : match - sh_res.total;
-    for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) a.histr[b] = 0;
   };
 
   const bool pred = s->g_key != 0 && !s->need_full_hist;  // predicted candidate set valid
   const bool spec = pred && s->spec_ok;                    // pass A zeroed all candidates
   uint32_t level = s->start_level;
+  K prefix = (K)s->prefix;
+  unsigned long long need = s->need, match = s->match;
+  bool delta = false;
 
-  // ---- exact threshold T
+  // ---- exact threshold T (state identical in every CTA)
   if (sizeof(T) == 4 && pred && level == 0) {
     const K G = (K)s->g_key;
+    uint32_t cb;
+    unsigned long long above, bcnt;
     // coarse digit min((key - G) >> kCoarseShift, 4095): the top bin collects
-    // every key an octave or more above G (overflow); digit 0 is implicit.
-    hist_pass(kCoarseBins, [&](K key, uint32_t* d) {
-      const K dl = (key - G) >> kCoarseShift;
-      *d = dl < (K)(kCoarseBins - 1) ? (uint32_t)dl : kCoarseBins - 1;
-      return *d != 0;  // coarse digit 0 is implicit (C - sum of the others)
-    });
-    grid.sync();
-    phase();
-    if (blockIdx.x == 0) {
-      uint32_t bin;
-      unsigned long long above, bcnt;
-      resolve0(kCoarseBins, k, C, &bin, &above, &bcnt);
-      if (threadIdx.x == 0) {
-        if (bin < kCoarseBins - 1) {
-          s->b1 = bin;
-          s->need = k - above;
-          s->match = bcnt;
-          s->start_level = 100;  // fine level next
-        }  // else T is an octave above G: fall back to the key radix levels
-      }
-    }
-    grid.sync();
-    phase();
-    level = s->start_level;
-    if (level == 100) {
-      const K cb = (K)s->b1;
-      hist_pass(1u << kCoarseShift, [&](K key, uint32_t* d) {
-        const K dl = key - G;
-        *d = (uint32_t)(dl & ((1u << kCoarseShift) - 1));
-        return (dl >> kCoarseShift) == cb && *d != 0;  // fine digit 0 is implicit
-      });
-      grid.sync();
-      phase();
-      if (blockIdx.x == 0) {
-        uint32_t bin;
-        unsigned long long above, bcnt;
-        const unsigned long long need = s->need;
-        resolve0(1u << kCoarseShift, need, s->match, &bin, &above, &bcnt);
-        if (threadIdx.x == 0) {
-          s->prefix = (unsigned long long)(G + (cb << kCoarseShift) + (K)bin);  // exact T
-          s->need = need - above;
-          s->start_level = KO::kLevels;
-        }
-      }
-      grid.sync();
-      phase();
+    // every key an octave or more above G; digit 0 is implicit (C - others).
+    level_pass(a.hlev + kHistCoarse * kLevelHist, kCoarseBins, k, C,
+               [&](K key, uint32_t* d) {
+                 const K dl = (key - G) >> kCoarseShift;
+                 *d = dl < (K)(kCoarseBins - 1) ? (uint32_t)dl : kCoarseBins - 1;
+                 return *d != 0;
+               },
+               &cb, &above, &bcnt);
+    if (cb < kCoarseBins - 1) {
+      uint32_t fb;
+      unsigned long long fabove, fcnt;
+      level_pass(a.hlev + kHistFine * kLevelHist, 1u << kCoarseShift, k - above, bcnt,
+                 [&](K key, uint32_t* d) {
+                   const K dl = key - G;
+                   *d = (uint32_t)(dl & ((1u << kCoarseShift) - 1));
+                   return (dl >> kCoarseShift) == (K)cb && *d != 0;  // fine digit 0 implicit
+                 },
+                 &fb, &fabove, &fcnt);
+      prefix = G + ((K)cb << kCoarseShift) + (K)fb;  // exact T
+      need = k - above - fabove;
       level = KO::kLevels;
-    }
+      delta = true;
+    }  // else T is an octave or more above G: the key radix levels from level 0
   }
   for (; level < (uint32_t)KO::kLevels; ++level) {  // key radix levels
     const int pshift = level ? KO::shift(level - 1) : (int)(sizeof(K) * 8 - 1);
     const int shift = KO::shift(level);
     const uint32_t nbins = 1u << KO::width(level);
-    const K prefix = (K)s->prefix;
-    hist_pass(nbins, [&](K key, uint32_t* d) {
-      *d = (uint32_t)(key >> shift) & (nbins - 1);
-      return (key >> pshift) == prefix && *d != 0;  // digit 0 is implicit
-    });
-    grid.sync();
-    phase();
-    if (blockIdx.x == 0) {
-      uint32_t bin;
-      unsigned long long above, bcnt;
-      const unsigned long long need = s->need;
-      resolve0(nbins, need, s->match, &bin, &above, &bcnt);
-      if (threadIdx.x == 0) {
-        s->prefix = level ? ((s->prefix << KO::width(level)) | bin) : bin;
-        s->need = need - above;
-        s->match = bcnt;
-      }
-    }
-    grid.sync();
-    phase();
+    const K pf = prefix;
+    uint32_t bin;
+    unsigned long long above, bcnt;
+    level_pass(a.hlev + level * kLevelHist, nbins, need, match,
+               [&](K key, uint32_t* d) {
+                 *d = (uint32_t)(key >> shift) & (nbins - 1);
+                 return (key >> pshift) == pf && *d != 0;  // digit 0 implicit
+               },
+               &bin, &above, &bcnt);
+    prefix = level ? ((prefix << KO::width(level)) | bin) : bin;
+    need -= above;
+    match = bcnt;
   }
+  const K T_key = prefix;
+  const unsigned long long need_eq = need;
 
-  // ---- (gt, eq) counts per CTA and their exclusive scan
-  const K T_key = (K)s->prefix;
-  const unsigned long long need_eq = s->need;
+  // ---- (gt, eq) counts per CTA; every CTA sums the totals of the CTAs before it
   {
     uint32_t gt = 0, eq = 0;
     for (uint32_t base = 0; base < cnt; base += 4 * kCandThreads) {
@@ -287,22 +269,20 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   }
   grid.sync();
   phase();
-  if (blockIdx.x == 0) {
-    unsigned long long* sh_c = reinterpret_cast<unsigned long long*>(sh_h);  // gridDim.x <= 2048
-    for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) sh_c[b] = __ldcg(a.cta + b);
-    __syncthreads();
-    const uint32_t qb = (gridDim.x + blockDim.x - 1) / blockDim.x;
-    const uint32_t b0 = threadIdx.x * qb, b1 = min(gridDim.x, b0 + qb);
-    unsigned long long local = 0;
-    for (uint32_t b = b0; b < b1; ++b) local += sh_c[b];
+  {
+    unsigned long long part = 0;
+    for (uint32_t b = threadIdx.x; b < blockIdx.x; b += blockDim.x) part += __ldcg(a.cta + b);
     unsigned long long total;
-    unsigned long long run = block_exscan_u64(local, sh_warp, &total);
-    for (uint32_t b = b0; b < b1; ++b) {
-      const unsigned long long c = sh_c[b];
-      a.cta[b] = run;
-      run += c;
-    }
+    block_exscan_u64(part, sh_warp, &total);
+    if (threadIdx.x == 0) sh_base = total;
+  }
+  if (blockIdx.x == 0) {
+    // every CTA has read the level histograms: clear them for the next call
+    for (uint32_t b = threadIdx.x; b < kNumLevelHists * kLevelHist; b += blockDim.x) a.hlev[b] = 0;
     if (threadIdx.x == 0) {
+      s->prefix = T_key;  // diagnostics (psb_topk_stats)
+      s->need = need_eq;
+      if (delta) s->start_level = 100;  // T found on key - G
       // Next call's prediction G = key(T * rho * f): rho tracks the
       // threshold's drift (error feedback makes it creep up), f is a safety
       // margin adapted so the candidate set stays a little above k.
@@ -326,12 +306,26 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       w->g_key = (T_key == 0 || T_key >= KO::kInf) ? 0ull : scale_key(T_key, f * rho, T(0));
     }
   }
-  grid.sync();
-  phase();
+  __syncthreads();
 
-  // ---- ordered write
-  unsigned long long run = a.cta[blockIdx.x];  // (gt | eq << 32) before this slice
+  // ---- ordered write.  Loop 1: slots (block scans) and the sequential payload
+  // writes; loop 2 (staged slices): the scattered updates without barriers.
+  unsigned long long run = sh_base;  // (gt | eq << 32) before this slice
   bool bad = false;
+  auto scatter = [&](uint32_t id, T v, bool sel) {
+    if (sel) {
+      if (a.r && !spec) a.r[id] = T(0);  // cold mode: pass A stored p
+      if (a.theta) {
+        const T mean = mul_rn(v, T(1));  // P = 1: mean = v * (1/1)
+        const T t2 = add_rn(mul_rn(a.coef, mean), a.theta[id]);
+        a.theta[id] = t2;
+        if (a.mean_out) a.mean_out[id] = mean;
+        bad |= !is_finite(t2);
+      }
+    } else if (spec && a.r) {
+      a.r[id] = v;  // unselected candidate: undo the speculative +0
+    }
+  };
   for (uint32_t base = 0; base < cnt; base += 4 * kCandThreads) {
     const uint32_t j0 = base + 4 * threadIdx.x;
     T v[4];
@@ -349,40 +343,29 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
     const unsigned long long mine = (unsigned long long)__popc(gtm) | ((unsigned long long)__popc(eqm) << 32);
     unsigned long long tot;
     unsigned long long before = run + block_exscan_u64(mine, sh_warp, &tot);
-    uint32_t selm = 0;
-    unsigned long long slot[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const unsigned long long gt_b = before & 0xffffffffull, eq_b = before >> 32;
       const bool gt = (gtm >> c) & 1u, eq = (eqm >> c) & 1u;
-      slot[c] = gt_b + (eq_b < need_eq ? eq_b : need_eq);
-      if (gt || (eq && eq_b < need_eq)) selm |= 1u << c;
+      const bool sel = gt || (eq && eq_b < need_eq);
+      if (sel) {
+        const unsigned long long slot = gt_b + (eq_b < need_eq ? eq_b : need_eq);
+        a.idx_out[slot] = id[c];
+        a.val_out[slot] = v[c];
+      }
+      if (j0 + c < cnt) {
+        if (staged) st_slot[j0 + c] = sel ? 1u : kNoSlot;
+        else scatter(id[c], v[c], sel);
+      }
       before += (unsigned long long)gt | ((unsigned long long)eq << 32);
     }
-    // issue the scattered theta loads together (memory-level parallelism)
-    T th[4];
-    if (a.theta) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) th[c] = ((selm >> c) & 1u) ? a.theta[id[c]] : T(0);
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if ((selm >> c) & 1u) {
-        a.idx_out[slot[c]] = id[c];
-        a.val_out[slot[c]] = v[c];
-        if (a.r && !spec) a.r[id[c]] = T(0);  // cold mode: pass A stored p
-        if (a.theta) {
-          const T mean = mul_rn(v[c], T(1));  // P = 1: mean = v * (1/1)
-          const T t2 = add_rn(mul_rn(a.coef, mean), th[c]);
-          a.theta[id[c]] = t2;
-          if (a.mean_out) a.mean_out[id[c]] = mean;
-          bad |= !is_finite(t2);
-        }
-      } else if (spec && a.r && j0 + c < cnt) {
-        a.r[id[c]] = v[c];  // unselected candidate: undo the speculative +0
-      }
-    }
     run += tot;
+  }
+  if (staged) {
+    __syncthreads();
+#pragma unroll 4
+    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x)
+      scatter(st_idx[j], st_val[j], st_slot[j] != kNoSlot);
   }
   if (bad) sh_bad = 1;
   __syncthreads();

@@ -104,7 +104,7 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   ALLOC(c->d_tk, sizeof(TopkScratch));
   ALLOC(c->d_tw, sizeof(TopkWorker) * max_workers);
   ALLOC(c->d_hist1, sizeof(uint32_t) * PSB_HIST_BINS);
-  ALLOC(c->d_histr, sizeof(uint32_t) * PSB_HIST_BINS);
+  ALLOC(c->d_histr, sizeof(uint32_t) * PSB_HIST_BINS * 10);  // k_cand level histograms
   ALLOC(c->d_histd, sizeof(uint32_t) * 16384);
   ALLOC(c->d_seg_cnt, sizeof(uint32_t) * PSB_FINAL_TPC_MAX);
   ALLOC(c->d_seg_pre, sizeof(uint32_t) * (PSB_FINAL_TPC_MAX + 1));

@@ -515,7 +515,7 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   CandArgs<T> b;
   b.s = s;
   b.w = w;
-  b.histr = c->d_histr;
+  b.hlev = c->d_histr;
   b.cand_idx = c->d_stage_idx;
   b.cand_val = reinterpret_cast<const T*>(c->d_stage_val);
   b.seg_pre = c->d_seg_pre;
@@ -541,7 +541,7 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
     c->cand_smem[slot] = dyn;
   }
   const int dyn = c->cand_smem[slot];
-  b.stage_cap = (uint32_t)(((size_t)dyn - kCoarseBins * 4) / (sizeof(T) + 4)) & ~3u;
+  b.stage_cap = (uint32_t)(((size_t)dyn - kCoarseBins * 4) / (sizeof(T) + 8)) & ~3u;
   const uint32_t cgrid = (uint32_t)std::max<size_t>(1, std::min<size_t>((n + 4095) / 4096, (size_t)c->num_sms));
   void* kargs[] = {&b};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_cand<T>, dim3(cgrid), dim3(kCandThreads),
