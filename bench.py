@@ -329,8 +329,7 @@ def ours(args, cfg, world, rank, local_rank):
         e2e_ms = float(te[0])
 
     if rank != 0:
-        ctx.close()
-        return
+        return ctx
     peak, peak_src = load_peaks()
     dense_bytes = 4.0 * n * P
     value = dense_bytes / (ms_step * 1e-3) / 1e9
@@ -384,7 +383,17 @@ def ours(args, cfg, world, rank, local_rank):
             "sample": f"{done} steps of reference sync_data_parallel_step at N={n_s} (P={P}, k={k_s}), "
                       f"median {t_s:.3f} s/step, 1 thread (the reference is single-threaded)"}
     print(json.dumps(line), flush=True)
-    ctx.close()
+    return ctx
+
+
+def _teardown_watchdog(seconds: float) -> None:
+    """The JSON line is out; never let a stuck communicator teardown hang the run."""
+    def _kill():
+        time.sleep(seconds)
+        sys.stderr.write("bench.py: teardown exceeded %.0fs, exiting\n" % seconds)
+        sys.stderr.flush()
+        os._exit(0)
+    threading.Thread(target=_kill, daemon=True).start()
 
 
 def main():
@@ -415,12 +424,16 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    try:
-        ours(args, cfg, world, rank, local_rank)
-    finally:
-        if world > 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
+    ctx = ours(args, cfg, world, rank, local_rank)
+    _teardown_watchdog(60.0)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()          # every rank done with the communicators
+        ctx.close()             # ncclCommDestroy on all ranks together
+        dist.barrier()
+        dist.destroy_process_group()
+    else:
+        ctx.close()
 
 
 if __name__ == "__main__":

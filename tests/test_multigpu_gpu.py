@@ -1,0 +1,105 @@
+"""GPU, >= 2 devices: the NCCL exchange paths (one process per GPU).
+
+Every rank owns W local workers (worker id = rank*W + w); after each step the
+replicas must be bitwise identical to each other and to the oracle composite
+of sync_data_parallel_step / the async loop over all P = W*R workers.
+"""
+import multiprocessing as mp
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def _worker(rank, nranks, uid, W, comp, order, steps, q):
+    sys.path.insert(0, ROOT)
+    try:
+        import torch as th
+
+        from oracle import oracle as O
+        from paper_2506_17551_b200 import _lib as L
+        from paper_2506_17551_b200.engine import Context, topology
+
+        th.cuda.set_device(rank)
+        n, k, lr = 50_000, 500, 0.05
+        P = W * nranks
+        c = Context(n, k, P, device=rank)
+        c.comm_init(rank, nranks, uid)
+        code = {"topk": L.PSB_COMP_TOPK, "topk_q8": L.PSB_COMP_TOPK_Q8, "onebit": L.PSB_COMP_ONEBIT,
+                "none": L.PSB_COMP_NONE, "q8": L.PSB_COMP_Q8, "async": L.PSB_COMP_TOPK,
+                "async_q8": L.PSB_COMP_TOPK_Q8}[comp]
+        dpn, npr = (2, 1) if order == "hierarchical" else (0, 1)
+        topo = topology(1, npr, dpn) if dpn else None
+        theta = th.zeros(n, device="cuda")
+        res = th.zeros(W, n, device="cuda")
+        theta_h = np.zeros(n, dtype=np.float32)
+        res_h = np.zeros((P, n), dtype=np.float32)
+        gu = gu_h = 0
+        worst = 0.0
+        for step in range(steps):
+            g_all = np.stack([O.generate("llmrec", 7, p, step, n) for p in range(P)])
+            g = th.from_numpy(g_all[rank * W:(rank + 1) * W].copy()).cuda()
+            d = c.step_desc(code, g, res, theta, lr, k, order, 256, topo)
+            if comp.startswith("async"):
+                gu = c.async_round(d, 2, gu)
+                gu_h = O.async_round(g_all, theta_h, lr, k, res_h, 2, gu_h, q8=comp == "async_q8")
+            else:
+                c.sync_step(d)
+                O.sync_step(g_all, theta_h, lr, comp, k, order, res_h, dpn, npr, 256)
+            c.check()
+            got = theta.cpu().numpy()
+            if comp == "onebit":
+                worst = max(worst, float(np.max(np.abs(got - theta_h))))
+                theta.copy_(th.from_numpy(theta_h))
+                res.copy_(th.from_numpy(res_h[rank * W:(rank + 1) * W]))
+            else:
+                if not np.array_equal(got.view(np.uint32), theta_h.view(np.uint32)):
+                    q.put((rank, f"theta mismatch at step {step}"))
+                    return
+                if not np.array_equal(res.cpu().numpy().view(np.uint32),
+                                      res_h[rank * W:(rank + 1) * W].view(np.uint32)):
+                    q.put((rank, f"residual mismatch at step {step}"))
+                    return
+        q.put((rank, "ok" if worst < 1e-6 else f"onebit deviation {worst}"))
+        c.close()
+    except Exception as e:  # report, never hang the parent
+        q.put((rank, f"error: {type(e).__name__}: {e}"))
+
+
+def _run(nranks, W, comp, order, steps=4):
+    from paper_2506_17551_b200.engine import Context
+    uid = Context.unique_id()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, nranks, uid, W, comp, order, steps, q))
+             for r in range(nranks)]
+    for p in procs:
+        p.start()
+    results = {}
+    for _ in range(nranks):
+        r, msg = q.get(timeout=300)
+        results[r] = msg
+    for p in procs:
+        p.join(timeout=60)
+    return results
+
+
+needs2 = pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+
+
+@needs2
+@pytest.mark.parametrize("comp,order,W", [
+    ("topk", "ring", 1), ("topk", "naive", 2), ("topk", "hierarchical", 2),
+    ("topk_q8", "naive", 1), ("onebit", "ring", 1), ("none", "naive", 2),
+    ("q8", "naive", 1), ("q8", "ring", 2), ("async", "naive", 2), ("async_q8", "naive", 1),
+])
+def test_nccl_paths_match_oracle(comp, order, W):
+    nr = min(torch.cuda.device_count(), 4)
+    res = _run(nr, W, comp, order)
+    assert all(v == "ok" for v in res.values()), res
