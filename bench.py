@@ -199,9 +199,8 @@ def ours(args, cfg, world, rank, local_rank):
     stream = torch.cuda.Stream(dev)
     ctx = Context(n, max(k, 1), P, device=local_rank)
     if world > 1:
-        uid = [Context.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx.comm_init(rank, world, uid[0])
+        from paper_2506_17551_b200.dist import init_comm
+        init_comm(ctx)  # NCCL unique id from rank 0 over the process group
 
     NB = 3  # rotated gradient buffers (each > L2): inputs larger than L2
     with torch.cuda.stream(stream):
