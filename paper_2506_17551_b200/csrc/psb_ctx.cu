@@ -83,6 +83,7 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   c->max_k = max_k < 1 ? 1 : max_k;
   c->max_workers = max_workers;
   if (const char* np = getenv("PSB_NO_PREDICT")) c->predict = np[0] == '0';
+  if (const char* ns = getenv("PSB_NO_STAGE")) c->no_stage = ns[0] != '0';
   auto fail = [&](cudaError_t e) {
     psb_ctx_destroy(c);
     return e == cudaErrorMemoryAllocation ? PSB_ENOMEM : PSB_ECUDA;

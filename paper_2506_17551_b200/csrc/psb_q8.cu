@@ -6,7 +6,9 @@
 //   per block of B consecutive elements: scale = absmax / 127  (IEEE f32 div)
 //   code = clamp(rint(p / scale), -127, 127)  (IEEE div, round-half-even), 0 if scale == 0
 //   xhat = code * scale;  error feedback r' = p - xhat (compression.hpp:153-154 shape)
-// One warp per block, float4 loads, char4 code stores (128-bit per 4 lanes).
+// One warp per block; each lane owns 4 consecutive elements per 128-element
+// row (float4 / char4 accesses); the next block's loads are issued before the
+// current block is processed (register double buffer) to keep HBM busy.
 //
 // Dense 8-bit "hierarchical" all-reduce (cfg3), P = W local workers x R ranks:
 //   1. quantize each local worker's p = r + g          (k_q8_quant)
@@ -21,10 +23,47 @@
 
 namespace {
 
-__device__ __forceinline__ int q8_code(float p, float scale) {
+// code = clamp(rint(RN(p / scale)), -127, 127), bit-identical to the IEEE
+// division of the spec, but computed from y = p * inv (inv = RN(1/scale), one
+// division per block): |y - RN(p/scale)| <= 3 ulp, so rint(y) == rint(RN(p/scale))
+// unless y lies within 3 ulp (< 6.1e-5 for |y| < 128) of a half-integer; those
+// rare lanes, and a non-finite inv, take the exact division.
+__device__ __forceinline__ int q8_code(float p, float scale, float inv) {
   if (!(scale > 0.f)) return 0;
-  int q = __float2int_rn(__fdiv_rn(p, scale));
+  const float y = __fmul_rn(p, inv);
+  const float fr = fabsf(y - rintf(y));
+  int q;
+  if (is_finite(inv) && fabsf(fr - 0.5f) > 6.1e-5f) q = __float2int_rn(y);
+  else q = __float2int_rn(__fdiv_rn(p, scale));
   return q > 127 ? 127 : (q < -127 ? -127 : q);
+}
+
+// Loads one block's p = r + x for this lane: VPL rows of 4 elements.
+template <int VPL>
+__device__ __forceinline__ void q8_load(const float* __restrict__ x, const float* __restrict__ r, size_t n,
+                                        size_t lo, bool full, int lane, float (&p)[VPL][4]) {
+#pragma unroll
+  for (int it = 0; it < VPL; ++it) {
+    const size_t e = lo + (size_t)it * 128 + lane * 4;
+    if (full) {
+      const float4 xv = __ldcs(reinterpret_cast<const float4*>(x + e));
+      if (r) {
+        const float4 rv = __ldcs(reinterpret_cast<const float4*>(r + e));
+        p[it][0] = __fadd_rn(rv.x, xv.x);
+        p[it][1] = __fadd_rn(rv.y, xv.y);
+        p[it][2] = __fadd_rn(rv.z, xv.z);
+        p[it][3] = __fadd_rn(rv.w, xv.w);
+      } else {
+        p[it][0] = xv.x; p[it][1] = xv.y; p[it][2] = xv.z; p[it][3] = xv.w;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const size_t ei = e + c;
+        p[it][c] = ei < n ? (r ? __fadd_rn(r[ei], x[ei]) : x[ei]) : 0.f;
+      }
+    }
+  }
 }
 
 template <int VPL>
@@ -38,32 +77,16 @@ __global__ void __launch_bounds__(256) k_q8_quant(const float* __restrict__ x, f
   const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
   const bool vec_ok = ((((uintptr_t)x) | ((uintptr_t)r) | ((uintptr_t)codes)) & 15) == 0;
   bool bad = false;
-  for (size_t blk = warp; blk < nb; blk += nwarps) {
+  float p[VPL][4];
+  size_t blk = warp;
+  if (blk < nb) q8_load<VPL>(x, r, n, blk * B, vec_ok && blk * B + B <= n, lane, p);
+  for (; blk < nb; blk += nwarps) {
     const size_t lo = blk * B;
     const bool full = vec_ok && lo + B <= n;
-    float p[VPL][4];
-#pragma unroll
-    for (int it = 0; it < VPL; ++it) {
-      const size_t e = lo + (size_t)it * 128 + lane * 4;
-      if (full) {
-        const float4 xv = __ldcs(reinterpret_cast<const float4*>(x + e));
-        if (r) {
-          const float4 rv = *reinterpret_cast<const float4*>(r + e);
-          p[it][0] = __fadd_rn(rv.x, xv.x);
-          p[it][1] = __fadd_rn(rv.y, xv.y);
-          p[it][2] = __fadd_rn(rv.z, xv.z);
-          p[it][3] = __fadd_rn(rv.w, xv.w);
-        } else {
-          p[it][0] = xv.x; p[it][1] = xv.y; p[it][2] = xv.z; p[it][3] = xv.w;
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const size_t ei = e + c;
-          p[it][c] = ei < n ? (r ? __fadd_rn(r[ei], x[ei]) : x[ei]) : 0.f;
-        }
-      }
-    }
+    // prefetch the next block of this warp before working on this one
+    float pn[VPL][4];
+    const size_t nxt = blk + nwarps;
+    if (nxt < nb) q8_load<VPL>(x, r, n, nxt * B, vec_ok && nxt * B + B <= n, lane, pn);
     float amax = 0.f;
 #pragma unroll
     for (int it = 0; it < VPL; ++it)
@@ -75,6 +98,7 @@ __global__ void __launch_bounds__(256) k_q8_quant(const float* __restrict__ x, f
 #pragma unroll
     for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     const float scale = __fdiv_rn(amax, 127.0f);
+    const float inv = __frcp_rn(scale);
     if (lane == 0) scales[blk] = scale;
 #pragma unroll
     for (int it = 0; it < VPL; ++it) {
@@ -83,13 +107,13 @@ __global__ void __launch_bounds__(256) k_q8_quant(const float* __restrict__ x, f
       float res[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        q[c] = q8_code(p[it][c], scale);
+        q[c] = q8_code(p[it][c], scale, inv);
         res[c] = __fsub_rn(p[it][c], __fmul_rn((float)q[c], scale));
       }
       if (full) {
-        char4 cv = make_char4((signed char)q[0], (signed char)q[1], (signed char)q[2], (signed char)q[3]);
-        *reinterpret_cast<char4*>(codes + e) = cv;
-        if (r) *reinterpret_cast<float4*>(r + e) = make_float4(res[0], res[1], res[2], res[3]);
+        *reinterpret_cast<char4*>(codes + e) =
+            make_char4((signed char)q[0], (signed char)q[1], (signed char)q[2], (signed char)q[3]);
+        if (r) __stcs(reinterpret_cast<float4*>(r + e), make_float4(res[0], res[1], res[2], res[3]));
       } else {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -100,6 +124,10 @@ __global__ void __launch_bounds__(256) k_q8_quant(const float* __restrict__ x, f
         }
       }
     }
+#pragma unroll
+    for (int it = 0; it < VPL; ++it)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) p[it][c] = pn[it][c];
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1u);
 }
@@ -109,6 +137,55 @@ __global__ void k_q8_dequant(const int8_t* __restrict__ codes, const float* __re
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
     out[i] = __fmul_rn((float)codes[i], scales[i / B]);
+}
+
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+
+// The reference fold orders (psb_fold.cuh) on 4 consecutive elements at once;
+// ring_start is the rotated first worker of their (common) ring chunk.
+template <class Get4>
+__device__ __forceinline__ float4 fold_sum4(const Get4& get4, int P, int order, int ring_start,
+                                            uint32_t dpn, uint32_t npr) {
+  float4 acc;
+  if (order == PSB_ORDER_RING) {
+    acc = get4(ring_start);
+    for (int s = 1; s < P; ++s) {
+      int q = ring_start + s;
+      if (q >= P) q -= P;
+      acc = add4(acc, get4(q));
+    }
+  } else if (order == PSB_ORDER_HIER && dpn < (uint32_t)P) {
+    const uint32_t nodes = ((uint32_t)P + dpn - 1) / dpn;
+    float4 total = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool have_total = false;
+    for (uint32_t nb = 0; nb < nodes; nb += npr) {
+      float4 rack = make_float4(0.f, 0.f, 0.f, 0.f);
+      bool have_rack = false;
+      for (uint32_t nd = nb; nd < nodes && nd < nb + npr; ++nd) {
+        const uint32_t base = nd * dpn;
+        float4 node = get4((int)base);
+        for (uint32_t p = base + 1; p < base + dpn && p < (uint32_t)P; ++p) node = add4(node, get4((int)p));
+        rack = have_rack ? add4(rack, node) : node;
+        have_rack = true;
+      }
+      total = have_total ? add4(total, rack) : rack;
+      have_total = true;
+    }
+    acc = total;
+  } else {
+    acc = get4(0);
+    for (int q = 1; q < P; ++q) acc = add4(acc, get4(q));
+  }
+  return acc;
+}
+
+__device__ __forceinline__ uint32_t ring_chunk(size_t i, size_t n, int P) {
+  uint32_t j = (uint32_t)((i * (size_t)P) / n);
+  while (j + 1 < (uint32_t)P && ((size_t)(j + 1) * n) / (size_t)P <= i) ++j;
+  while (j > 0 && ((size_t)j * n) / (size_t)P > i) --j;
+  return j;
 }
 
 // Fold P workers' dequantized values over blocks [blk_lo, blk_hi) (global block
@@ -128,46 +205,98 @@ __global__ void __launch_bounds__(256) k_q8_reduce(
   const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
   const size_t e_base = blk_lo * B;
   const float inv = (float)(1.0 / (double)P);
+  const bool vec_ok = ((((uintptr_t)wcodes) | ((uintptr_t)mcodes) | ((uintptr_t)theta) | wstride) & 15) == 0 &&
+                      !mean_out;
   bool bad = false;
   for (size_t blk = blk_lo + warp; blk < blk_hi; blk += nwarps) {
     float m[VPL][4];
     float amax = 0.f;
+    // issue the theta loads first: independent of the fold, overlaps its latency
+    float4 thv[VPL];
+    if (theta && vec_ok) {
+#pragma unroll
+      for (int it = 0; it < VPL; ++it) {
+        const size_t e0 = blk * B + (size_t)it * 128 + lane * 4;
+        if (e0 + 4 <= n) thv[it] = __ldcs(reinterpret_cast<const float4*>(theta + e0));
+      }
+    }
 #pragma unroll
     for (int it = 0; it < VPL; ++it) {
+      const size_t e0 = blk * B + (size_t)it * 128 + lane * 4;
+      const bool full = vec_ok && e0 + 4 <= n;
+      const int rs0 = order == PSB_ORDER_RING ? (int)((ring_chunk(e0, n, P) + 1) % (uint32_t)P) : 0;
+      const bool same_chunk =
+          order != PSB_ORDER_RING || (e0 + 3 < n && ring_chunk(e0 + 3, n, P) == ring_chunk(e0, n, P));
+      if (full && same_chunk) {
+        auto get4 = [&](int q) -> float4 {
+          const char4 cv = *reinterpret_cast<const char4*>(wcodes + (size_t)q * wstride + (e0 - e_base));
+          const float sc = wscales[(size_t)q * sstride + (blk - blk_lo)];
+          return make_float4(__fmul_rn((float)cv.x, sc), __fmul_rn((float)cv.y, sc),
+                             __fmul_rn((float)cv.z, sc), __fmul_rn((float)cv.w, sc));
+        };
+        const float4 s = fold_sum4(get4, P, order, rs0, dpn, npr);
+        m[it][0] = __fmul_rn(s.x, inv);
+        m[it][1] = __fmul_rn(s.y, inv);
+        m[it][2] = __fmul_rn(s.z, inv);
+        m[it][3] = __fmul_rn(s.w, inv);
+      } else {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const size_t e = blk * B + (size_t)it * 128 + lane * 4 + c;
-        float mean = 0.f;
-        if (e < n) {
-          auto get = [&](int q) -> float {
-            const int8_t code = wcodes[(size_t)q * wstride + (e - e_base)];
-            const float sc = wscales[(size_t)q * sstride + (blk - blk_lo)];
-            return __fmul_rn((float)code, sc);
-          };
-          mean = __fmul_rn(fold_sum<float>(get, P, order, e, n, dpn, npr), inv);
+        for (int c = 0; c < 4; ++c) {
+          const size_t e = e0 + c;
+          float mean = 0.f;
+          if (e < n) {
+            auto get = [&](int q) -> float {
+              const int8_t code = wcodes[(size_t)q * wstride + (e - e_base)];
+              const float sc = wscales[(size_t)q * sstride + (blk - blk_lo)];
+              return __fmul_rn((float)code, sc);
+            };
+            mean = __fmul_rn(fold_sum<float>(get, P, order, e, n, dpn, npr), inv);
+          }
+          m[it][c] = mean;
         }
-        m[it][c] = mean;
-        amax = fmaxf(amax, fabsf(mean));
       }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) amax = fmaxf(amax, fabsf(m[it][c]));
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     const float scale = __fdiv_rn(amax, 127.0f);
+    const float inv = __frcp_rn(scale);
     if (lane == 0) mscales[blk] = scale;
 #pragma unroll
     for (int it = 0; it < VPL; ++it) {
+      const size_t e0 = blk * B + (size_t)it * 128 + lane * 4;
+      int q[4];
+      float mh[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const size_t e = blk * B + (size_t)it * 128 + lane * 4 + c;
-        if (e >= n) continue;
-        const int q = q8_code(m[it][c], scale);
-        mcodes[e] = (int8_t)q;
+        q[c] = q8_code(m[it][c], scale, inv);
+        mh[c] = __fmul_rn((float)q[c], scale);
+      }
+      if (vec_ok && e0 + 4 <= n) {
+        *reinterpret_cast<char4*>(mcodes + e0) =
+            make_char4((signed char)q[0], (signed char)q[1], (signed char)q[2], (signed char)q[3]);
         if (theta) {
-          const float mhat = __fmul_rn((float)q, scale);
-          const float th = __fadd_rn(__fmul_rn(coef, mhat), theta[e]);
-          theta[e] = th;
-          if (mean_out) mean_out[e] = mhat;
-          bad |= !is_finite(th);
+          float4 th = thv[it];
+          th.x = __fadd_rn(__fmul_rn(coef, mh[0]), th.x);
+          th.y = __fadd_rn(__fmul_rn(coef, mh[1]), th.y);
+          th.z = __fadd_rn(__fmul_rn(coef, mh[2]), th.z);
+          th.w = __fadd_rn(__fmul_rn(coef, mh[3]), th.w);
+          __stcs(reinterpret_cast<float4*>(theta + e0), th);
+          bad |= !is_finite(th.x) || !is_finite(th.y) || !is_finite(th.z) || !is_finite(th.w);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const size_t e = e0 + c;
+          if (e >= n) continue;
+          mcodes[e] = (int8_t)q[c];
+          if (theta) {
+            const float th = __fadd_rn(__fmul_rn(coef, mh[c]), theta[e]);
+            theta[e] = th;
+            if (mean_out) mean_out[e] = mh[c];
+            bad |= !is_finite(th);
+          }
         }
       }
     }
@@ -188,12 +317,12 @@ __global__ void __launch_bounds__(256) k_q8_apply(const int8_t* __restrict__ mco
       const size_t e = v * 4;
       const char4 cv = *reinterpret_cast<const char4*>(mcodes + e);
       const float sc = mscales[e / B];
-      float4 th = *reinterpret_cast<float4*>(theta + e);
+      float4 th = __ldcs(reinterpret_cast<const float4*>(theta + e));
       th.x = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.x, sc)), th.x);
       th.y = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.y, sc)), th.y);
       th.z = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.z, sc)), th.z);
       th.w = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.w, sc)), th.w);
-      *reinterpret_cast<float4*>(theta + e) = th;
+      __stcs(reinterpret_cast<float4*>(theta + e), th);
       bad |= !is_finite(th.x) || !is_finite(th.y) || !is_finite(th.z) || !is_finite(th.w);
     }
     for (size_t e = nv * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;

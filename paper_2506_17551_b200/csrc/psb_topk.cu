@@ -542,6 +542,7 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   }
   const int dyn = c->cand_smem[slot];
   b.stage_cap = (uint32_t)(((size_t)dyn - kCoarseBins * 4) / (sizeof(T) + 8)) & ~3u;
+  if (c->no_stage) b.stage_cap = 0;  // diagnostics: PSB_NO_STAGE=1 streams the list from L2/HBM
   const uint32_t cgrid = (uint32_t)std::max<size_t>(1, std::min<size_t>((n + 4095) / 4096, (size_t)c->num_sms));
   void* kargs[] = {&b};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_cand<T>, dim3(cgrid), dim3(kCandThreads),

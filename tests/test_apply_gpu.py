@@ -167,6 +167,30 @@ def test_q8_quantize_bitwise(ctx, block):
         assert np.array_equal(bits(tnp(deq)), bits(O.q8_dequant(oc, osc, block)))
 
 
+def test_q8_rounding_ties_and_near_ties(ctx):
+    """Exact .5 ties (round-half-even) and values 1-3 ulp around them, where the
+    reciprocal fast path must defer to the exact IEEE division."""
+    base = np.array([127.0, 2.5, 3.5, -4.5, 0.5, -0.5, 126.5, 1.5], dtype=np.float32)
+    vals = [base]
+    for d in (1, 2, 3, 5):
+        up = np.nextafter(base, np.float32(np.inf))
+        dn = np.nextafter(base, np.float32(-np.inf))
+        for _ in range(d - 1):
+            up = np.nextafter(up, np.float32(np.inf))
+            dn = np.nextafter(dn, np.float32(-np.inf))
+        vals += [up.astype(np.float32), dn.astype(np.float32)]
+    x = np.concatenate(vals).astype(np.float32)
+    x = np.concatenate([x, np.zeros((-x.size) % 128, dtype=np.float32)])
+    # scale a copy so absmax/127 is not exactly 1 as well
+    for mult in (np.float32(1.0), np.float32(0.37), np.float32(3.1e-3)):
+        xs = (x * mult).astype(np.float32)
+        codes, scales = ctx.q8_quantize(torch.from_numpy(xs).cuda(), None, 128)
+        oc, osc, _ = O.q8_quant(xs, None, 128)
+        ctx.check()
+        assert np.array_equal(tnp(codes), oc)
+        assert np.array_equal(bits(tnp(scales)), bits(osc))
+
+
 COMPS = {"topk": L.PSB_COMP_TOPK, "onebit": L.PSB_COMP_ONEBIT, "none": L.PSB_COMP_NONE,
          "q8": L.PSB_COMP_Q8, "topk_q8": L.PSB_COMP_TOPK_Q8}
 
