@@ -47,106 +47,258 @@ __device__ __forceinline__ T pl_val(const PayloadView& v, int q, size_t j) {
   return reinterpret_cast<const T*>(b + v.val_off)[j];
 }
 
-__global__ void k_seg_offsets(PayloadView v, int P, size_t k, uint32_t nseg, int seg_shift,
-                              uint32_t* __restrict__ seg_off) {
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
-  const size_t work1 = (size_t)P * k;
-  const size_t work2 = (size_t)P * (nseg + 1);
-  const size_t work = work1 > work2 ? work1 : work2;
-  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < work; t += stride) {
-    if (t < work1) {
-      const int q = (int)(t / k);
-      const size_t j = t - (size_t)q * k;
-      const uint32_t* idx = pl_idx(v, q);
-      const long long sj = (long long)(idx[j] >> seg_shift);
-      const long long sp = j ? (long long)(idx[j - 1] >> seg_shift) : -1ll;
-      uint32_t* row = seg_off + (size_t)q * (nseg + 1);
-      for (long long s = sp + 1; s <= sj && s <= (long long)nseg; ++s) row[s] = (uint32_t)j;
-    }
-    if (t < work2) {
-      const int q = (int)(t / (nseg + 1));
-      const uint32_t s = (uint32_t)(t - (size_t)q * (nseg + 1));
-      const uint32_t last = pl_idx(v, q)[k - 1] >> seg_shift;
-      if (s > last) seg_off[(size_t)q * (nseg + 1) + s] = (uint32_t)k;
-    }
+// Per-worker segment offsets: seg_off[q][s] = first payload position of worker
+// q whose index is >= s*S (k past the end).  Grid (x, P); 32-bit positions.
+#ifdef PSB_APPLY_TRACE
+__device__ unsigned long long g_apply_trace[8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define APPLY_MARK(slot)                                             \
+  do {                                                               \
+    __syncthreads();                                                 \
+    if (threadIdx.x == 0) {                                          \
+      const unsigned long long t_ = gtimer();                        \
+      atomicAdd(&g_apply_trace[slot], t_ - t_prev);                  \
+      t_prev = t_;                                                   \
+    }                                                                \
+  } while (0)
+#else
+#define APPLY_MARK(slot) \
+  do {                   \
+  } while (0)
+#endif
+
+constexpr int kSegU = 8;  // entries per thread in k_seg_offsets
+
+__global__ void __launch_bounds__(256) k_seg_offsets(PayloadView v, int P, uint32_t k, uint32_t nseg,
+                                                     int seg_shift, uint32_t* __restrict__ seg_off) {
+  const int q = blockIdx.y;
+  const uint32_t* idx = pl_idx(v, q);
+  uint32_t* row = seg_off + (size_t)q * (nseg + 1);
+  const uint32_t base = blockIdx.x * (blockDim.x * kSegU) + threadIdx.x;
+  uint32_t cur[kSegU], prv[kSegU];
+#pragma unroll
+  for (int u = 0; u < kSegU; ++u) {
+    const uint32_t j = base + u * blockDim.x;
+    cur[u] = j < k ? idx[j] : 0u;
+    prv[u] = (j && j < k) ? idx[j - 1] : 0u;
   }
+#pragma unroll
+  for (int u = 0; u < kSegU; ++u) {
+    const uint32_t j = base + u * blockDim.x;
+    if (j >= k) continue;
+    const uint32_t s0 = j ? (prv[u] >> seg_shift) + 1 : 0;
+    for (uint32_t s = s0; s <= (cur[u] >> seg_shift); ++s) row[s] = j;
+  }
+  const uint32_t last = idx[k - 1] >> seg_shift;
+  for (uint32_t s = last + 1 + blockIdx.x * blockDim.x + threadIdx.x; s <= nseg; s += gridDim.x * blockDim.x)
+    row[s] = k;
 }
 
-template <class T, bool ASYNC>
-__global__ void __launch_bounds__(256) k_sparse_apply(PayloadView v, int P, uint32_t nseg,
-                                                      int seg_shift,
-                                                      const uint32_t* __restrict__ seg_off,
-                                                      int order, uint32_t dpn, uint32_t npr,
-                                                      T coef, WorkerCoefs wscale,
-                                                      T* __restrict__ theta, size_t n,
-                                                      T* __restrict__ mean_out, uint32_t* flags) {
+// Bitmap-rank apply (P >= 2).  One CTA per segment of S = 2^seg_shift
+// indices.  The segment's entries of all P workers form one flat range
+// e in [0, tot) (worker q owns [vb[q], vb[q+1])); they are loaded once,
+// batched so the global loads of a thread overlap, and staged in shared
+// memory as (local index, value) when tot <= vcap.  Each worker's touched
+// indices become a presence bitmap; the first entry of a worker in each
+// bitmap word records its rank there, so the position of index i in worker
+// q2's list is pre[q2][w] + popc(word & below) (only words holding a set bit
+// are ever queried, so no scan is needed).  The lowest worker touching i owns
+// it: it folds the P dense values (+0 where absent) in the configured
+// reference order and updates theta once (async: applies the present workers
+// in order).  Dependent global round trips per segment: segment offsets,
+// entry loads, theta -- the rest is shared memory.  PT > 0 fixes P at
+// compile time (worker lookup in registers); PT == 0 is the generic kernel.
+#ifndef PSB_APPLY_MINB
+#define PSB_APPLY_MINB 4
+#endif
+template <class T, bool ASYNC, int PT>
+__global__ void __launch_bounds__(256, PSB_APPLY_MINB) k_sparse_apply_bm(PayloadView v, int P_rt, uint32_t nseg,
+                                                         int seg_shift, uint32_t vcap,
+                                                         const uint32_t* __restrict__ seg_off,
+                                                         int order, uint32_t dpn, uint32_t npr,
+                                                         T coef, WorkerCoefs wscale,
+                                                         T* __restrict__ theta, size_t n,
+                                                         T* __restrict__ mean_out, uint32_t* flags) {
+  constexpr int U = 4;  // entries per thread per batch
+  const int P = PT > 0 ? PT : P_rt;
   extern __shared__ __align__(16) unsigned char smem[];
-  const uint32_t S = 1u << seg_shift;
-  uint32_t* mask = reinterpret_cast<uint32_t*>(smem);
-  T* vals = reinterpret_cast<T*>(smem + (size_t)S * 4);
-  __shared__ uint32_t lo[PSB_MAX_P], hi[PSB_MAX_P];
-  __shared__ uint32_t sh_any, sh_bad;
+  const uint32_t NW = (1u << seg_shift) >> 5;  // bitmap words per worker
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem);  // [P][NW] presence bits
+  uint32_t* pre = bm + (size_t)P * NW;                 // [P][NW] rank of a word's first entry
+  T* sval = reinterpret_cast<T*>(pre + (size_t)P * NW);  // [vcap] staged values
+  __shared__ uint32_t lo[PSB_MAX_P], vb[PSB_MAX_P + 1];
   __shared__ T coefs[PSB_MAX_P];
-  if (threadIdx.x == 0) sh_bad = 0;
   if (ASYNC && threadIdx.x < (unsigned)P) coefs[threadIdx.x] = (T)(-wscale.v[threadIdx.x]);
   const T inv = (T)(1.0 / (double)P);
   bool bad = false;
+  RingChunk rc;
+  const uint32_t lane = threadIdx.x & 31;
 
+#ifdef PSB_APPLY_TRACE
+  unsigned long long t_prev = gtimer();
+#endif
   for (uint32_t seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
-    __syncthreads();
-    if (threadIdx.x == 0) sh_any = 0;
-    __syncthreads();
-    if (threadIdx.x < (unsigned)P) {
-      const uint32_t* row = seg_off + (size_t)threadIdx.x * (nseg + 1);
-      lo[threadIdx.x] = row[seg];
-      hi[threadIdx.x] = row[seg + 1];
-      if (hi[threadIdx.x] > lo[threadIdx.x]) atomicOr(&sh_any, 1u);
+    __syncthreads();  // the previous segment is done with shared memory
+    if (threadIdx.x < 32) {
+      uint32_t l = 0, cnt = 0;
+      if (lane < (uint32_t)P) {
+        const uint32_t* row = seg_off + (size_t)lane * (nseg + 1);
+        l = row[seg];
+        cnt = row[seg + 1] - l;
+      }
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += t;
+      }
+      if (lane < (uint32_t)P) {
+        lo[lane] = l;
+        vb[lane + 1] = incl;
+      }
+      if (lane == 0) vb[0] = 0;
+    }
+    {
+      uint4* b4 = reinterpret_cast<uint4*>(bm);
+      for (uint32_t w = threadIdx.x; w < ((uint32_t)P * NW) >> 2; w += blockDim.x) b4[w] = make_uint4(0, 0, 0, 0);
     }
     __syncthreads();
-    if (!sh_any) continue;
-    for (uint32_t i = threadIdx.x; i < S; i += blockDim.x) mask[i] = 0;
-    __syncthreads();
+    APPLY_MARK(0);
+    const uint32_t tot = vb[P];
+    if (!tot) continue;  // uniform across the CTA
+    const bool staged = tot <= vcap;
     const size_t seg_base = (size_t)seg << seg_shift;
-    for (int q = 0; q < P; ++q) {
-      const uint32_t* idx = pl_idx(v, q);
-      for (uint32_t j = lo[q] + threadIdx.x; j < hi[q]; j += blockDim.x) {
-        const uint32_t il = (uint32_t)(idx[j] - seg_base);
-        vals[(size_t)q * S + il] = pl_val<T>(v, q, j);
-        atomicOr(&mask[il], 1u << q);
-      }
+    uint32_t vbr[PT > 0 ? PT : 1];
+    if constexpr (PT > 0) {
+#pragma unroll
+      for (int p = 0; p < PT; ++p) vbr[p] = vb[p];
     }
-    __syncthreads();
-    for (int q = 0; q < P; ++q) {
-      const uint32_t* idx = pl_idx(v, q);
-      for (uint32_t j = lo[q] + threadIdx.x; j < hi[q]; j += blockDim.x) {
-        const size_t i = idx[j];
-        const uint32_t il = (uint32_t)(i - seg_base);
-        const uint32_t m = mask[il];
-        if (__ffs(m) - 1 != q) continue;  // the lowest touching worker owns index i
-        T th = theta ? theta[i] : T(0);
-        if (ASYNC) {
-          uint32_t mm = m;
-          while (mm) {
-            const int w = __ffs(mm) - 1;
-            mm &= mm - 1;
-            th = add_rn(mul_rn(coefs[w], vals[(size_t)w * S + il]), th);
+    // worker owning flat entry e, and the flat index of that worker's first entry
+    auto worker_of = [&](uint32_t e, uint32_t& base) {
+      int q = 0;
+      base = 0;
+      if constexpr (PT > 0) {
+#pragma unroll
+        for (int p = 1; p < PT; ++p)
+          if (e >= vbr[p]) {
+            q = p;
+            base = vbr[p];
           }
-        } else {
-          auto get = [&](int w) -> T { return ((m >> w) & 1u) ? vals[(size_t)w * S + il] : T(0); };
-          const T mean = mul_rn(fold_sum<T>(get, P, order, i, n, dpn, npr), inv);
-          th = add_rn(mul_rn(coef, mean), th);
-          if (mean_out) mean_out[i] = mean;
+      } else {
+        for (int p = 1; p < P; ++p) q += e >= vb[p];
+        base = vb[q];
+      }
+      return q;
+    };
+    // 1. presence bitmaps, word ranks, staging; a batch issues all its loads first
+    for (uint32_t e0 = threadIdx.x; e0 < tot; e0 += U * blockDim.x) {
+      uint32_t il[U], ilp[U], r[U];
+      T val[U];
+      int qq[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t e = e0 + u * blockDim.x;
+        qq[u] = -1;
+        if (e < tot) {
+          uint32_t base;
+          const int q = worker_of(e, base);
+          const uint32_t rq = e - base;
+          const uint32_t j = lo[q] + rq;
+          const uint32_t* idx = pl_idx(v, q);
+          qq[u] = q;
+          r[u] = rq;
+          il[u] = (uint32_t)(idx[j] - seg_base);
+          ilp[u] = rq ? (uint32_t)(idx[j - 1] - seg_base) : 0xffffffffu;
+          if (staged) val[u] = pl_val<T>(v, q, j);
         }
-        if (theta) {
-          theta[i] = th;
-          bad |= !is_finite(th);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (qq[u] < 0) continue;
+        const uint32_t w = il[u] >> 5;
+        atomicOr(&bm[(size_t)qq[u] * NW + w], 1u << (il[u] & 31));
+        if (ilp[u] == 0xffffffffu || (ilp[u] >> 5) != w) pre[(size_t)qq[u] * NW + w] = r[u];
+        if (staged) sval[e0 + u * blockDim.x] = val[u];
+        // warm L2 with theta at this index: phase 2 reads it after the barrier
+        if (theta) asm volatile("prefetch.global.L2 [%0];" ::"l"(theta + seg_base + il[u]));
+      }
+    }
+    APPLY_MARK(1);
+    __syncthreads();
+    // 2. fold and update by bitmap word: a thread takes word w of the
+    //    segment, ORs the P workers' words, and folds each touched index;
+    //    theta loads of up to U indices are issued together
+    for (uint32_t w = threadIdx.x; w < NW; w += blockDim.x) {
+      uint32_t uni = 0;
+      for (int q = 0; q < P; ++q) uni |= bm[(size_t)q * NW + w];
+      while (uni) {
+        uint32_t bs[U];
+        T th[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          bs[u] = 32;
+          if (uni) {
+            bs[u] = __ffs(uni) - 1;
+            uni &= uni - 1;
+            th[u] = theta ? theta[seg_base + w * 32 + bs[u]] : T(0);
+          }
+        }
+        auto finish = [&](auto get) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (bs[u] >= 32) continue;
+            const uint32_t bit = 1u << bs[u], below = bit - 1u;
+            const size_t i = seg_base + w * 32 + bs[u];
+            auto g = [&](int q2) { return get(q2, bit, below); };
+            T t = th[u];
+            if (ASYNC) {
+              auto step = [&](int q2) {
+                const T x = add_rn(mul_rn(coefs[q2], g(q2)), t);
+                t = (bm[(size_t)q2 * NW + w] & bit) ? x : t;
+              };
+              if constexpr (PT > 0) {
+#pragma unroll
+                for (int q2 = 0; q2 < PT; ++q2) step(q2);
+              } else {
+                for (int q2 = 0; q2 < P; ++q2) step(q2);
+              }
+            } else {
+              const int rs = order == PSB_ORDER_RING ? rc.start_for(i, n, P) : 0;
+              const T mean = mul_rn(fold_sum_start<T>(g, P, order, rs, dpn, npr), inv);
+              t = add_rn(mul_rn(coef, mean), t);
+              if (mean_out) mean_out[i] = mean;
+            }
+            if (theta) {
+              theta[i] = t;
+              bad |= !is_finite(t);
+            }
+          }
+        };
+        if (staged) {
+          // branch-free: every worker's lookup is issued; absent ones read a
+          // clamped (unused) slot and contribute +0
+          finish([&](int q2, uint32_t bit, uint32_t below) -> T {
+            const uint32_t word = bm[(size_t)q2 * NW + w];
+            const uint32_t at = min(vb[q2] + pre[(size_t)q2 * NW + w] + __popc(word & below), vcap - 1);
+            const T x = sval[at];
+            return (word & bit) ? x : T(0);
+          });
+        } else {
+          finish([&](int q2, uint32_t bit, uint32_t below) -> T {
+            const uint32_t word = bm[(size_t)q2 * NW + w];
+            if (!(word & bit)) return T(0);
+            return pl_val<T>(v, q2, lo[q2] + pre[(size_t)q2 * NW + w] + __popc(word & below));
+          });
         }
       }
     }
+    APPLY_MARK(2);
   }
-  if (bad) sh_bad = 1;
-  __syncthreads();
-  if (threadIdx.x == 0 && sh_bad) atomicOr(flags, 1u);
+  if (bad) atomicOr(flags, 1u);
 }
 
 // P == 1: one payload, every touched index owned by worker 0.
@@ -184,6 +336,7 @@ __global__ void __launch_bounds__(256) k_dense_apply(const T* __restrict__ bufs,
   const size_t nw = (n + 31) / 32;
   const T inv = (T)(1.0 / (double)P);
   bool bad = false;
+  RingChunk rc;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {
     auto get = [&](int q) -> T {
@@ -193,7 +346,8 @@ __global__ void __launch_bounds__(256) k_dense_apply(const T* __restrict__ bufs,
       }
       return bufs[(size_t)q * n + i];
     };
-    const T mean = mul_rn(fold_sum<T>(get, P, order, i, n, dpn, npr), inv);
+    const int rs = order == PSB_ORDER_RING ? rc.start_for(i, n, P) : 0;
+    const T mean = mul_rn(fold_sum_start<T>(get, P, order, rs, dpn, npr), inv);
     if (mean_out) mean_out[i] = mean;
     if (theta) {
       const T th = add_rn(mul_rn(coef, mean), theta[i]);
@@ -261,29 +415,44 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
     PSB_LAUNCH_CHECK(c, "psb_sparse_mean_sgd");
     return PSB_OK;
   }
-  // segment size: P*S*sizeof(T) + 4*S <= 96 KB, S <= 4096
-  int seg_shift = 12;
-  while (seg_shift > 6 && ((size_t)P * sizeof(T) + 4) << seg_shift > 96 * 1024) --seg_shift;
+  // bitmap segments: P * (S/32) * 8 B <= 16 KB (2^10 <= S <= 2^15), plus a
+  // stage of vcap (value, local index) pairs; a segment with more entries
+  // reads them from L2 instead
+  int seg_shift = 15;
+  while (seg_shift > 10 && ((size_t)P * 8) << (seg_shift - 5) > 16 * 1024) --seg_shift;
   const uint32_t nseg = (uint32_t)((n + ((size_t)1 << seg_shift) - 1) >> seg_shift);
   PSB_REQUIRE(c, (size_t)P * (nseg + 1) <= c->seg_cap, "sparse apply: segment table exceeds ctx capacity");
-  const size_t work = std::max((size_t)P * k, (size_t)P * (nseg + 1));
-  const unsigned g1 = (unsigned)std::min<size_t>((work + 255) / 256, (size_t)c->num_sms * 16);
-  k_seg_offsets<<<g1, 256, 0, st>>>(v, P, k, nseg, seg_shift, c->d_seg_off);
-  const size_t smem = (((size_t)P * sizeof(T) + 4) << seg_shift);
+  PSB_REQUIRE(c, k <= 0xffffffffu, "sparse apply: k exceeds 32-bit positions");
+  {
+    const unsigned gx = (unsigned)((k + 256 * kSegU - 1) / (256 * kSegU));
+    k_seg_offsets<<<dim3(gx, (unsigned)P), 256, 0, st>>>(v, P, (uint32_t)k, nseg, seg_shift, c->d_seg_off);
+  }
+  const uint32_t vcap = c->apply_vcap;
+  const size_t smem = (((size_t)P * 8) << (seg_shift - 5)) + (size_t)vcap * sizeof(T);
   WorkerCoefs ws{};
   if (async_mode)
     for (int q = 0; q < P; ++q) ws.v[q] = wscale_host[q];
-  const unsigned grid = nseg;
+  // one CTA per segment: many segments in flight hide the dependent loads
+  const unsigned grid = (unsigned)std::min<size_t>(nseg, 1u << 20);
+  auto launch = [&](auto kern, T* mo) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 256, smem, st>>>(v, P, nseg, seg_shift, vcap, c->d_seg_off, (int)order, dpn, npr, coef, ws,
+                                  theta, n, mo, c->d_flags);
+  };
   if (async_mode) {
-    auto kern = k_sparse_apply<T, true>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, 256, smem, st>>>(v, P, nseg, seg_shift, c->d_seg_off, (int)order, dpn, npr, coef,
-                                  ws, theta, n, nullptr, c->d_flags);
+    switch (P) {
+      case 2: launch(k_sparse_apply_bm<T, true, 2>, nullptr); break;
+      case 4: launch(k_sparse_apply_bm<T, true, 4>, nullptr); break;
+      case 8: launch(k_sparse_apply_bm<T, true, 8>, nullptr); break;
+      default: launch(k_sparse_apply_bm<T, true, 0>, nullptr);
+    }
   } else {
-    auto kern = k_sparse_apply<T, false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, 256, smem, st>>>(v, P, nseg, seg_shift, c->d_seg_off, (int)order, dpn, npr, coef,
-                                  ws, theta, n, mean_out, c->d_flags);
+    switch (P) {
+      case 2: launch(k_sparse_apply_bm<T, false, 2>, mean_out); break;
+      case 4: launch(k_sparse_apply_bm<T, false, 4>, mean_out); break;
+      case 8: launch(k_sparse_apply_bm<T, false, 8>, mean_out); break;
+      default: launch(k_sparse_apply_bm<T, false, 0>, mean_out);
+    }
   }
   c->launches += 2;
   PSB_LAUNCH_CHECK(c, "psb_sparse_mean_sgd");
@@ -317,6 +486,17 @@ static psb_status check_common(psb_ctx* c, int P, size_t n, psb_order order, con
     PSB_REQUIRE(c, topo->racks >= 1 && topo->nodes_per_rack >= 1, "Topology: counts must be >= 1");
   return PSB_OK;
 }
+
+#ifdef PSB_APPLY_TRACE
+extern "C" PSB_API void psb_debug_apply_trace(unsigned long long* out8, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out8, g_apply_trace, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_apply_trace, z, sizeof(z));
+  }
+}
+#endif
 
 extern "C" psb_status psb_sparse_mean_sgd(psb_ctx* c, psb_compressor comp, psb_dtype dt, int P,
                                           const void* payloads, size_t k, psb_order order,

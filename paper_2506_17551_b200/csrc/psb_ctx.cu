@@ -84,6 +84,7 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   c->max_workers = max_workers;
   if (const char* np = getenv("PSB_NO_PREDICT")) c->predict = np[0] == '0';
   if (const char* ns = getenv("PSB_NO_STAGE")) c->no_stage = ns[0] != '0';
+  if (const char* vc = getenv("PSB_APPLY_VCAP")) c->apply_vcap = (uint32_t)std::min(16384l, std::max(0l, atol(vc))) & ~1u;
   auto fail = [&](cudaError_t e) {
     psb_ctx_destroy(c);
     return e == cudaErrorMemoryAllocation ? PSB_ENOMEM : PSB_ECUDA;

@@ -11,18 +11,34 @@
 #pragma once
 #include "psb_internal.cuh"
 
+// The ring chunk containing index i, cached: consecutive indices almost always
+// share a chunk (chunks are n/P long), so the 64-bit divisions run only when
+// the chunk changes.
+struct RingChunk {
+  size_t lo = 1, hi = 0;  // current chunk [lo, hi) (empty initially)
+  int start = 0;          // first worker folded for this chunk: (j + 1) % P
+  __device__ __forceinline__ int start_for(size_t i, size_t n, int P) {
+    if (i < lo || i >= hi) {
+      uint32_t j = (uint32_t)((i * (size_t)P) / n);
+      while (j + 1 < (uint32_t)P && ((size_t)(j + 1) * n) / (size_t)P <= i) ++j;
+      while (j > 0 && ((size_t)j * n) / (size_t)P > i) --j;
+      lo = ((size_t)j * n) / (size_t)P;
+      hi = ((size_t)(j + 1) * n) / (size_t)P;
+      start = (int)((j + 1) % (uint32_t)P);
+    }
+    return start;
+  }
+};
+
+// Fold with an explicit ring start (ignored by the other orders).
 template <class T, class Get>
-__device__ __forceinline__ T fold_sum(const Get& get, int P, int order, size_t i, size_t n,
-                                      uint32_t dpn, uint32_t npr) {
+__device__ __forceinline__ T fold_sum_start(const Get& get, int P, int order, int ring_start, uint32_t dpn,
+                                            uint32_t npr) {
   T acc;
   if (order == PSB_ORDER_RING) {
-    uint32_t j = (uint32_t)((i * (size_t)P) / n);
-    while (j + 1 < (uint32_t)P && ((size_t)(j + 1) * n) / (size_t)P <= i) ++j;
-    while (j > 0 && ((size_t)j * n) / (size_t)P > i) --j;
-    const int start = (int)((j + 1) % (uint32_t)P);
-    acc = get(start);
+    acc = get(ring_start);
     for (int s = 1; s < P; ++s) {
-      int q = start + s;
+      int q = ring_start + s;
       if (q >= P) q -= P;
       acc = add_rn(acc, get(q));
     }
@@ -51,4 +67,12 @@ __device__ __forceinline__ T fold_sum(const Get& get, int P, int order, size_t i
     for (int q = 1; q < P; ++q) acc = add_rn(acc, get(q));
   }
   return acc;
+}
+
+template <class T, class Get>
+__device__ __forceinline__ T fold_sum(const Get& get, int P, int order, size_t i, size_t n, uint32_t dpn,
+                                      uint32_t npr) {
+  RingChunk rc;
+  const int start = order == PSB_ORDER_RING ? rc.start_for(i, n, P) : 0;
+  return fold_sum_start<T>(get, P, order, start, dpn, npr);
 }

@@ -208,6 +208,7 @@ __global__ void __launch_bounds__(256) k_q8_reduce(
   const bool vec_ok = ((((uintptr_t)wcodes) | ((uintptr_t)mcodes) | ((uintptr_t)theta) | wstride) & 15) == 0 &&
                       !mean_out;
   bool bad = false;
+  RingChunk rc;
   for (size_t blk = blk_lo + warp; blk < blk_hi; blk += nwarps) {
     float m[VPL][4];
     float amax = 0.f;
@@ -224,9 +225,12 @@ __global__ void __launch_bounds__(256) k_q8_reduce(
     for (int it = 0; it < VPL; ++it) {
       const size_t e0 = blk * B + (size_t)it * 128 + lane * 4;
       const bool full = vec_ok && e0 + 4 <= n;
-      const int rs0 = order == PSB_ORDER_RING ? (int)((ring_chunk(e0, n, P) + 1) % (uint32_t)P) : 0;
-      const bool same_chunk =
-          order != PSB_ORDER_RING || (e0 + 3 < n && ring_chunk(e0 + 3, n, P) == ring_chunk(e0, n, P));
+      int rs0 = 0;
+      bool same_chunk = true;
+      if (order == PSB_ORDER_RING) {  // cached: divisions only when the chunk changes
+        rs0 = rc.start_for(e0, n, P);
+        same_chunk = e0 + 3 < rc.hi;
+      }
       if (full && same_chunk) {
         auto get4 = [&](int q) -> float4 {
           const char4 cv = *reinterpret_cast<const char4*>(wcodes + (size_t)q * wstride + (e0 - e_base));
