@@ -333,15 +333,25 @@ def ours(args, cfg, world, rank, local_rank):
     dense_bytes = 4.0 * n * P
     value = dense_bytes / (ms_step * 1e-3) / 1e9
     e2e_value = dense_bytes / (e2e_ms * 1e-3) / 1e9
-    # roofline of the dominant kernel (K1 streaming pass): algorithmic bytes
-    # per launch = 12 bytes/element (read g, read r, write r) x n elements
-    k1_bytes = 12.0 * n
+    # roofline of the dominant kernel: algorithmic bytes per launch
+    if comp == "q8" and world == 1:
+        # fused single-rank q8 step: per worker read g, read r, write r; theta read+write
+        k1_name = "k_q8_step1 (quantize + EF + fold + requantize + SGD, one pass)"
+        k1_bytes = (12.0 * W + 8.0) * n
+    elif comp == "q8":
+        b = extra.get("q8_block", 256)
+        k1_name = "k_q8_quant (EF add + per-block int8 quantization)"
+        k1_bytes = W * (13.0 + 4.0 / b) * n
+    else:
+        # K1 streaming pass: 12 bytes/element (read g, read r, write r) x n
+        k1_name = "k_scan<float,MODE_A> (EF add + level-1 histogram)"
+        k1_bytes = 12.0 * n
     k1_gbs = k1_bytes / (k1_avg_ms * 1e-3) / 1e9 if k1_avg_ms > 0 else None
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
             tr = json.load(f)
-        traffic = tr.get(f"{comp}:{n}")
+        traffic = tr.get(f"{comp}:{n}:{world}") or tr.get(f"{comp}:{n}")
     except Exception:
         pass
     # whole-step algorithmic bytes per GPU: 12N + 8k + 8Pk + 8|U| (|U| <= Pk)
@@ -355,7 +365,7 @@ def ours(args, cfg, world, rank, local_rank):
                    "launch": "eager" if args.eager else "cuda-graph of the K timed steps",
                    "compressor": comp, "order": order, "mode": mode,
                    "l2": f"inputs larger than L2: {NB} rotated {4 * n * W / 1e6:.0f} MB gradient buffers"},
-        "roofline": {"bound": "hbm", "kernel": "k_scan<float,MODE_A> (EF add + level-1 histogram)",
+        "roofline": {"bound": "hbm", "kernel": k1_name,
                      "achieved": k1_gbs, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": (k1_gbs / peak) if k1_gbs else None, "traffic": traffic,
                      "alg_bytes_per_launch": k1_bytes, "avg_launch_ms": k1_avg_ms,

@@ -20,6 +20,9 @@ psb_status psb_q8_reduce_launch(psb_ctx* c, const int8_t* wcodes, size_t wstride
                                 size_t blk_hi, size_t n, uint32_t B, psb_order order, uint32_t dpn,
                                 uint32_t npr, int8_t* mcodes, float* mscales, double lr,
                                 float* theta, float* mean_out, cudaStream_t st);
+psb_status psb_q8_step1_launch(psb_ctx* c, const float* g, size_t gstride, float* r, size_t rstride,
+                               int P, size_t n, uint32_t B, psb_order order, uint32_t dpn, uint32_t npr,
+                               double lr, float* theta, float* mean_out, cudaStream_t st);
 psb_status psb_q8_apply_launch(psb_ctx* c, const int8_t* mcodes, const float* mscales, size_t n,
                                uint32_t B, double lr, float* theta, float* mean_out,
                                cudaStream_t st);
@@ -84,6 +87,7 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   c->max_workers = max_workers;
   if (const char* np = getenv("PSB_NO_PREDICT")) c->predict = np[0] == '0';
   if (const char* ns = getenv("PSB_NO_STAGE")) c->no_stage = ns[0] != '0';
+  if (const char* qu = getenv("PSB_Q8_UNFUSED")) c->q8_unfused = qu[0] != '0';
   if (const char* vc = getenv("PSB_APPLY_VCAP")) c->apply_vcap = (uint32_t)std::min(16384l, std::max(0l, atol(vc))) & ~1u;
   auto fail = [&](cudaError_t e) {
     psb_ctx_destroy(c);
@@ -369,12 +373,21 @@ static psb_status q8_step(psb_ctx* c, const psb_step_desc* d, cudaStream_t st) {
     dpn = d->topo.devices_per_node;
     npr = d->topo.nodes_per_rack;
   }
+  if (R == 1 && d->theta && !c->q8_unfused && (P == 1 || d->order != PSB_ORDER_RING)) {
+    // single rank: quantize, fold, requantize and apply in one pass
+    return psb_q8_step1_launch(c, reinterpret_cast<const float*>(d->g), n, reinterpret_cast<float*>(d->r), n, P,
+                               n, B, d->order, dpn, npr, d->lr, reinterpret_cast<float*>(d->theta),
+                               reinterpret_cast<float*>(d->mean_out), st);
+  }
+  const bool prof_quant = R > 1;  // multi-rank: the quantizer is the dominant kernel
+  if (prof_quant && c->prof) cudaEventRecord(psb_prof_event(c), st);
   for (int w = 0; w < W; ++w) {
     const float* g = reinterpret_cast<const float*>(d->g) + (size_t)w * n;
     float* r = d->r ? reinterpret_cast<float*>(d->r) + (size_t)w * n : nullptr;
     s = psb_q8_quant_launch(c, g, r, n, B, lcodes + (size_t)w * n_pad, lscales + (size_t)w * R * nbs, st);
     if (s) return s;
   }
+  if (prof_quant && c->prof) cudaEventRecord(psb_prof_event(c), st);
   float* theta = reinterpret_cast<float*>(d->theta);
   float* mean_out = reinterpret_cast<float*>(d->mean_out);
   if (R == 1) {

@@ -90,6 +90,7 @@ struct psb_ctx {
   int prof = 0;
   int predict = 1;  // K1 threshold prediction (PSB_NO_PREDICT=1 disables)
   uint32_t apply_vcap = 4096;  // PSB_APPLY_VCAP: staged entries per apply segment
+  int q8_unfused = 0;  // PSB_Q8_UNFUSED=1: single-rank q8 step as quant + reduce (diagnostics)
   int no_stage = 0; // PSB_NO_STAGE=1: k_cand reads the list from global memory (diagnostics)
   int cand_smem[2] = {0, 0};  // dynamic shared memory of the cooperative k_cand (f32, f64)
   std::vector<cudaEvent_t> prof_ev;  // pairs (start, stop)

@@ -308,6 +308,160 @@ __global__ void __launch_bounds__(256) k_q8_reduce(
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1u);
 }
 
+// Single-rank fused step (R == 1): per block of B elements, each local worker
+// q's p = r + g is quantized (codes stay in registers), r' = p - xhat written,
+// and xhat = code*scale folded in the reference order; the mean is requantized
+// per block and applied to theta.  Bitwise the same as k_q8_quant followed by
+// k_q8_reduce (same per-element operations in the same order), without the
+// int8 round trip through HBM: 12 B/element per worker + 8 B theta.
+// Fold orders handled sequentially: naive, hierarchical (node/rack/total
+// accumulators), and ring when P == 1; the host uses the unfused path for a
+// ring fold over several local workers (its start worker varies per chunk).
+// The warp walks (block, worker) items; the next item's loads are issued
+// before the current one is processed (register double buffer).
+template <int VPL, bool HIER>
+__global__ void __launch_bounds__(256) k_q8_step1(const float* __restrict__ g, size_t gstride,
+                                                  float* __restrict__ r, size_t rstride, int P, size_t n,
+                                                  int order, uint32_t dpn, uint32_t npr, float coef,
+                                                  float* __restrict__ theta, float* __restrict__ mean_out,
+                                                  uint32_t* flags) {
+  constexpr int B = VPL * 128;
+  const int lane = threadIdx.x & 31;
+  const size_t nb = (n + B - 1) / B;
+  const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  const bool vec_ok = ((((uintptr_t)g) | ((uintptr_t)r) | ((uintptr_t)theta) | ((uintptr_t)mean_out) |
+                        (gstride * 4) | (rstride * 4)) & 15) == 0;
+  const float inv_p = (float)(1.0 / (double)P);
+  bool bad = false;
+  auto load = [&](size_t blk, int q, float (&p)[VPL][4]) {
+    const size_t lo = blk * B;
+    q8_load<VPL>(g + (size_t)q * gstride, r ? r + (size_t)q * rstride : nullptr, n, lo, vec_ok && lo + B <= n,
+                 lane, p);
+  };
+  float p[VPL][4];
+  size_t blk = warp;
+  int q = 0;
+  if (blk < nb) load(blk, 0, p);
+  float acc[VPL][4], node[HIER ? VPL : 1][4], rack[HIER ? VPL : 1][4];
+  float4 thv[VPL];
+  while (blk < nb) {
+    const size_t lo = blk * B;
+    const bool full = vec_ok && lo + B <= n;
+    if (q == 0 && full) {
+#pragma unroll
+      for (int it = 0; it < VPL; ++it)
+        thv[it] = __ldcs(reinterpret_cast<const float4*>(theta + lo + (size_t)it * 128 + lane * 4));
+    }
+    // next item's loads first
+    float pn[VPL][4];
+    size_t nblk = blk;
+    int nq = q + 1;
+    if (nq == P) {
+      nq = 0;
+      nblk = blk + nwarps;
+    }
+    if (nblk < nb) load(nblk, nq, pn);
+    // quantize worker q's block; EF residual; dequantized value x
+    float amax = 0.f;
+#pragma unroll
+    for (int it = 0; it < VPL; ++it)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        amax = fmaxf(amax, fabsf(p[it][c]));
+        bad |= !is_finite(p[it][c]);
+      }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const float scale = __fdiv_rn(amax, 127.0f);
+    const float inv = __frcp_rn(scale);
+    float* rq = r ? r + (size_t)q * rstride : nullptr;
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+      const size_t e = lo + (size_t)it * 128 + lane * 4;
+      float x[4], res[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        x[c] = __fmul_rn((float)q8_code(p[it][c], scale, inv), scale);
+        res[c] = __fsub_rn(p[it][c], x[c]);
+      }
+      if (rq) {
+        if (full) {
+          __stcs(reinterpret_cast<float4*>(rq + e), make_float4(res[0], res[1], res[2], res[3]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (e + c < n) rq[e + c] = res[c];
+        }
+      }
+      // fold (collectives.hpp:68-128 orders, sequential form)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if constexpr (!HIER) {
+          acc[it][c] = q == 0 ? x[c] : __fadd_rn(acc[it][c], x[c]);
+        } else {
+          const uint32_t uq = (uint32_t)q, nd = uq / dpn;
+          node[it][c] = uq % dpn == 0 ? x[c] : __fadd_rn(node[it][c], x[c]);
+          if (uq % dpn == dpn - 1 || q == P - 1) {
+            rack[it][c] = nd % npr == 0 ? node[it][c] : __fadd_rn(rack[it][c], node[it][c]);
+            if (nd % npr == npr - 1 || q == P - 1)
+              acc[it][c] = nd < npr ? rack[it][c] : __fadd_rn(acc[it][c], rack[it][c]);
+          }
+        }
+      }
+    }
+    if (q == P - 1) {
+      // mean, per-block requantization, SGD
+      float m[VPL][4];
+      float mmax = 0.f;
+#pragma unroll
+      for (int it = 0; it < VPL; ++it)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          m[it][c] = __fmul_rn(acc[it][c], inv_p);
+          mmax = fmaxf(mmax, fabsf(m[it][c]));
+        }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mmax = fmaxf(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
+      const float ms = __fdiv_rn(mmax, 127.0f);
+      const float minv = __frcp_rn(ms);
+#pragma unroll
+      for (int it = 0; it < VPL; ++it) {
+        const size_t e = lo + (size_t)it * 128 + lane * 4;
+        float mh[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) mh[c] = __fmul_rn((float)q8_code(m[it][c], ms, minv), ms);
+        if (full) {
+          float4 th = thv[it];
+          th.x = __fadd_rn(__fmul_rn(coef, mh[0]), th.x);
+          th.y = __fadd_rn(__fmul_rn(coef, mh[1]), th.y);
+          th.z = __fadd_rn(__fmul_rn(coef, mh[2]), th.z);
+          th.w = __fadd_rn(__fmul_rn(coef, mh[3]), th.w);
+          __stcs(reinterpret_cast<float4*>(theta + e), th);
+          if (mean_out) *reinterpret_cast<float4*>(mean_out + e) = make_float4(mh[0], mh[1], mh[2], mh[3]);
+          bad |= !is_finite(th.x) || !is_finite(th.y) || !is_finite(th.z) || !is_finite(th.w);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if (e + c >= n) continue;
+            const float th = __fadd_rn(__fmul_rn(coef, mh[c]), theta[e + c]);
+            theta[e + c] = th;
+            if (mean_out) mean_out[e + c] = mh[c];
+            bad |= !is_finite(th);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < VPL; ++it)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) p[it][c] = pn[it][c];
+    blk = nblk;
+    q = nq;
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1u);
+}
+
 __global__ void __launch_bounds__(256) k_q8_apply(const int8_t* __restrict__ mcodes,
                                                   const float* __restrict__ mscales, size_t n,
                                                   uint32_t B, float coef, float* __restrict__ theta,
@@ -389,6 +543,33 @@ psb_status psb_q8_reduce_launch(psb_ctx* c, const int8_t* wcodes, size_t wstride
 #undef PSB_RED
   c->launches += 1;
   PSB_LAUNCH_CHECK(c, "q8 reduce");
+  return PSB_OK;
+}
+
+psb_status psb_q8_step1_launch(psb_ctx* c, const float* g, size_t gstride, float* r, size_t rstride,
+                               int P, size_t n, uint32_t B, psb_order order, uint32_t dpn, uint32_t npr,
+                               double lr, float* theta, float* mean_out, cudaStream_t st) {
+  const size_t nb = (n + B - 1) / B;
+  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((nb + 7) / 8, (size_t)c->num_sms * 8));
+  const float coef = (float)(-lr);
+  if (c->prof) cudaEventRecord(psb_prof_event(c), st);
+  const bool hier = order == PSB_ORDER_HIER && dpn < (uint32_t)P;
+#define PSB_S1(V)                                                                                          \
+  (hier ? k_q8_step1<V, true><<<grid, 256, 0, st>>>(g, gstride, r, rstride, P, n, (int)order, dpn, npr, coef, \
+                                                     theta, mean_out, c->d_flags)                            \
+        : k_q8_step1<V, false><<<grid, 256, 0, st>>>(g, gstride, r, rstride, P, n, (int)order, dpn, npr,      \
+                                                      coef, theta, mean_out, c->d_flags))
+  switch (B) {
+    case 128: PSB_S1(1); break;
+    case 256: PSB_S1(2); break;
+    case 512: PSB_S1(4); break;
+    case 1024: PSB_S1(8); break;
+    default: return psb_set_err(c, PSB_EINVAL, "q8: block must be 128, 256, 512 or 1024");
+  }
+#undef PSB_S1
+  if (c->prof) cudaEventRecord(psb_prof_event(c), st);
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "q8 fused step");
   return PSB_OK;
 }
 

@@ -197,12 +197,13 @@ COMPS = {"topk": L.PSB_COMP_TOPK, "onebit": L.PSB_COMP_ONEBIT, "none": L.PSB_COM
 
 @pytest.mark.parametrize("comp", ["topk", "topk_q8", "none", "q8", "onebit"])
 @pytest.mark.parametrize("order", ["naive", "ring", "hierarchical"])
-@pytest.mark.parametrize("W", [1, 4])
+@pytest.mark.parametrize("W", [1, 3, 4])
 def test_sync_step_virtual_workers(ctx, comp, order, W):
     """psb_sync_step with W virtual workers on one GPU (cfg1 shape) vs the
     oracle composite of sync_data_parallel_step, 10 steps, EF carried."""
     n, k, lr = 100_000, 1_000, 0.05
-    dpn, npr = (2, 2) if order == "hierarchical" and W == 4 else (0, 1)
+    # W=4: 2 nodes in one rack; W=3: a ragged node and two racks
+    dpn, npr = {4: (2, 2), 3: (2, 1)}.get(W, (0, 1)) if order == "hierarchical" else (0, 1)
     topo = topology(1, npr, dpn) if dpn else None
     theta_h = np.zeros(n, dtype=np.float32)
     res_h = np.zeros((W, n), dtype=np.float32)
