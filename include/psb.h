@@ -131,6 +131,13 @@ PSB_API int psb_comm_size(const psb_ctx* ctx);
 /* In-place allgather: buf holds nranks blocks of bytes_per_rank; this rank's
  * block is at buf + rank*bytes_per_rank. */
 PSB_API psb_status psb_allgather(psb_ctx* ctx, void* buf, size_t bytes_per_rank, psb_stream_t stream);
+/* Payload exchange of psb_sync_step / psb_async_round with nranks > 1:
+ * on (default) = pull over NVLink peer memory (CUDA IPC arenas, device-side
+ * sequence flags; set up collectively on first use), off = NCCL all-gather.
+ * PSB_NO_PEER=1 in the environment turns it off at ctx creation. */
+PSB_API psb_status psb_peer_mode(psb_ctx* ctx, int on);
+/* 1 once the peer arenas are mapped. */
+PSB_API int psb_peer_active(const psb_ctx* ctx);
 
 /* ---------------------------------------------------------- generator
  * Counter-based synthetic gradients, identical bits to

@@ -88,6 +88,8 @@ _SIGS = {
     "psb_comm_rank": (_i, [_vp]),
     "psb_comm_size": (_i, [_vp]),
     "psb_allgather": (_i, [_vp, _vp, _sz, _vp]),
+    "psb_peer_mode": (_i, [_vp, _i]),
+    "psb_peer_active": (_i, [_vp]),
     "psb_generate": (_i, [_i, _u64, _u32, _u32, _sz, _vp, _vp]),
     "psb_ef_topk": (_i, [_vp, _i, _i, _vp, _vp, _sz, _sz, _vp, _vp, _vp]),
     "psb_ef_topk_q8": (_i, [_vp, _i, _vp, _vp, _sz, _sz, _vp, _vp, _vp, _vp]),

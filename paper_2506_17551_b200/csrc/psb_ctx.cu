@@ -37,18 +37,6 @@ psb_status psb_cuda_err(psb_ctx* c, cudaError_t e, const char* where) {
   return PSB_ECUDA;
 }
 
-#define CUDA_TRY(c, expr, where)                                  \
-  do {                                                            \
-    cudaError_t e__ = (expr);                                     \
-    if (e__ != cudaSuccess) return psb_cuda_err((c), e__, where); \
-  } while (0)
-
-#define NCCL_TRY(c, expr, where)                                                        \
-  do {                                                                                  \
-    ncclResult_t r__ = (expr);                                                          \
-    if (r__ != ncclSuccess)                                                             \
-      return psb_set_err((c), PSB_ENCCL, std::string(where) + ": " + ncclGetErrorString(r__)); \
-  } while (0)
 
 extern "C" int psb_abi_version(void) { return PSB_ABI_VERSION; }
 
@@ -87,6 +75,7 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   c->max_workers = max_workers;
   if (const char* np = getenv("PSB_NO_PREDICT")) c->predict = np[0] == '0';
   if (const char* ns = getenv("PSB_NO_STAGE")) c->no_stage = ns[0] != '0';
+  if (const char* np = getenv("PSB_NO_PEER")) c->peer_mode = np[0] == '0';
   if (const char* qu = getenv("PSB_Q8_UNFUSED")) c->q8_unfused = qu[0] != '0';
   if (const char* vc = getenv("PSB_APPLY_VCAP")) c->apply_vcap = (uint32_t)std::min(16384l, std::max(0l, atol(vc))) & ~1u;
   auto fail = [&](cudaError_t e) {
@@ -131,6 +120,8 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
 extern "C" void psb_ctx_destroy(psb_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  psb_peer_destroy(c);
   void* ptrs[] = {c->d_flags,    c->d_tk,        c->d_tw,        c->d_hist1,   c->d_histr,
                   c->d_seg_cnt,  c->d_seg_pre,   c->d_cta,       c->d_histd,       c->d_stage_idx, c->d_stage_val,
                   c->d_seg_off,  c->d_partials,  c->d_gather,    c->d_work,    c->d_qmean};
@@ -189,6 +180,7 @@ extern "C" psb_status psb_check(psb_ctx* c, psb_stream_t stream) {
   }
   if (flags) {
     CUDA_TRY(c, cudaMemset(c->d_flags, 0, sizeof(uint32_t)), "psb_check");
+    if (flags & 8u) return psb_set_err(c, PSB_ESTATE, "peer exchange: timed out waiting for a peer rank");
     if (flags & 2u) return psb_set_err(c, PSB_EINVAL, "decompress: index out of range for dim");
     if (flags & 4u) return psb_set_err(c, PSB_EINVAL, "decompress: indices not strictly increasing");
     return psb_set_err(c, PSB_ENONFINITE, "ef_compress_step residual: non-finite entry");
@@ -305,9 +297,22 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
   const int W = d->workers, P = W * c->nranks;
   const size_t es = d->dtype == PSB_F64 ? 8 : 4;
   const size_t blk = psb_payload_bytes(d->compressor, d->dtype, d->k);
-  psb_status s = ensure(c, &c->d_gather, &c->gather_bytes, blk * P, "payload gather buffer");
-  if (s) return s;
-  uint8_t* gb = reinterpret_cast<uint8_t*>(c->d_gather);
+  // multi-rank: payloads go straight into this rank's slots of its NVLink
+  // peer arena (psb_peer.cu); single rank / PSB_NO_PEER: the gather buffer
+  const bool peer = c->nranks > 1 && c->peer_mode;
+  psb_status s;
+  uint8_t* gb;
+  if (peer) {
+    s = psb_peer_ensure(c, blk * P, st);
+    if (s) return s;
+    gb = psb_peer_payload(c);
+    s = psb_peer_wait_ack(c, st);  // peers done reading our previous payload
+    if (s) return s;
+  } else {
+    s = ensure(c, &c->d_gather, &c->gather_bytes, blk * P, "payload gather buffer");
+    if (s) return s;
+    gb = reinterpret_cast<uint8_t*>(c->d_gather);
+  }
   for (int w = 0; w < W; ++w) {
     const int gid = c->rank * W + w;
     uint8_t* slot = gb + (size_t)gid * blk;
@@ -328,7 +333,10 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
     }
     if (s) return s;
   }
-  if (c->nranks > 1) {
+  if (peer) {
+    s = psb_peer_exchange(c, (size_t)W * blk, st);
+    if (s) return s;
+  } else if (c->nranks > 1) {
     if (!c->comm) return psb_set_err(c, PSB_ESTATE, "sync step: communicator not initialised");
     NCCL_TRY(c, ncclAllGather(gb + (size_t)c->rank * W * blk, gb, (size_t)W * blk, ncclUint8, c->comm, st),
              "ncclAllGather(payloads)");

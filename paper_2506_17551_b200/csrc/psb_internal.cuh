@@ -91,11 +91,23 @@ struct psb_ctx {
   int predict = 1;  // K1 threshold prediction (PSB_NO_PREDICT=1 disables)
   uint32_t apply_vcap = 4096;  // PSB_APPLY_VCAP: staged entries per apply segment
   int q8_unfused = 0;  // PSB_Q8_UNFUSED=1: single-rank q8 step as quant + reduce (diagnostics)
+  // NVLink peer exchange (psb_peer.cu)
+  int peer_mode = 1;            // use it when nranks > 1 (PSB_NO_PEER=1 / psb_peer_mode(0): NCCL all-gather)
+  void* peer_arena = nullptr;   // own arena: 4 KB flag header + payload slots
+  size_t peer_bytes = 0;        // payload capacity of the arenas
+  void* peer_base[PSB_MAX_P] = {};  // every rank's arena mapped here (own included)
   int no_stage = 0; // PSB_NO_STAGE=1: k_cand reads the list from global memory (diagnostics)
   int cand_smem[2] = {0, 0};  // dynamic shared memory of the cooperative k_cand (f32, f64)
   std::vector<cudaEvent_t> prof_ev;  // pairs (start, stop)
   size_t prof_used = 0;
 };
+
+// NVLink peer exchange (psb_peer.cu)
+psb_status psb_peer_ensure(psb_ctx* c, size_t payload_bytes, cudaStream_t st);
+uint8_t* psb_peer_payload(psb_ctx* c);
+psb_status psb_peer_wait_ack(psb_ctx* c, cudaStream_t st);
+psb_status psb_peer_exchange(psb_ctx* c, size_t bytes_per_rank, cudaStream_t st);
+void psb_peer_destroy(psb_ctx* c);
 
 // Record a profiling event pair around the dominant kernel (no-op unless enabled).
 cudaEvent_t psb_prof_event(psb_ctx* c);
@@ -113,6 +125,19 @@ psb_status psb_cuda_err(psb_ctx* c, cudaError_t e, const char* where);
   do {                                                                   \
     cudaError_t e_ = cudaGetLastError();                                 \
     if (e_ != cudaSuccess) return psb_cuda_err((ctx), e_, (where));      \
+  } while (0)
+
+#define CUDA_TRY(c, expr, where)                                  \
+  do {                                                            \
+    cudaError_t e__ = (expr);                                     \
+    if (e__ != cudaSuccess) return psb_cuda_err((c), e__, where); \
+  } while (0)
+
+#define NCCL_TRY(c, expr, where)                                                        \
+  do {                                                                                  \
+    ncclResult_t r__ = (expr);                                                          \
+    if (r__ != ncclSuccess)                                                             \
+      return psb_set_err((c), PSB_ENCCL, std::string(where) + ": " + ncclGetErrorString(r__)); \
   } while (0)
 
 static inline size_t psb_align16(size_t b) { return (b + 15) & ~(size_t)15; }

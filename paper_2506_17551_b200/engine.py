@@ -147,6 +147,14 @@ class Context:
         self._ck(self.lib.psb_allgather(self.h, buf.data_ptr(), bytes_per_rank, self.stream()),
                  "psb_allgather")
 
+    def peer_mode(self, on: bool) -> None:
+        """Payload exchange over NVLink peer memory (on, default) or NCCL all-gather."""
+        self._ck(self.lib.psb_peer_mode(self.h, int(bool(on))), "psb_peer_mode")
+
+    @property
+    def peer_active(self) -> bool:
+        return bool(self.lib.psb_peer_active(self.h))
+
     # ---------------------------------------------------------- compressors
     def ef_topk(self, g: torch.Tensor, r: Optional[torch.Tensor], k: int, worker: int = 0,
                 idx_out: Optional[torch.Tensor] = None,

@@ -1,4 +1,6 @@
-"""GPU, >= 2 devices: the NCCL exchange paths (one process per GPU).
+"""GPU, >= 2 devices: the multi-rank exchange paths (one process per GPU):
+payloads over NVLink peer memory (default) or NCCL all-gather, dense/q8
+paths over NCCL.
 
 Every rank owns W local workers (worker id = rank*W + w); after each step the
 replicas must be bitwise identical to each other and to the oracle composite
@@ -17,7 +19,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 
 
-def _worker(rank, nranks, uid, W, comp, order, steps, q):
+def _worker(rank, nranks, uid, W, comp, order, steps, q, peer=True):
     sys.path.insert(0, ROOT)
     try:
         import torch as th
@@ -29,8 +31,11 @@ def _worker(rank, nranks, uid, W, comp, order, steps, q):
         th.cuda.set_device(rank)
         n, k, lr = 50_000, 500, 0.05
         P = W * nranks
-        c = Context(n, k, P, device=rank)
+        c = Context(n, 2 * k, P, device=rank)
         c.comm_init(rank, nranks, uid)
+        c.peer_mode(peer)
+        grow = comp == "topk_grow"  # k doubles mid-run: the peer arenas are re-created
+        comp = "topk" if grow else comp
         code = {"topk": L.PSB_COMP_TOPK, "topk_q8": L.PSB_COMP_TOPK_Q8, "onebit": L.PSB_COMP_ONEBIT,
                 "none": L.PSB_COMP_NONE, "q8": L.PSB_COMP_Q8, "async": L.PSB_COMP_TOPK,
                 "async_q8": L.PSB_COMP_TOPK_Q8}[comp]
@@ -45,6 +50,8 @@ def _worker(rank, nranks, uid, W, comp, order, steps, q):
         for step in range(steps):
             g_all = np.stack([O.generate("llmrec", 7, p, step, n) for p in range(P)])
             g = th.from_numpy(g_all[rank * W:(rank + 1) * W].copy()).cuda()
+            if grow and step == steps // 2:
+                k *= 2
             d = c.step_desc(code, g, res, theta, lr, k, order, 256, topo)
             if comp.startswith("async"):
                 gu = c.async_round(d, 2, gu)
@@ -53,6 +60,9 @@ def _worker(rank, nranks, uid, W, comp, order, steps, q):
                 c.sync_step(d)
                 O.sync_step(g_all, theta_h, lr, comp, k, order, res_h, dpn, npr, 256)
             c.check()
+            if comp.startswith(("topk", "async")) and c.peer_active != peer:
+                q.put((rank, f"peer_active={c.peer_active}, expected {peer}"))
+                return
             got = theta.cpu().numpy()
             if comp == "onebit":
                 worst = max(worst, float(np.max(np.abs(got - theta_h))))
@@ -72,12 +82,12 @@ def _worker(rank, nranks, uid, W, comp, order, steps, q):
         q.put((rank, f"error: {type(e).__name__}: {e}"))
 
 
-def _run(nranks, W, comp, order, steps=4):
+def _run(nranks, W, comp, order, steps=4, peer=True):
     from paper_2506_17551_b200.engine import Context
     uid = Context.unique_id()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, nranks, uid, W, comp, order, steps, q))
+    procs = [ctx.Process(target=_worker, args=(r, nranks, uid, W, comp, order, steps, q, peer))
              for r in range(nranks)]
     for p in procs:
         p.start()
@@ -99,7 +109,20 @@ needs2 = pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GP
     ("topk_q8", "naive", 1), ("onebit", "ring", 1), ("none", "naive", 2),
     ("q8", "naive", 1), ("q8", "ring", 2), ("async", "naive", 2), ("async_q8", "naive", 1),
 ])
-def test_nccl_paths_match_oracle(comp, order, W):
+def test_exchange_paths_match_oracle(comp, order, W):
     nr = min(torch.cuda.device_count(), 4)
     res = _run(nr, W, comp, order)
+    assert all(v == "ok" for v in res.values()), res
+
+
+@needs2
+@pytest.mark.parametrize("comp,order,W,peer,steps", [
+    ("topk", "ring", 1, False, 4), ("async", "naive", 2, False, 4), ("topk_q8", "naive", 1, False, 4),
+    ("topk_grow", "ring", 1, True, 6), ("topk", "ring", 1, True, 12),
+])
+def test_payload_exchange_modes(comp, order, W, peer, steps):
+    """NCCL all-gather fallback, arena re-creation when k grows, and a long
+    run through the device-side sequence flags."""
+    nr = min(torch.cuda.device_count(), 4)
+    res = _run(nr, W, comp, order, steps=steps, peer=peer)
     assert all(v == "ok" for v in res.values()), res
