@@ -361,11 +361,49 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
     }
     run += tot;
   }
+  phase();
   if (staged) {
     __syncthreads();
-#pragma unroll 4
-    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x)
-      scatter(st_idx[j], st_val[j], st_slot[j] != kNoSlot);
+    // batches of U entries per thread: all theta loads of a batch are issued
+    // before any store (the indices are distinct), so U loads per thread are
+    // in flight instead of one dependent round trip per entry
+    constexpr int U = 8;
+    for (uint32_t j0 = threadIdx.x; j0 < cnt; j0 += U * blockDim.x) {
+      uint32_t id[U];
+      T v[U], th[U];
+      uint32_t selm = 0, actm = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t j = j0 + u * blockDim.x;
+        if (j < cnt) {
+          actm |= 1u << u;
+          id[u] = st_idx[j];
+          v[u] = st_val[j];
+          if (st_slot[j] != kNoSlot) selm |= 1u << u;
+        }
+      }
+      if (a.theta) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if ((selm >> u) & 1u) th[u] = a.theta[id[u]];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!((actm >> u) & 1u)) continue;
+        if ((selm >> u) & 1u) {
+          if (a.r && !spec) a.r[id[u]] = T(0);
+          if (a.theta) {
+            const T mean = mul_rn(v[u], T(1));  // P = 1: mean = v * (1/1)
+            const T t2 = add_rn(mul_rn(a.coef, mean), th[u]);
+            a.theta[id[u]] = t2;
+            if (a.mean_out) a.mean_out[id[u]] = mean;
+            bad |= !is_finite(t2);
+          }
+        } else if (spec && a.r) {
+          a.r[id[u]] = v[u];  // unselected candidate: undo the speculative +0
+        }
+      }
+    }
   }
   if (bad) sh_bad = 1;
   __syncthreads();

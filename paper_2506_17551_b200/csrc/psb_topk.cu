@@ -300,6 +300,15 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
     const bool full = a.vec_ok && (base + TILE <= a.n);
     T x[4][VW];
     uint32_t valid = 0;
+    if (MODE == MODE_A && threadIdx.x == 0 && tile + 1 < t_hi && base + 2 * (size_t)TILE <= a.n && a.vec_ok) {
+      // TMA bulk prefetch of the next tile into L2: its loads then hit L2
+      // while this tile's scan and stores run
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + base + TILE),
+                   "r"((uint32_t)(TILE * sizeof(T))) : "memory");
+      if (rr != nullptr)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rr + base + TILE),
+                     "r"((uint32_t)(TILE * sizeof(T))) : "memory");
+    }
     if (full) {
       valid = 0xffffu;
       if (MODE == MODE_A && rr != nullptr) {
