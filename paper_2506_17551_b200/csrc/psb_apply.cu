@@ -116,13 +116,13 @@ __global__ void __launch_bounds__(256) k_seg_offsets(PayloadView v, int P, uint3
 #define PSB_APPLY_MINB 4
 #endif
 template <class T, bool ASYNC, int PT>
-__global__ void __launch_bounds__(256, PSB_APPLY_MINB) k_sparse_apply_bm(PayloadView v, int P_rt, uint32_t nseg,
-                                                         int seg_shift, uint32_t vcap,
-                                                         const uint32_t* __restrict__ seg_off,
-                                                         int order, uint32_t dpn, uint32_t npr,
-                                                         T coef, WorkerCoefs wscale,
-                                                         T* __restrict__ theta, size_t n,
-                                                         T* __restrict__ mean_out, uint32_t* flags) {
+__global__ void __launch_bounds__(256, PSB_APPLY_MINB)
+    k_sparse_apply_bm(PayloadView v, int P_rt, uint32_t nseg, uint32_t seg_lo, const uint32_t* __restrict__ range,
+                      int seg_shift, uint32_t vcap,
+                      const uint32_t* __restrict__ seg_off, int order, uint32_t dpn, uint32_t npr, T coef,
+                      WorkerCoefs wscale, T* __restrict__ theta, size_t n, T* __restrict__ mean_out,
+                      uint32_t* __restrict__ list_idx, T* __restrict__ list_val, uint32_t* list_cnt,
+                      uint32_t* flags) {
   constexpr int U = 4;  // entries per thread per batch
   const int P = PT > 0 ? PT : P_rt;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -132,6 +132,8 @@ __global__ void __launch_bounds__(256, PSB_APPLY_MINB) k_sparse_apply_bm(Payload
   T* sval = reinterpret_cast<T*>(pre + (size_t)P * NW);  // [vcap] staged values
   __shared__ uint32_t lo[PSB_MAX_P], vb[PSB_MAX_P + 1];
   __shared__ T coefs[PSB_MAX_P];
+  __shared__ unsigned long long sh_scan[32];
+  __shared__ uint32_t sh_lbase;
   if (ASYNC && threadIdx.x < (unsigned)P) coefs[threadIdx.x] = (T)(-wscale.v[threadIdx.x]);
   const T inv = (T)(1.0 / (double)P);
   bool bad = false;
@@ -141,6 +143,10 @@ __global__ void __launch_bounds__(256, PSB_APPLY_MINB) k_sparse_apply_bm(Payload
 #ifdef PSB_APPLY_TRACE
   unsigned long long t_prev = gtimer();
 #endif
+  if (range) {  // segment range decided on the device (sharded multi-rank apply)
+    seg_lo = range[0];
+    nseg = range[1] - range[0];
+  }
   for (uint32_t seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
     __syncthreads();  // the previous segment is done with shared memory
     if (threadIdx.x < 32) {
@@ -171,7 +177,7 @@ __global__ void __launch_bounds__(256, PSB_APPLY_MINB) k_sparse_apply_bm(Payload
     const uint32_t tot = vb[P];
     if (!tot) continue;  // uniform across the CTA
     const bool staged = tot <= vcap;
-    const size_t seg_base = (size_t)seg << seg_shift;
+    const size_t seg_base = (size_t)(seg_lo + seg) << seg_shift;
     uint32_t vbr[PT > 0 ? PT : 1];
     if constexpr (PT > 0) {
 #pragma unroll
@@ -229,6 +235,22 @@ __global__ void __launch_bounds__(256, PSB_APPLY_MINB) k_sparse_apply_bm(Payload
     }
     APPLY_MARK(1);
     __syncthreads();
+    // list mode (sharded multi-rank apply): every touched index of the
+    // segment gets one slot of the update list, in (word, bit) order
+    uint32_t lpos = 0;
+    if (list_idx) {
+      uint32_t cnt = 0;
+      for (uint32_t w = threadIdx.x; w < NW; w += blockDim.x) {
+        uint32_t uni = 0;
+        for (int q = 0; q < P; ++q) uni |= bm[(size_t)q * NW + w];
+        cnt += __popc(uni);
+      }
+      unsigned long long tsum;
+      const uint32_t ex = (uint32_t)block_exscan_u64(cnt, sh_scan, &tsum);
+      if (threadIdx.x == 0) sh_lbase = atomicAdd(list_cnt, (uint32_t)tsum);
+      __syncthreads();
+      lpos = sh_lbase + ex;
+    }
     // 2. fold and update by bitmap word: a thread takes word w of the
     //    segment, ORs the P workers' words, and folds each touched index;
     //    theta loads of up to U indices are issued together
@@ -275,6 +297,11 @@ __global__ void __launch_bounds__(256, PSB_APPLY_MINB) k_sparse_apply_bm(Payload
             if (theta) {
               theta[i] = t;
               bad |= !is_finite(t);
+            }
+            if (list_idx) {
+              list_idx[lpos] = (uint32_t)i;
+              list_val[lpos] = t;
+              ++lpos;
             }
           }
         };
@@ -418,8 +445,7 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
   // bitmap segments: P * (S/32) * 8 B <= 16 KB (2^10 <= S <= 2^15), plus a
   // stage of vcap (value, local index) pairs; a segment with more entries
   // reads them from L2 instead
-  int seg_shift = 15;
-  while (seg_shift > 10 && ((size_t)P * 8) << (seg_shift - 5) > 16 * 1024) --seg_shift;
+  const int seg_shift = psb_apply_seg_shift(P);
   const uint32_t nseg = (uint32_t)((n + ((size_t)1 << seg_shift) - 1) >> seg_shift);
   PSB_REQUIRE(c, (size_t)P * (nseg + 1) <= c->seg_cap, "sparse apply: segment table exceeds ctx capacity");
   PSB_REQUIRE(c, k <= 0xffffffffu, "sparse apply: k exceeds 32-bit positions");
@@ -436,8 +462,8 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
   const unsigned grid = (unsigned)std::min<size_t>(nseg, 1u << 20);
   auto launch = [&](auto kern, T* mo) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, 256, smem, st>>>(v, P, nseg, seg_shift, vcap, c->d_seg_off, (int)order, dpn, npr, coef, ws,
-                                  theta, n, mo, c->d_flags);
+    kern<<<grid, 256, smem, st>>>(v, P, nseg, 0u, nullptr, seg_shift, vcap, c->d_seg_off, (int)order, dpn, npr, coef, ws,
+                                  theta, n, mo, nullptr, nullptr, nullptr, c->d_flags);
   };
   if (async_mode) {
     switch (P) {
@@ -473,7 +499,73 @@ psb_status dense_impl(psb_ctx* c, int P, const void* bufs, const uint32_t* words
   return PSB_OK;
 }
 
+template <class T>
+psb_status shard_fold_impl(psb_ctx* c, int P, const uint32_t* sidx, const T* sval, const uint32_t* srow,
+                           const uint32_t* range, int seg_shift, psb_order order, const psb_topology* topo,
+                           double lr, const double* wscale_host, bool async_mode, T* theta, size_t n,
+                           uint32_t* list_idx, T* list_val, uint32_t* list_cnt, cudaStream_t st) {
+  PayloadView v;  // flat view: every worker's slice lives in one (idx, val) array pair
+  v.base = reinterpret_cast<const uint8_t*>(sidx);
+  v.block_bytes = 0;
+  v.val_off = (size_t)(reinterpret_cast<const uint8_t*>(sval) - v.base);
+  v.scale_off = 0;
+  v.q8 = 0;
+  uint32_t dpn, npr;
+  topo_fields(topo, P, &dpn, &npr);
+  const T coef = (T)(-lr);
+  const uint32_t vcap = c->apply_vcap;
+  const size_t smem = (((size_t)P * 8) << (seg_shift - 5)) + (size_t)vcap * sizeof(T);
+  WorkerCoefs ws{};
+  if (async_mode)
+    for (int q = 0; q < P; ++q) ws.v[q] = wscale_host[q];
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // persistent CTAs over the device-decided segment range
+    kern<<<c->num_sms * 4, 256, smem, st>>>(v, P, 0u, 0u, range, seg_shift, vcap, srow, (int)order, dpn, npr, coef,
+                                            ws, theta, n, nullptr, list_idx, list_val, list_cnt, c->d_flags);
+  };
+  if (async_mode) {
+    switch (P) {
+      case 2: launch(k_sparse_apply_bm<T, true, 2>); break;
+      case 4: launch(k_sparse_apply_bm<T, true, 4>); break;
+      case 8: launch(k_sparse_apply_bm<T, true, 8>); break;
+      default: launch(k_sparse_apply_bm<T, true, 0>);
+    }
+  } else {
+    switch (P) {
+      case 2: launch(k_sparse_apply_bm<T, false, 2>); break;
+      case 4: launch(k_sparse_apply_bm<T, false, 4>); break;
+      case 8: launch(k_sparse_apply_bm<T, false, 8>); break;
+      default: launch(k_sparse_apply_bm<T, false, 0>);
+    }
+  }
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "shard fold");
+  return PSB_OK;
+}
+
 }  // namespace
+
+psb_status psb_seg_offsets(psb_ctx* c, psb_compressor comp, psb_dtype dt, int nw, const void* payloads, size_t k,
+                           uint32_t nseg, int seg_shift, uint32_t* rows, cudaStream_t st) {
+  const PayloadView v = make_view(comp, dt, payloads, k);
+  const unsigned gx = (unsigned)((k + 256 * kSegU - 1) / (256 * kSegU));
+  k_seg_offsets<<<dim3(gx, (unsigned)nw), 256, 0, st>>>(v, nw, (uint32_t)k, nseg, seg_shift, rows);
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "segment offsets");
+  return PSB_OK;
+}
+
+psb_status psb_shard_fold(psb_ctx* c, psb_dtype dt, int P, const uint32_t* sidx, const void* sval,
+                          const uint32_t* srow, const uint32_t* range, int seg_shift, psb_order order,
+                          const psb_topology* topo, double lr, const double* wscale, int async_mode, void* theta,
+                          size_t n, uint32_t* list_idx, void* list_val, uint32_t* list_cnt, cudaStream_t st) {
+  if (dt == PSB_F64)
+    return shard_fold_impl<double>(c, P, sidx, (const double*)sval, srow, range, seg_shift, order, topo, lr, wscale,
+                                   async_mode != 0, (double*)theta, n, list_idx, (double*)list_val, list_cnt, st);
+  return shard_fold_impl<float>(c, P, sidx, (const float*)sval, srow, range, seg_shift, order, topo, lr, wscale,
+                                async_mode != 0, (float*)theta, n, list_idx, (float*)list_val, list_cnt, st);
+}
 
 static psb_status check_common(psb_ctx* c, int P, size_t n, psb_order order, const psb_topology* topo) {
   PSB_REQUIRE(c, c != nullptr, "null ctx");

@@ -76,6 +76,8 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   if (const char* np = getenv("PSB_NO_PREDICT")) c->predict = np[0] == '0';
   if (const char* ns = getenv("PSB_NO_STAGE")) c->no_stage = ns[0] != '0';
   if (const char* np = getenv("PSB_NO_PEER")) c->peer_mode = np[0] == '0';
+  if (const char* sh = getenv("PSB_SHARD")) c->shard_mode = sh[0] != '0';
+  if (const char* sm = getenv("PSB_STEP_MARKS")) c->marks_on = sm[0] != '0';
   if (const char* qu = getenv("PSB_Q8_UNFUSED")) c->q8_unfused = qu[0] != '0';
   if (const char* vc = getenv("PSB_APPLY_VCAP")) c->apply_vcap = (uint32_t)std::min(16384l, std::max(0l, atol(vc))) & ~1u;
   auto fail = [&](cudaError_t e) {
@@ -130,6 +132,26 @@ extern "C" void psb_ctx_destroy(psb_ctx* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
   delete c;
+}
+
+void psb_mark(psb_ctx* c, cudaStream_t st) {
+  if (!c->marks_on) return;
+  if (c->marks_used == c->mark_ev.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->mark_ev.push_back(e);
+  }
+  cudaEventRecord(c->mark_ev[c->marks_used++], st);
+}
+
+// Milliseconds between consecutive milestones recorded since the last call.
+extern "C" PSB_API int psb_debug_marks(psb_ctx* c, float* out, int max) {
+  if (!c) return 0;
+  cudaDeviceSynchronize();
+  int m = 0;
+  for (size_t i = 1; i < c->marks_used && m < max; ++i, ++m) cudaEventElapsedTime(out + m, c->mark_ev[i - 1], c->mark_ev[i]);
+  c->marks_used = 0;
+  return m;
 }
 
 cudaEvent_t psb_prof_event(psb_ctx* c) {
@@ -292,22 +314,57 @@ static psb_status check_desc(psb_ctx* c, const psb_step_desc* d) {
 // buffer and exchange; on return the gather buffer holds all P payloads.
 // fuse_apply (P == 1, sync, top-k): the SGD update of the single payload is
 // done inside K1's final write (psb_topk_run_fused), no separate apply pass.
+//
+// Multi-rank over NVLink peer memory, two modes (psb_peer.cu):
+//   full    -- every rank pulls all P payloads, then applies them all;
+//   sharded -- (ShardPlan non-null on return .on) rank r folds only segments
+//              [seg_lo, seg_hi) of the index space: the producer also writes
+//              its payloads' per-segment offsets into its arena; shard_apply
+//              pulls the matching slices, folds them into theta and an update
+//              list, and applies the other ranks' lists.
+struct ShardPlan {
+  bool on = false;
+  int seg_shift = 0;
+  uint32_t nseg = 0;
+  size_t blk = 0, tab_off = 0, list_off = 0, list_voff = 0, cap = 0;
+};
+
 static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaStream_t st,
-                                      uint8_t** payloads_out, bool fuse_apply = false) {
+                                      uint8_t** payloads_out, bool fuse_apply = false,
+                                      ShardPlan* plan = nullptr) {
   const int W = d->workers, P = W * c->nranks;
   const size_t es = d->dtype == PSB_F64 ? 8 : 4;
   const size_t blk = psb_payload_bytes(d->compressor, d->dtype, d->k);
   // multi-rank: payloads go straight into this rank's slots of its NVLink
   // peer arena (psb_peer.cu); single rank / PSB_NO_PEER: the gather buffer
   const bool peer = c->nranks > 1 && c->peer_mode;
+  const bool shard = peer && plan != nullptr && c->shard_mode && d->mean_out == nullptr && d->theta && P >= 2;
   psb_status s;
   uint8_t* gb;
   if (peer) {
-    s = psb_peer_ensure(c, blk * P, st);
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    size_t region = al(blk * P);
+    if (shard) {
+      ShardPlan& sp = *plan;
+      sp.on = true;
+      sp.blk = blk;
+      sp.seg_shift = psb_apply_seg_shift(P);
+      sp.nseg = (uint32_t)((d->n + ((size_t)1 << sp.seg_shift) - 1) >> sp.seg_shift);
+      sp.tab_off = region;
+      region += al(sizeof(uint32_t) * P * (sp.nseg + 1));
+      sp.cap = std::min((size_t)P * d->k, d->n);
+      sp.list_off = region;
+      region += al(sizeof(uint32_t) * sp.cap);
+      sp.list_voff = region;
+      region += al(es * sp.cap);
+    }
+    s = psb_peer_ensure(c, region, st);
     if (s) return s;
     gb = psb_peer_payload(c);
-    s = psb_peer_wait_ack(c, st);  // peers done reading our previous payload
+    psb_mark(c, st);
+    s = psb_peer_wait_ack(c, st);  // peers done with our previous payloads / update list
     if (s) return s;
+    psb_mark(c, st);
   } else {
     s = ensure(c, &c->d_gather, &c->gather_bytes, blk * P, "payload gather buffer");
     if (s) return s;
@@ -333,9 +390,20 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
     }
     if (s) return s;
   }
-  if (peer) {
+  psb_mark(c, st);
+  if (shard) {
+    const ShardPlan& sp = *plan;
+    uint32_t* tab = reinterpret_cast<uint32_t*>(gb + sp.tab_off) + (size_t)c->rank * W * (sp.nseg + 1);
+    s = psb_seg_offsets(c, d->compressor, d->dtype, W, gb + (size_t)c->rank * W * blk, d->k, sp.nseg, sp.seg_shift,
+                        tab, st);
+    if (s) return s;
+    s = psb_peer_signal(c, st);
+    if (s) return s;
+    psb_mark(c, st);
+  } else if (peer) {
     s = psb_peer_exchange(c, (size_t)W * blk, st);
     if (s) return s;
+    psb_mark(c, st);
   } else if (c->nranks > 1) {
     if (!c->comm) return psb_set_err(c, PSB_ESTATE, "sync step: communicator not initialised");
     NCCL_TRY(c, ncclAllGather(gb + (size_t)c->rank * W * blk, gb, (size_t)W * blk, ncclUint8, c->comm, st),
@@ -343,6 +411,44 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
   }
   *payloads_out = gb;
   return PSB_OK;
+}
+
+// Sharded apply after compress_and_gather (plan.on): pull this rank's slices,
+// fold them (theta + update list), publish, apply the other ranks' lists.
+static psb_status shard_apply(psb_ctx* c, const psb_step_desc* d, const ShardPlan& sp, const double* wscale,
+                              bool async_mode, cudaStream_t st) {
+  const int W = d->workers, P = W * c->nranks;
+  const size_t es = d->dtype == PSB_F64 ? 8 : 4;
+  // local scratch: flat slices (idx | val) of up to P*k entries, P rows of up
+  // to nseg+1 offsets, the device-decided segment range
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t cap = (size_t)P * d->k;
+  const size_t o_val = al(sizeof(uint32_t) * cap);
+  const size_t o_row = o_val + al(es * cap);
+  const size_t o_rng = o_row + al(sizeof(uint32_t) * P * ((size_t)sp.nseg + 1));
+  const size_t total = o_rng + 256;
+  psb_status s = ensure(c, &c->d_gather, &c->gather_bytes, total, "shard scratch");
+  if (s) return s;
+  uint8_t* ws = reinterpret_cast<uint8_t*>(c->d_gather);
+  uint32_t* sidx = reinterpret_cast<uint32_t*>(ws);
+  void* sval = ws + o_val;
+  uint32_t* srow = reinterpret_cast<uint32_t*>(ws + o_row);
+  uint32_t* range = reinterpret_cast<uint32_t*>(ws + o_rng);
+  const size_t voff = psb_align16(d->k * 4);
+  const size_t soff = voff + psb_align16(d->k);
+  s = psb_shard_pull(c, d->dtype, W, d->compressor == PSB_COMP_TOPK_Q8, sp.blk, voff, soff, sp.tab_off, sp.nseg,
+                     range, sidx, sval, srow, (size_t)W * d->k, st);
+  if (s) return s;
+  psb_mark(c, st);
+  uint8_t* region = psb_peer_payload(c);
+  s = psb_shard_fold(c, d->dtype, P, sidx, sval, srow, range, sp.seg_shift, d->order, &d->topo, d->lr,
+                     wscale, async_mode, d->theta, d->n, reinterpret_cast<uint32_t*>(region + sp.list_off),
+                     region + sp.list_voff, psb_peer_list_cnt(c), st);
+  if (s) return s;
+  psb_mark(c, st);
+  s = psb_shard_finish(c, d->dtype, sp.list_off, sp.list_voff, d->theta, sp.cap, st);
+  psb_mark(c, st);
+  return s;
 }
 
 static psb_status q8_step(psb_ctx* c, const psb_step_desc* d, cudaStream_t st) {
@@ -448,10 +554,14 @@ extern "C" psb_status psb_sync_step(psb_ctx* c, const psb_step_desc* d, psb_stre
     case PSB_COMP_TOPK_Q8: {
       uint8_t* pl = nullptr;
       const bool fuse = P == 1 && d->compressor == PSB_COMP_TOPK;
-      s = compress_and_gather(c, d, st, &pl, fuse);
+      ShardPlan sp;
+      s = compress_and_gather(c, d, st, &pl, fuse, &sp);
       if (s || fuse) return s;
-      return psb_sparse_mean_sgd(c, d->compressor, d->dtype, P, pl, d->k, d->order, &d->topo, d->lr,
-                                 d->theta, d->n, d->mean_out, stream);
+      if (sp.on) return shard_apply(c, d, sp, nullptr, false, st);
+      s = psb_sparse_mean_sgd(c, d->compressor, d->dtype, P, pl, d->k, d->order, &d->topo, d->lr,
+                              d->theta, d->n, d->mean_out, stream);
+      psb_mark(c, st);
+      return s;
     }
     case PSB_COMP_ONEBIT: {
       const size_t nw = (d->n + 31) / 32;
@@ -513,7 +623,8 @@ extern "C" psb_status psb_async_round(psb_ctx* c, const psb_step_desc* d, uint32
   cudaStream_t st = (cudaStream_t)stream;
   const int P = d->workers * c->nranks;
   uint8_t* pl = nullptr;
-  s = compress_and_gather(c, d, st, &pl);
+  ShardPlan sp;
+  s = compress_and_gather(c, d, st, &pl, false, &sp);
   if (s) return s;
   std::vector<double> scale(P);
   const uint64_t g0 = *global_updates;
@@ -522,7 +633,8 @@ extern "C" psb_status psb_async_round(psb_ctx* c, const psb_step_desc* d, uint32
     const uint64_t tau = std::min<uint64_t>(g0 + (uint64_t)p, (uint64_t)p % bound);
     scale[p] = d->lr / (1.0 + (double)tau);  // strategies.hpp:127
   }
-  s = psb_sparse_async_apply(c, d->compressor, d->dtype, P, pl, d->k, scale.data(), d->theta, d->n, stream);
+  if (sp.on) s = shard_apply(c, d, sp, scale.data(), true, st);
+  else s = psb_sparse_async_apply(c, d->compressor, d->dtype, P, pl, d->k, scale.data(), d->theta, d->n, stream);
   if (s) return s;
   *global_updates = g0 + (uint64_t)P;
   return PSB_OK;

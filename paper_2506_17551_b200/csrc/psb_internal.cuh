@@ -96,11 +96,19 @@ struct psb_ctx {
   void* peer_arena = nullptr;   // own arena: 4 KB flag header + payload slots
   size_t peer_bytes = 0;        // payload capacity of the arenas
   void* peer_base[PSB_MAX_P] = {};  // every rank's arena mapped here (own included)
+  int shard_mode = 0;           // sharded multi-rank sparse apply (psb_peer_mode 2 / PSB_SHARD=1)
   int no_stage = 0; // PSB_NO_STAGE=1: k_cand reads the list from global memory (diagnostics)
   int cand_smem[2] = {0, 0};  // dynamic shared memory of the cooperative k_cand (f32, f64)
   std::vector<cudaEvent_t> prof_ev;  // pairs (start, stop)
   size_t prof_used = 0;
+  // step milestones (PSB_STEP_MARKS=1, eager diagnostics: psb_debug_marks)
+  int marks_on = 0;
+  std::vector<cudaEvent_t> mark_ev;
+  size_t marks_used = 0;
 };
+
+// Records the next step milestone event (no-op unless PSB_STEP_MARKS=1).
+void psb_mark(psb_ctx* c, cudaStream_t st);
 
 // NVLink peer exchange (psb_peer.cu)
 psb_status psb_peer_ensure(psb_ctx* c, size_t payload_bytes, cudaStream_t st);
@@ -108,6 +116,28 @@ uint8_t* psb_peer_payload(psb_ctx* c);
 psb_status psb_peer_wait_ack(psb_ctx* c, cudaStream_t st);
 psb_status psb_peer_exchange(psb_ctx* c, size_t bytes_per_rank, cudaStream_t st);
 void psb_peer_destroy(psb_ctx* c);
+uint32_t* psb_peer_list_cnt(psb_ctx* c);
+psb_status psb_peer_signal(psb_ctx* c, cudaStream_t st);
+psb_status psb_shard_pull(psb_ctx* c, psb_dtype dt, int W, int q8, size_t blk, size_t voff, size_t soff,
+                          size_t tab_off, uint32_t nseg, uint32_t* range, uint32_t* sidx, void* sval,
+                          uint32_t* srow, size_t max_entries, cudaStream_t st);
+psb_status psb_shard_finish(psb_ctx* c, psb_dtype dt, size_t list_off, size_t list_voff, void* theta,
+                            size_t max_entries, cudaStream_t st);
+// sparse apply pieces (psb_apply.cu)
+psb_status psb_seg_offsets(psb_ctx* c, psb_compressor comp, psb_dtype dt, int nw, const void* payloads, size_t k,
+                           uint32_t nseg, int seg_shift, uint32_t* rows, cudaStream_t st);
+psb_status psb_shard_fold(psb_ctx* c, psb_dtype dt, int P, const uint32_t* sidx, const void* sval,
+                          const uint32_t* srow, const uint32_t* range, int seg_shift, psb_order order,
+                          const psb_topology* topo, double lr, const double* wscale, int async_mode, void* theta,
+                          size_t n, uint32_t* list_idx, void* list_val, uint32_t* list_cnt, cudaStream_t st);
+
+// Segment size of the P-worker sparse apply: P bitmaps of S bits (x2 with the
+// word ranks) within 16 KB of shared memory, 2^10 <= S <= 2^15.
+static inline int psb_apply_seg_shift(int P) {
+  int s = 15;
+  while (s > 10 && ((size_t)P * 8) << (s - 5) > 16 * 1024) --s;
+  return s;
+}
 
 // Record a profiling event pair around the dominant kernel (no-op unless enabled).
 cudaEvent_t psb_prof_event(psb_ctx* c);

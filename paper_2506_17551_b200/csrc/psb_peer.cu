@@ -20,14 +20,20 @@
 // the kernel sets flag bit 3 and psb_check reports PSB_ESTATE instead of
 // hanging.
 #include <cstdio>
+#include <cstdlib>
 
 #include "psb_internal.cuh"
 
 namespace {
 
 constexpr size_t kHdrBytes = 4096;
-// header words: [0, 32) ready[p], [32, 64) ack[p], 64 local seq, 65 pull CTA counter
-constexpr int kReady = 0, kAck = 32, kSeq = 64, kCtr = 65;
+// header words: [0,32) ready[p]: p's payloads of seq are in place
+//               [32,64) ackp[p]: p has finished reading our payloads of seq
+//               [64,96) upd[p]: p's update list of seq is complete (sharded apply)
+//               [96,128) acku[p]: p has finished reading our update list of seq
+//               128 local seq, 129/130 last-CTA counters, 131 update-list length
+constexpr int kReady = 0, kAck = 32, kUpd = 64, kAckU = 96, kSeq = 128, kCtr = 129, kCtr2 = 130,
+              kListCnt = 131;
 constexpr unsigned long long kSpinNs = 10ull * 1000 * 1000 * 1000;
 
 struct PeerPtrs {
@@ -61,8 +67,32 @@ __device__ bool wait_all(const uint32_t* hdr, int slot0, int R, int rank, uint32
   return true;
 }
 
+// Step start: every peer is done with our previous payloads and update list;
+// then the list may be reset.
 __global__ void k_peer_wait_ack(uint32_t* hdr, int R, int rank, uint32_t* flags) {
-  if (!wait_all(hdr, kAck, R, rank, hdr[kSeq])) atomicOr(flags, 8u);
+  const uint32_t s = hdr[kSeq];
+  if (!wait_all(hdr, kAck, R, rank, s) || !wait_all(hdr, kAckU, R, rank, s)) atomicOr(flags, 8u);
+  hdr[kListCnt] = 0;
+}
+
+// Last CTA out (counter word ctr) publishes value s into slot0 + rank of every peer.
+__device__ void last_cta_publish(const PeerPtrs& pp, int R, int rank, int ctr, int slot0, int slot1,
+                                 uint32_t s) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t* hdr = reinterpret_cast<uint32_t*>(pp.base[rank]);
+    __threadfence();
+    if (atomicAdd(hdr + ctr, 1u) == gridDim.x - 1) {
+      hdr[ctr] = 0;
+      __threadfence_system();
+      for (int p = 0; p < R; ++p) {
+        if (p == rank) continue;
+        uint32_t* ph = reinterpret_cast<uint32_t*>(pp.base[p]);
+        st_release_sys(ph + slot0 + rank, s);
+        if (slot1 >= 0) st_release_sys(ph + slot1 + rank, s);
+      }
+    }
+  }
 }
 
 __global__ void k_peer_signal(PeerPtrs pp, int R, int rank) {
@@ -110,17 +140,226 @@ __global__ void __launch_bounds__(256) k_peer_pull(PeerPtrs pp, int R, int rank,
     for (int u = 0; u < U; ++u)
       if (dst[u]) *dst[u] = v[u];
   }
-  // last CTA out acknowledges to every peer
+  // last CTA out acknowledges to every peer (no update list in this mode)
+  last_cta_publish(pp, R, rank, kCtr, kAck, kAckU, s);
+}
+
+// ------------------------------------------------------ sharded apply
+// Rank r folds only the segments [seg_lo, seg_hi) of the index space; it
+// pulls from every worker's payload just the entries inside them (the
+// producer's per-segment offsets tell where), folds them locally into theta
+// and an update list (index, new theta), and every rank then applies the
+// other ranks' lists.  NVLink traffic per rank: ~W*k payload entries in, the
+// other shards' update lists in -- instead of all P payloads.
+struct ShardArgs {
+  PeerPtrs pp;
+  int R, rank, W, P, q8;
+  size_t blk, voff, soff;  // payload block layout (psb_payload_bytes)
+  size_t tab_off;          // per-worker segment offset rows, from the payload region start
+  uint32_t nseg;
+  uint32_t* range;         // [seg_lo, seg_hi) of this rank, written by k_shard_plan
+  uint32_t* sidx;  // local flat slices: indices
+  void* sval;      //                    values (T)
+  uint32_t* srow;  // P x (seg_hi - seg_lo + 1) offsets into the flat slices
+  uint32_t* flags;
+};
+
+__device__ __forceinline__ const uint32_t* shard_tab(const ShardArgs& a, int q) {
+  return reinterpret_cast<const uint32_t*>(a.pp.base[q / a.W] + kHdrBytes + a.tab_off) + (size_t)q * (a.nseg + 1);
+}
+
+// Balanced shard boundaries (one CTA, every rank computes the same ones):
+// rank r takes segments [b_r, b_{r+1}) with b_r the first segment whose
+// cumulative entry count over all P workers, cum(s) = sum_q tab_q[s], reaches
+// r*P*k/R.  cum is sampled at 1024 points, then the bracketing interval is
+// searched exactly.
+__global__ void __launch_bounds__(1024) k_shard_plan(ShardArgs a, uint32_t k) {
+  uint32_t* hdr = reinterpret_cast<uint32_t*>(a.pp.base[a.rank]);
+  __shared__ int ok;
+  __shared__ unsigned long long samp[1025];
+  __shared__ uint32_t bnd[2];
+  if (threadIdx.x == 0) ok = wait_all(hdr, kReady, a.R, a.rank, hdr[kSeq]);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(hdr + kCtr, 1u) == gridDim.x - 1) {
-      hdr[kCtr] = 0;
-      __threadfence_system();
-      for (int p = 0; p < R; ++p)
-        if (p != rank) st_release_sys(reinterpret_cast<uint32_t*>(pp.base[p]) + kAck + rank, s);
+  if (!ok) {
+    if (threadIdx.x == 0) atomicOr(a.flags, 8u);
+    return;
+  }
+  // cost model: entries + one average segment's worth per segment (the
+  // per-segment fixed cost of the fold), so sparse regions get fewer segments
+  const unsigned long long avg = ((unsigned long long)a.P * k + a.nseg - 1) / a.nseg;
+  auto cum = [&](uint32_t sg) {
+    unsigned long long c = 0;
+    for (int q = 0; q < a.P; ++q) c += shard_tab(a, q)[sg];
+    return c + avg * sg;
+  };
+  const uint32_t t = threadIdx.x;
+  const uint32_t ns = a.nseg;
+  samp[t] = cum((uint32_t)((unsigned long long)t * ns / 1024));
+  if (t == 0) samp[1024] = (unsigned long long)a.P * k + avg * ns;
+  __syncthreads();
+  const unsigned long long total = (unsigned long long)a.P * k + avg * ns;
+  for (int side = 0; side < 2; ++side) {
+    const int r = a.rank + side;
+    const unsigned long long target = total * (unsigned long long)r / (unsigned long long)a.R;
+    if (r == 0 || r == a.R) {
+      if (t == 0) bnd[side] = r == 0 ? 0u : ns;
+      continue;
+    }
+    // last sample below target: the boundary lies in (s_i, s_{i+1}]
+    __shared__ uint32_t si;
+    if (t < 1024 && samp[t] < target && samp[t + 1] >= target) si = t;
+    if (t == 0 && samp[0] >= target) si = 0xffffffffu;
+    __syncthreads();
+    if (si == 0xffffffffu) {
+      if (t == 0) bnd[side] = 0;
+    } else {
+      const uint32_t lo = (uint32_t)((unsigned long long)si * ns / 1024);
+      const uint32_t hi = si + 1 == 1024 ? ns : (uint32_t)((unsigned long long)(si + 1) * ns / 1024);
+      if (t == 0) bnd[side] = hi;
+      __syncthreads();
+      for (uint32_t sg = lo + 1 + t; sg < hi; sg += blockDim.x)
+        if (cum(sg) >= target) atomicMin(&bnd[side], sg);
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    a.range[0] = bnd[0];
+    a.range[1] = max(bnd[0], bnd[1]);
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_shard_pull(ShardArgs a) {
+  uint32_t* hdr = reinterpret_cast<uint32_t*>(a.pp.base[a.rank]);
+  const uint32_t s = hdr[kSeq];
+  const uint32_t seg_lo = a.range[0], seg_hi = a.range[1];
+  __shared__ uint32_t s_a[PSB_MAX_P], s_base[PSB_MAX_P + 1];  // (peers are ready: k_shard_plan waited)
+  auto tab = [&](int q) { return shard_tab(a, q); };
+  auto block = [&](int q) { return a.pp.base[q / a.W] + kHdrBytes + (size_t)q * a.blk; };
+  if (threadIdx.x < 32) {
+    const int q = threadIdx.x;
+    uint32_t len = 0, lo = 0;
+    if (q < a.P) {
+      lo = tab(q)[seg_lo];
+      len = tab(q)[seg_hi] - lo;
+    }
+    uint32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (q >= o) incl += t;
+    }
+    if (q < a.P) {
+      s_a[q] = lo;
+      s_base[q + 1] = incl;
+    }
+    if (q == 0) s_base[0] = 0;
+  }
+  __syncthreads();
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t gt = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // rows, rebased onto the flat slices
+  const uint32_t nr = seg_hi - seg_lo + 1;
+  for (size_t t = gt; t < (size_t)a.P * nr; t += stride) {
+    const int q = (int)(t / nr);
+    const uint32_t sj = (uint32_t)(t - (size_t)q * nr);
+    a.srow[t] = s_base[q] + (tab(q)[seg_lo + sj] - s_a[q]);
+  }
+  // entries; a batch issues all of its remote loads first
+  const uint32_t total = s_base[a.P];
+  T* sval = reinterpret_cast<T*>(a.sval);
+  constexpr int U = 4;
+  for (size_t e0 = gt; e0 < total; e0 += U * stride) {
+    uint32_t id[U];
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const size_t e = e0 + u * stride;
+      if (e < total) {
+        int q = 0;
+        while (q + 1 < a.P && s_base[q + 1] <= e) ++q;
+        const uint32_t j = s_a[q] + (uint32_t)(e - s_base[q]);
+        const uint8_t* b = block(q);
+        id[u] = reinterpret_cast<const uint32_t*>(b)[j];
+        if (a.q8) {
+          const int8_t code = reinterpret_cast<const int8_t*>(b + a.voff)[j];
+          v[u] = (T)__fmul_rn((float)code, reinterpret_cast<const float*>(b + a.soff)[j >> 7]);
+        } else {
+          v[u] = reinterpret_cast<const T*>(b + a.voff)[j];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const size_t e = e0 + u * stride;
+      if (e < total) {
+        a.sidx[e] = id[u];
+        sval[e] = v[u];
+      }
     }
   }
+  last_cta_publish(a.pp, a.R, a.rank, kCtr, kAck, -1, s);  // done with the peers' payloads
+}
+
+// Our update list is complete: publish it.
+__global__ void k_peer_publish_upd(PeerPtrs pp, int R, int rank) {
+  const uint32_t s = reinterpret_cast<uint32_t*>(pp.base[rank])[kSeq];
+  __threadfence_system();
+  for (int p = 0; p < R; ++p)
+    if (p != rank) st_release_sys(reinterpret_cast<uint32_t*>(pp.base[p]) + kUpd + rank, s);
+}
+
+// theta[idx] = new value, for every other rank's update list (remote reads).
+template <class T>
+__global__ void __launch_bounds__(256) k_shard_scatter(PeerPtrs pp, int R, int rank, size_t list_off,
+                                                       size_t list_voff, T* __restrict__ theta, uint32_t* flags) {
+  uint32_t* hdr = reinterpret_cast<uint32_t*>(pp.base[rank]);
+  const uint32_t s = hdr[kSeq];
+  __shared__ int ok;
+  __shared__ uint32_t s_base[PSB_MAX_P + 1];
+  if (threadIdx.x == 0) ok = wait_all(hdr, kUpd, R, rank, s);
+  __syncthreads();
+  if (!ok) {
+    if (threadIdx.x == 0) atomicOr(flags, 8u);
+    return;
+  }
+  if (threadIdx.x < 32) {
+    const int q = threadIdx.x;
+    uint32_t len = 0;
+    if (q < R && q != rank) len = ld_acquire_sys(reinterpret_cast<const uint32_t*>(pp.base[q]) + kListCnt);
+    uint32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (q >= o) incl += t;
+    }
+    if (q < R) s_base[q + 1] = incl;
+    if (q == 0) s_base[0] = 0;
+  }
+  __syncthreads();
+  const uint32_t total = s_base[R];
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  constexpr int U = 8;
+  for (size_t e0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += U * stride) {
+    uint32_t id[U];
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const size_t e = e0 + u * stride;
+      if (e < total) {
+        int q = 0;
+        while (q + 1 < R && s_base[q + 1] <= e) ++q;
+        const size_t j = e - s_base[q];
+        const uint8_t* b = pp.base[q] + kHdrBytes;
+        id[u] = __ldcs(reinterpret_cast<const uint32_t*>(b + list_off) + j);
+        v[u] = __ldcs(reinterpret_cast<const T*>(b + list_voff) + j);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * stride < total) theta[id[u]] = v[u];
+  }
+  last_cta_publish(pp, R, rank, kCtr2, kAckU, -1, s);  // done with the peers' lists
 }
 
 PeerPtrs peer_ptrs(const psb_ctx* c) {
@@ -215,10 +454,134 @@ psb_status psb_peer_exchange(psb_ctx* c, size_t bytes_per_rank, cudaStream_t st)
 
 void psb_peer_destroy(psb_ctx* c) { peer_release(c); }
 
-extern "C" psb_status psb_peer_mode(psb_ctx* c, int on) {
+uint32_t* psb_peer_list_cnt(psb_ctx* c) { return reinterpret_cast<uint32_t*>(c->peer_arena) + kListCnt; }
+
+psb_status psb_peer_signal(psb_ctx* c, cudaStream_t st) {
+  k_peer_signal<<<1, 1, 0, st>>>(peer_ptrs(c), c->nranks, c->rank);
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "peer signal");
+  return PSB_OK;
+}
+
+psb_status psb_shard_pull(psb_ctx* c, psb_dtype dt, int W, int q8, size_t blk, size_t voff, size_t soff,
+                          size_t tab_off, uint32_t nseg, uint32_t* range, uint32_t* sidx, void* sval,
+                          uint32_t* srow, size_t max_entries, cudaStream_t st) {
+  ShardArgs a;
+  a.pp = peer_ptrs(c);
+  a.R = c->nranks;
+  a.rank = c->rank;
+  a.W = W;
+  a.P = W * c->nranks;
+  a.q8 = q8;
+  a.blk = blk;
+  a.voff = voff;
+  a.soff = soff;
+  a.tab_off = tab_off;
+  a.nseg = nseg;
+  a.range = range;
+  a.sidx = sidx;
+  a.sval = sval;
+  a.srow = srow;
+  a.flags = c->d_flags;
+  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((max_entries + 1023) / 1024,
+                                                                         (size_t)c->num_sms * 4));
+  k_shard_plan<<<1, 1024, 0, st>>>(a, (uint32_t)(max_entries / (size_t)W));
+  if (dt == PSB_F64) k_shard_pull<double><<<grid, 256, 0, st>>>(a);
+  else k_shard_pull<float><<<grid, 256, 0, st>>>(a);
+  c->launches += 2;
+  PSB_LAUNCH_CHECK(c, "shard pull");
+  return PSB_OK;
+}
+
+psb_status psb_shard_finish(psb_ctx* c, psb_dtype dt, size_t list_off, size_t list_voff, void* theta,
+                            size_t max_entries, cudaStream_t st) {
+  const PeerPtrs pp = peer_ptrs(c);
+  k_peer_publish_upd<<<1, 1, 0, st>>>(pp, c->nranks, c->rank);
+  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((max_entries + 1023) / 1024,
+                                                                         (size_t)c->num_sms * 4));
+  const int reps = c->marks_on && getenv("PSB_SCATTER_TWICE") ? 2 : 1;  // diagnostics: time a wait-free rerun
+  for (int rep = 0; rep < reps; ++rep) {
+    if (rep) psb_mark(c, st);
+    if (dt == PSB_F64)
+      k_shard_scatter<double><<<grid, 256, 0, st>>>(pp, c->nranks, c->rank, list_off, list_voff,
+                                                    reinterpret_cast<double*>(theta), c->d_flags);
+    else
+      k_shard_scatter<float><<<grid, 256, 0, st>>>(pp, c->nranks, c->rank, list_off, list_voff,
+                                                   reinterpret_cast<float*>(theta), c->d_flags);
+  }
+  c->launches += 2;
+  PSB_LAUNCH_CHECK(c, "shard scatter");
+  return PSB_OK;
+}
+
+extern "C" psb_status psb_peer_mode(psb_ctx* c, int mode) {
   PSB_REQUIRE(c, c != nullptr, "null ctx");
-  c->peer_mode = on ? 1 : 0;
+  PSB_REQUIRE(c, mode >= 0 && mode <= 2, "psb_peer_mode: mode must be 0, 1 or 2");
+  c->peer_mode = mode > 0;
+  c->shard_mode = mode == 2;
   return PSB_OK;
 }
 
 extern "C" int psb_peer_active(const psb_ctx* c) { return c && c->peer_arena ? 1 : 0; }
+
+// ------------------------------------------------------------ diagnostics
+namespace {
+__global__ void __launch_bounds__(256) k_copy16(int4* __restrict__ dst, const int4* __restrict__ src, size_t nv) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  constexpr int U = 4;
+  for (size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < nv; i0 += U * stride) {
+    int4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * stride < nv) v[u] = __ldcs(src + i0 + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * stride < nv) __stcs(dst + i0 + u * stride, v[u]);
+  }
+}
+}  // namespace
+
+// SM-driven 16-byte copy (either pointer may live on a peer GPU of the same
+// process after cudaDeviceEnablePeerAccess); for NVLink bandwidth probes.
+extern "C" PSB_API int psb_debug_copy16(void* dst, const void* src, size_t bytes, int ctas, void* stream) {
+  k_copy16<<<ctas, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<int4*>(dst), reinterpret_cast<const int4*>(src),
+                                                   bytes / 16);
+  return (int)cudaGetLastError();
+}
+extern "C" PSB_API int psb_debug_enable_peer(int dev, int peer) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(dev);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  cudaSetDevice(cur);
+  return e == cudaErrorPeerAccessAlreadyEnabled ? 0 : (int)e;
+}
+
+namespace {
+__global__ void __launch_bounds__(256) k_debug_scatter(float* __restrict__ theta, const uint32_t* __restrict__ idx,
+                                                       const float* __restrict__ val, size_t cnt) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  constexpr int U = 8;
+  for (size_t e0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < cnt; e0 += U * stride) {
+    uint32_t id[U];
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * stride < cnt) {
+        id[u] = __ldcs(idx + e0 + u * stride);
+        v[u] = __ldcs(val + e0 + u * stride);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * stride < cnt) theta[id[u]] = v[u];
+  }
+}
+}  // namespace
+
+// theta[idx[j]] = val[j] (the update-list scatter of the sharded apply, lists
+// anywhere in the peer-mapped address space); for bandwidth probes.
+extern "C" PSB_API int psb_debug_scatter(float* theta, const uint32_t* idx, const float* val, size_t cnt, int ctas,
+                                         void* stream) {
+  k_debug_scatter<<<ctas, 256, 0, (cudaStream_t)stream>>>(theta, idx, val, cnt);
+  return (int)cudaGetLastError();
+}

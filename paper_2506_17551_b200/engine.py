@@ -147,9 +147,11 @@ class Context:
         self._ck(self.lib.psb_allgather(self.h, buf.data_ptr(), bytes_per_rank, self.stream()),
                  "psb_allgather")
 
-    def peer_mode(self, on: bool) -> None:
-        """Payload exchange over NVLink peer memory (on, default) or NCCL all-gather."""
-        self._ck(self.lib.psb_peer_mode(self.h, int(bool(on))), "psb_peer_mode")
+    def peer_mode(self, mode) -> None:
+        """Multi-rank sparse exchange: 1 / "full" (default, NVLink, every rank
+        applies all payloads), 2 / "shard" (NVLink, sharded apply), 0 / "nccl"."""
+        m = {"shard": 2, "full": 1, "nccl": 0, True: 1, False: 0}.get(mode, mode)
+        self._ck(self.lib.psb_peer_mode(self.h, int(m)), "psb_peer_mode")
 
     @property
     def peer_active(self) -> bool:

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 
 
-def _worker(rank, nranks, uid, W, comp, order, steps, q, peer=True):
+def _worker(rank, nranks, uid, W, comp, order, steps, q, peer="full"):
     sys.path.insert(0, ROOT)
     try:
         import torch as th
@@ -60,7 +60,7 @@ def _worker(rank, nranks, uid, W, comp, order, steps, q, peer=True):
                 c.sync_step(d)
                 O.sync_step(g_all, theta_h, lr, comp, k, order, res_h, dpn, npr, 256)
             c.check()
-            if comp.startswith(("topk", "async")) and c.peer_active != peer:
+            if comp.startswith(("topk", "async")) and c.peer_active != (peer != "nccl"):
                 q.put((rank, f"peer_active={c.peer_active}, expected {peer}"))
                 return
             got = theta.cpu().numpy()
@@ -82,7 +82,7 @@ def _worker(rank, nranks, uid, W, comp, order, steps, q, peer=True):
         q.put((rank, f"error: {type(e).__name__}: {e}"))
 
 
-def _run(nranks, W, comp, order, steps=4, peer=True):
+def _run(nranks, W, comp, order, steps=4, peer="full"):
     from paper_2506_17551_b200.engine import Context
     uid = Context.unique_id()
     ctx = mp.get_context("spawn")
@@ -117,12 +117,14 @@ def test_exchange_paths_match_oracle(comp, order, W):
 
 @needs2
 @pytest.mark.parametrize("comp,order,W,peer,steps", [
-    ("topk", "ring", 1, False, 4), ("async", "naive", 2, False, 4), ("topk_q8", "naive", 1, False, 4),
-    ("topk_grow", "ring", 1, True, 6), ("topk", "ring", 1, True, 12),
+    ("topk", "ring", 1, "nccl", 4), ("async", "naive", 2, "nccl", 4), ("topk_q8", "naive", 1, "nccl", 4),
+    ("topk", "ring", 1, "shard", 4), ("async_q8", "naive", 2, "shard", 4), ("topk", "hierarchical", 2, "shard", 4),
+    ("async", "naive", 1, "shard", 4), ("topk_q8", "ring", 2, "shard", 4),
+    ("topk_grow", "ring", 1, "shard", 6), ("topk_grow", "naive", 2, "full", 6), ("topk", "ring", 1, "full", 12),
 ])
 def test_payload_exchange_modes(comp, order, W, peer, steps):
-    """NCCL all-gather fallback, arena re-creation when k grows, and a long
-    run through the device-side sequence flags."""
+    """NCCL all-gather fallback, the sharded NVLink apply, arena re-creation
+    when k grows, and a long run through the device-side sequence flags."""
     nr = min(torch.cuda.device_count(), 4)
     res = _run(nr, W, comp, order, steps=steps, peer=peer)
     assert all(v == "ok" for v in res.values()), res
