@@ -426,7 +426,7 @@ template <class T>
 psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* payloads, size_t k,
                        psb_order order, const psb_topology* topo, double lr,
                        const double* wscale_host, bool async_mode, T* theta, size_t n, T* mean_out,
-                       cudaStream_t st) {
+                       cudaStream_t st, const uint32_t* tab = nullptr) {
   PayloadView v = make_view(comp, sizeof(T) == 8 ? PSB_F64 : PSB_F32, payloads, k);
   uint32_t dpn, npr;
   topo_fields(topo, P, &dpn, &npr);
@@ -447,11 +447,13 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
   // reads them from L2 instead
   const int seg_shift = psb_apply_seg_shift(P);
   const uint32_t nseg = (uint32_t)((n + ((size_t)1 << seg_shift) - 1) >> seg_shift);
-  PSB_REQUIRE(c, (size_t)P * (nseg + 1) <= c->seg_cap, "sparse apply: segment table exceeds ctx capacity");
   PSB_REQUIRE(c, k <= 0xffffffffu, "sparse apply: k exceeds 32-bit positions");
-  {
+  if (!tab) {
+    PSB_REQUIRE(c, (size_t)P * (nseg + 1) <= c->seg_cap, "sparse apply: segment table exceeds ctx capacity");
     const unsigned gx = (unsigned)((k + 256 * kSegU - 1) / (256 * kSegU));
     k_seg_offsets<<<dim3(gx, (unsigned)P), 256, 0, st>>>(v, P, (uint32_t)k, nseg, seg_shift, c->d_seg_off);
+    c->launches += 1;
+    tab = c->d_seg_off;
   }
   const uint32_t vcap = c->apply_vcap;
   const size_t smem = (((size_t)P * 8) << (seg_shift - 5)) + (size_t)vcap * sizeof(T);
@@ -462,7 +464,7 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
   const unsigned grid = (unsigned)std::min<size_t>(nseg, 1u << 20);
   auto launch = [&](auto kern, T* mo) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, 256, smem, st>>>(v, P, nseg, 0u, nullptr, seg_shift, vcap, c->d_seg_off, (int)order, dpn, npr, coef, ws,
+    kern<<<grid, 256, smem, st>>>(v, P, nseg, 0u, nullptr, seg_shift, vcap, tab, (int)order, dpn, npr, coef, ws,
                                   theta, n, mo, nullptr, nullptr, nullptr, c->d_flags);
   };
   if (async_mode) {
@@ -480,7 +482,7 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
       default: launch(k_sparse_apply_bm<T, false, 0>, mean_out);
     }
   }
-  c->launches += 2;
+  c->launches += 1;
   PSB_LAUNCH_CHECK(c, "psb_sparse_mean_sgd");
   return PSB_OK;
 }
@@ -545,6 +547,17 @@ psb_status shard_fold_impl(psb_ctx* c, int P, const uint32_t* sidx, const T* sva
 }
 
 }  // namespace
+
+psb_status psb_sparse_apply_tab(psb_ctx* c, psb_compressor comp, psb_dtype dt, int P, const void* payloads, size_t k,
+                                const uint32_t* tab, psb_order order, const psb_topology* topo, double lr,
+                                const double* wscale, int async_mode, void* theta, size_t n, void* mean_out,
+                                cudaStream_t st) {
+  if (dt == PSB_F64)
+    return sparse_impl<double>(c, comp, P, payloads, k, order, topo, lr, wscale, async_mode != 0, (double*)theta, n,
+                               (double*)mean_out, st, tab);
+  return sparse_impl<float>(c, comp, P, payloads, k, order, topo, lr, wscale, async_mode != 0, (float*)theta, n,
+                            (float*)mean_out, st, tab);
+}
 
 psb_status psb_seg_offsets(psb_ctx* c, psb_compressor comp, psb_dtype dt, int nw, const void* payloads, size_t k,
                            uint32_t nseg, int seg_shift, uint32_t* rows, cudaStream_t st) {

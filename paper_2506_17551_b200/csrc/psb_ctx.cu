@@ -323,7 +323,8 @@ static psb_status check_desc(psb_ctx* c, const psb_step_desc* d) {
 //              pulls the matching slices, folds them into theta and an update
 //              list, and applies the other ranks' lists.
 struct ShardPlan {
-  bool on = false;
+  bool on = false;         // sharded apply
+  bool tab_ready = false;  // full exchange: every worker's offset rows are in the arena
   int seg_shift = 0;
   uint32_t nseg = 0;
   size_t blk = 0, tab_off = 0, list_off = 0, list_voff = 0, cap = 0;
@@ -344,14 +345,19 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
   if (peer) {
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
     size_t region = al(blk * P);
-    if (shard) {
+    if (plan && P >= 2) {
+      // per-segment offset rows of every worker's payload, computed by its
+      // producer and exchanged with it (the consumer skips k_seg_offsets)
       ShardPlan& sp = *plan;
-      sp.on = true;
       sp.blk = blk;
       sp.seg_shift = psb_apply_seg_shift(P);
       sp.nseg = (uint32_t)((d->n + ((size_t)1 << sp.seg_shift) - 1) >> sp.seg_shift);
       sp.tab_off = region;
       region += al(sizeof(uint32_t) * P * (sp.nseg + 1));
+    }
+    if (shard) {
+      ShardPlan& sp = *plan;
+      sp.on = true;
       sp.cap = std::min((size_t)P * d->k, d->n);
       sp.list_off = region;
       region += al(sizeof(uint32_t) * sp.cap);
@@ -391,18 +397,23 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
     if (s) return s;
   }
   psb_mark(c, st);
-  if (shard) {
+  const bool tabs = peer && plan && P >= 2;
+  if (tabs) {
     const ShardPlan& sp = *plan;
     uint32_t* tab = reinterpret_cast<uint32_t*>(gb + sp.tab_off) + (size_t)c->rank * W * (sp.nseg + 1);
     s = psb_seg_offsets(c, d->compressor, d->dtype, W, gb + (size_t)c->rank * W * blk, d->k, sp.nseg, sp.seg_shift,
                         tab, st);
     if (s) return s;
+  }
+  if (shard) {
     s = psb_peer_signal(c, st);
     if (s) return s;
     psb_mark(c, st);
   } else if (peer) {
-    s = psb_peer_exchange(c, (size_t)W * blk, st);
+    s = psb_peer_exchange(c, (size_t)W * blk, tabs ? plan->tab_off : 0,
+                          tabs ? (size_t)W * (plan->nseg + 1) : 0, st);
     if (s) return s;
+    if (tabs) plan->tab_ready = true;
     psb_mark(c, st);
   } else if (c->nranks > 1) {
     if (!c->comm) return psb_set_err(c, PSB_ESTATE, "sync step: communicator not initialised");
@@ -558,8 +569,13 @@ extern "C" psb_status psb_sync_step(psb_ctx* c, const psb_step_desc* d, psb_stre
       s = compress_and_gather(c, d, st, &pl, fuse, &sp);
       if (s || fuse) return s;
       if (sp.on) return shard_apply(c, d, sp, nullptr, false, st);
-      s = psb_sparse_mean_sgd(c, d->compressor, d->dtype, P, pl, d->k, d->order, &d->topo, d->lr,
-                              d->theta, d->n, d->mean_out, stream);
+      if (sp.tab_ready)
+        s = psb_sparse_apply_tab(c, d->compressor, d->dtype, P, pl, d->k,
+                                 reinterpret_cast<const uint32_t*>(pl + sp.tab_off), d->order, &d->topo, d->lr,
+                                 nullptr, 0, d->theta, d->n, d->mean_out, st);
+      else
+        s = psb_sparse_mean_sgd(c, d->compressor, d->dtype, P, pl, d->k, d->order, &d->topo, d->lr,
+                                d->theta, d->n, d->mean_out, stream);
       psb_mark(c, st);
       return s;
     }
@@ -634,6 +650,9 @@ extern "C" psb_status psb_async_round(psb_ctx* c, const psb_step_desc* d, uint32
     scale[p] = d->lr / (1.0 + (double)tau);  // strategies.hpp:127
   }
   if (sp.on) s = shard_apply(c, d, sp, scale.data(), true, st);
+  else if (sp.tab_ready)
+    s = psb_sparse_apply_tab(c, d->compressor, d->dtype, P, pl, d->k, reinterpret_cast<const uint32_t*>(pl + sp.tab_off),
+                             PSB_ORDER_NAIVE, nullptr, 0.0, scale.data(), 1, d->theta, d->n, nullptr, st);
   else s = psb_sparse_async_apply(c, d->compressor, d->dtype, P, pl, d->k, scale.data(), d->theta, d->n, stream);
   if (s) return s;
   *global_updates = g0 + (uint64_t)P;

@@ -114,7 +114,8 @@ void psb_mark(psb_ctx* c, cudaStream_t st);
 psb_status psb_peer_ensure(psb_ctx* c, size_t payload_bytes, cudaStream_t st);
 uint8_t* psb_peer_payload(psb_ctx* c);
 psb_status psb_peer_wait_ack(psb_ctx* c, cudaStream_t st);
-psb_status psb_peer_exchange(psb_ctx* c, size_t bytes_per_rank, cudaStream_t st);
+psb_status psb_peer_exchange(psb_ctx* c, size_t bytes_per_rank, size_t tab_off, size_t tab_words_per_rank,
+                             cudaStream_t st);
 void psb_peer_destroy(psb_ctx* c);
 uint32_t* psb_peer_list_cnt(psb_ctx* c);
 psb_status psb_peer_signal(psb_ctx* c, cudaStream_t st);
@@ -126,6 +127,12 @@ psb_status psb_shard_finish(psb_ctx* c, psb_dtype dt, size_t list_off, size_t li
 // sparse apply pieces (psb_apply.cu)
 psb_status psb_seg_offsets(psb_ctx* c, psb_compressor comp, psb_dtype dt, int nw, const void* payloads, size_t k,
                            uint32_t nseg, int seg_shift, uint32_t* rows, cudaStream_t st);
+// P-worker sparse apply with the per-segment offset rows already computed
+// (tab: [P][nseg+1] for segments of 2^psb_apply_seg_shift(P); nullptr: compute them)
+psb_status psb_sparse_apply_tab(psb_ctx* c, psb_compressor comp, psb_dtype dt, int P, const void* payloads, size_t k,
+                                const uint32_t* tab, psb_order order, const psb_topology* topo, double lr,
+                                const double* wscale, int async_mode, void* theta, size_t n, void* mean_out,
+                                cudaStream_t st);
 psb_status psb_shard_fold(psb_ctx* c, psb_dtype dt, int P, const uint32_t* sidx, const void* sval,
                           const uint32_t* srow, const uint32_t* range, int seg_shift, psb_order order,
                           const psb_topology* topo, double lr, const double* wscale, int async_mode, void* theta,

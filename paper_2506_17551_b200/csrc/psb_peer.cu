@@ -105,40 +105,54 @@ __global__ void k_peer_signal(PeerPtrs pp, int R, int rank) {
 }
 
 // Copies every peer's rank range [p*bpr, (p+1)*bpr) of the payload region
-// from its arena into ours, then acknowledges.  bpr is a multiple of 16.
-__global__ void __launch_bounds__(256) k_peer_pull(PeerPtrs pp, int R, int rank, size_t bpr, uint32_t* flags) {
+// from its arena into ours (bpr is a multiple of 16), plus, when tw > 0, its
+// tw words of per-segment offset rows at tab_off + p*tw*4; then acknowledges.
+// CTAs are dealt round-robin to the peers and each waits only for its own
+// peer, so a fast peer's payload moves while a slower one still compresses.
+__global__ void __launch_bounds__(256) k_peer_pull(PeerPtrs pp, int R, int rank, size_t bpr, size_t tab_off,
+                                                   size_t tw, uint32_t* flags) {
   uint32_t* hdr = reinterpret_cast<uint32_t*>(pp.base[rank]);
   const uint32_t s = hdr[kSeq];
+  const int npeer = R - 1;
+  const int pi = (int)(blockIdx.x % npeer);
+  const int p = pi + (pi >= rank);
+  const uint32_t cta = blockIdx.x / npeer;                                        // CTA index among p's
+  const uint32_t ncta = (gridDim.x - pi + npeer - 1) / npeer;                     // CTAs serving p
   __shared__ int ok;
-  if (threadIdx.x == 0) ok = wait_all(hdr, kReady, R, rank, s);
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = now_ns();
+    ok = 1;
+    while ((int32_t)(ld_acquire_sys(hdr + kReady + p) - s) < 0) {
+      if (now_ns() - t0 > kSpinNs) {
+        ok = 0;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
   __syncthreads();
   if (!ok) {
     if (threadIdx.x == 0) atomicOr(flags, 8u);
-    return;
-  }
-  const size_t v_per = bpr / 16;  // int4 per rank range
-  const size_t total = v_per * (size_t)(R - 1);
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
-  constexpr int U = 4;
-  for (size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < total; t0 += U * stride) {
-    int4 v[U];
-    int4* dst[U];
+  } else {
+    const size_t nv = bpr / 16;
+    const size_t stride = (size_t)ncta * blockDim.x;
+    const uint8_t* src = pp.base[p] + kHdrBytes + (size_t)p * bpr;
+    uint8_t* dst = pp.base[rank] + kHdrBytes + (size_t)p * bpr;
+    constexpr int U = 4;
+    for (size_t t0 = (size_t)cta * blockDim.x + threadIdx.x; t0 < nv; t0 += U * stride) {
+      int4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const size_t t = t0 + u * stride;
-      dst[u] = nullptr;
-      if (t < total) {
-        int pi = (int)(t / v_per);
-        const size_t j = t - (size_t)pi * v_per;
-        const int p = pi + (pi >= rank);  // skip our own range
-        const size_t off = kHdrBytes + (size_t)p * bpr + j * 16;
-        v[u] = __ldcs(reinterpret_cast<const int4*>(pp.base[p] + off));
-        dst[u] = reinterpret_cast<int4*>(pp.base[rank] + off);
-      }
+      for (int u = 0; u < U; ++u)
+        if (t0 + u * stride < nv) v[u] = __ldcs(reinterpret_cast<const int4*>(src) + t0 + u * stride);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (t0 + u * stride < nv) reinterpret_cast<int4*>(dst)[t0 + u * stride] = v[u];
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (dst[u]) *dst[u] = v[u];
+    if (tw) {
+      const uint32_t* ts = reinterpret_cast<const uint32_t*>(pp.base[p] + kHdrBytes + tab_off) + (size_t)p * tw;
+      uint32_t* td = reinterpret_cast<uint32_t*>(pp.base[rank] + kHdrBytes + tab_off) + (size_t)p * tw;
+      for (size_t t = (size_t)cta * blockDim.x + threadIdx.x; t < tw; t += stride) td[t] = ts[t];
+    }
   }
   // last CTA out acknowledges to every peer (no update list in this mode)
   last_cta_publish(pp, R, rank, kCtr, kAck, kAckU, s);
@@ -440,13 +454,16 @@ psb_status psb_peer_wait_ack(psb_ctx* c, cudaStream_t st) {
   return PSB_OK;
 }
 
-psb_status psb_peer_exchange(psb_ctx* c, size_t bytes_per_rank, cudaStream_t st) {
+psb_status psb_peer_exchange(psb_ctx* c, size_t bytes_per_rank, size_t tab_off, size_t tab_words_per_rank,
+                             cudaStream_t st) {
   if (bytes_per_rank % 16) return psb_set_err(c, PSB_EINVAL, "peer exchange: rank range not 16-byte aligned");
   const PeerPtrs pp = peer_ptrs(c);
   k_peer_signal<<<1, 1, 0, st>>>(pp, c->nranks, c->rank);
-  const size_t v = bytes_per_rank / 16 * (size_t)(c->nranks - 1);
-  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((v + 1023) / 1024, (size_t)c->num_sms * 4));
-  k_peer_pull<<<grid, 256, 0, st>>>(pp, c->nranks, c->rank, bytes_per_rank, c->d_flags);
+  const size_t npeer = (size_t)c->nranks - 1;
+  const size_t per = std::max<size_t>(1, std::min<size_t>((bytes_per_rank / 16 + 1023) / 1024,
+                                                          (size_t)c->num_sms * 4 / npeer));
+  k_peer_pull<<<(unsigned)(per * npeer), 256, 0, st>>>(pp, c->nranks, c->rank, bytes_per_rank, tab_off,
+                                                        tab_words_per_rank, c->d_flags);
   c->launches += 2;
   PSB_LAUNCH_CHECK(c, "peer exchange");
   return PSB_OK;
