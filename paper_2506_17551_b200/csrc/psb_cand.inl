@@ -116,34 +116,21 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   const uint32_t cnt = hi - lo;
   const bool staged = cnt <= a.stage_cap;
   if (staged && cnt) {
-    // copy the slice through registers: consecutive lanes load consecutive
-    // entries (one 128-byte request per warp instruction, unlike 4-byte
-    // cp.async which issues one request per entry), 8 entries per thread in
-    // flight; the slice may span several k_scan segments
-    constexpr int SU = 8;
-    for (uint32_t j0 = threadIdx.x; j0 < cnt; j0 += SU * blockDim.x) {
-      T v[SU];
-      uint32_t id[SU];
-#pragma unroll
-      for (int u = 0; u < SU; ++u) {
-        const uint32_t j = j0 + u * blockDim.x;
-        if (j < cnt) {
-          const uint32_t e = lo + j;
-          uint32_t sg = m.seg_of(e);
-          const size_t src = (size_t)sg * m.cap + (e - sh_pre[sg]);
-          v[u] = __ldcg(a.cand_val + src);
-          id[u] = __ldcg(a.cand_idx + src);
-        }
+    // copy the slice segment piece by segment piece with cp.async (LDGSTS):
+    // every thread keeps all of its copies in flight, no register round trip
+    uint32_t e = lo, sg = m.seg_of(lo);
+    while (e < hi) {
+      while (sh_pre[sg + 1] <= e) ++sg;
+      const uint32_t pe = min(hi, sh_pre[sg + 1]);
+      const size_t src = (size_t)sg * m.cap + (e - sh_pre[sg]);
+      for (uint32_t j = threadIdx.x; j < pe - e; j += blockDim.x) {
+        __pipeline_memcpy_async(st_val + (e - lo + j), a.cand_val + src + j, sizeof(T));
+        __pipeline_memcpy_async(st_idx + (e - lo + j), a.cand_idx + src + j, 4);
       }
-#pragma unroll
-      for (int u = 0; u < SU; ++u) {
-        const uint32_t j = j0 + u * blockDim.x;
-        if (j < cnt) {
-          st_val[j] = v[u];
-          st_idx[j] = id[u];
-        }
-      }
+      e = pe;
     }
+    __pipeline_commit();
+    __pipeline_wait_prior(0);
   }
   __syncthreads();
   phase();

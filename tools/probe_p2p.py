@@ -44,3 +44,33 @@ for mb in (8, 30, 100):
               f"{push[1]:.0f} GB/s | local {loc[0]:.1f} us {loc[1]:.0f} GB/s", flush=True)
     ce = t(lambda: y0.copy_(x1, non_blocking=True))
     print(f"{mb} MB copy engine peer->local: {ce[0]:.1f} us {ce[1]:.0f} GB/s", flush=True)
+
+# --- all-peer patterns (>= 3 GPUs): GPU0 pulls from / pushes to every peer at once
+if ng >= 3:
+    mb = 10
+    nb = mb * 1_000_000 // 16 * 16
+    src = {d: torch.empty(nb, dtype=torch.uint8, device=f"cuda:{d}") for d in range(ng)}
+    dst0 = [torch.empty(nb, dtype=torch.uint8, device="cuda:0") for _ in range(ng)]
+    torch.cuda.set_device(0)
+    streams = [torch.cuda.Stream(0) for _ in range(ng)]
+    s = torch.cuda.current_stream(0)
+
+    def multi(push):
+        ev = torch.cuda.Event()
+        ev.record(s)
+        for d in range(1, ng):
+            streams[d].wait_event(ev)
+            if push:
+                lib.psb_debug_copy16(src[d].data_ptr(), dst0[d].data_ptr(), nb, 148 * 4 // (ng - 1), streams[d].cuda_stream)
+            else:
+                lib.psb_debug_copy16(dst0[d].data_ptr(), src[d].data_ptr(), nb, 148 * 4 // (ng - 1), streams[d].cuda_stream)
+        for d in range(1, ng):
+            e = torch.cuda.Event()
+            e.record(streams[d])
+            s.wait_event(e)
+
+    for push in (False, True):
+        us, _ = t(lambda: multi(push))
+        tot = nb * (ng - 1)
+        print(f"{'push to' if push else 'pull from'} {ng - 1} peers x {mb} MB: {us:.1f} us, {tot / us / 1e3:.0f} GB/s "
+              f"aggregate", flush=True)
