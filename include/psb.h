@@ -131,16 +131,22 @@ PSB_API int psb_comm_size(const psb_ctx* ctx);
 /* In-place allgather: buf holds nranks blocks of bytes_per_rank; this rank's
  * block is at buf + rank*bytes_per_rank. */
 PSB_API psb_status psb_allgather(psb_ctx* ctx, void* buf, size_t bytes_per_rank, psb_stream_t stream);
-/* Sparse exchange + apply of psb_sync_step / psb_async_round with nranks > 1:
- *   1 (default) full: payloads exchanged over NVLink peer memory (CUDA IPC
- *     arenas, device-side sequence flags, set up collectively on first use):
- *     every rank pulls all P payloads, then applies them all;
+/* Sparse exchange + apply of psb_sync_step / psb_async_round with nranks > 1,
+ * over NVLink peer memory (CUDA IPC arenas, device-side sequence flags, set
+ * up collectively on first use) unless mode 0:
+ *   1 (default) pull: after K1 every rank copies the peers' payloads (and
+ *     their producer-computed per-segment offset rows) into its arena, each
+ *     CTA waiting only for its own peer, then applies all P payloads;
+ *   3 push: K1 stores each CTA's finished payload range straight into every
+ *     peer's arena (top-k f32/f64; top-k int8 falls back to 1), then every
+ *     rank applies all P payloads from its own arena;
  *   2 sharded: each rank pulls only the payload entries of its share of the
  *     index space (balanced on the device), folds them into theta and an
  *     update list, then applies the other ranks' lists;
  *   0 NCCL all-gather of the payloads, then the full apply.
- * Results are bitwise identical in every mode.  Environment at ctx creation:
- * PSB_NO_PEER=1 -> 0, PSB_SHARD=1 -> 2.  Steps with mean_out use mode 1. */
+ * Results are bitwise identical in every mode (1 is the fastest measured on
+ * B200: DESIGN.md section 4).  Environment at ctx creation: PSB_NO_PEER=1 -> 0,
+ * PSB_SHARD=1 -> 2.  Steps with mean_out never shard. */
 PSB_API psb_status psb_peer_mode(psb_ctx* ctx, int mode);
 /* 1 once the peer arenas are mapped. */
 PSB_API int psb_peer_active(const psb_ctx* ctx);

@@ -47,6 +47,11 @@ struct CandArgs {
   T* mean_out;  // with theta: dense mean at touched indices (nullable)
   T coef;       // (T)(-lr)
   uint32_t* flags;
+  // NVLink push (multi-rank full exchange): this worker's payload slot in
+  // every peer's arena; each CTA copies its contiguous payload range there
+  int npush;
+  uint32_t* push_idx[PSB_MAX_P];
+  T* push_val[PSB_MAX_P];
 };
 
 // Flat view of the segmented candidate list: logical entry e (index order)
@@ -362,6 +367,23 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
     run += tot;
   }
   phase();
+  if (a.npush) {
+    // this CTA's selected entries occupy payload slots [s_lo, s_hi) (index
+    // order); re-read them from L2 and store them to every peer over NVLink
+    // (coalesced 128-byte warp stores, posted: they drain during the scatter)
+    const unsigned long long b0 = sh_base;
+    const uint32_t s_lo = (uint32_t)((b0 & 0xffffffffull) + min(b0 >> 32, need_eq));
+    const uint32_t s_hi = (uint32_t)((run & 0xffffffffull) + min(run >> 32, need_eq));
+    __syncthreads();  // the CTA's payload writes are visible to the CTA
+    for (uint32_t j = s_lo + threadIdx.x; j < s_hi; j += blockDim.x) {
+      const uint32_t id = __ldcg(a.idx_out + j);
+      const T v = __ldcg(a.val_out + j);
+      for (int q = 0; q < a.npush; ++q) {
+        a.push_idx[q][j] = id;
+        a.push_val[q][j] = v;
+      }
+    }
+  }
   if (staged) {
     __syncthreads();
     // batches of U entries per thread: all theta loads of a batch are issued
@@ -406,6 +428,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
     }
   }
   if (bad) sh_bad = 1;
+  if (a.npush) __threadfence_system();  // the pushes are visible before the peers are signalled
   __syncthreads();
   if (threadIdx.x == 0 && sh_bad) atomicOr(a.flags, 1u);
   phase();

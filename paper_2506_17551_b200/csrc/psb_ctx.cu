@@ -325,6 +325,7 @@ static psb_status check_desc(psb_ctx* c, const psb_step_desc* d) {
 struct ShardPlan {
   bool on = false;         // sharded apply
   bool tab_ready = false;  // full exchange: every worker's offset rows are in the arena
+  bool ack_after_apply = false;  // push mode: acknowledge the peers' payloads once applied
   int seg_shift = 0;
   uint32_t nseg = 0;
   size_t blk = 0, tab_off = 0, list_off = 0, list_voff = 0, cap = 0;
@@ -340,6 +341,8 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
   // peer arena (psb_peer.cu); single rank / PSB_NO_PEER: the gather buffer
   const bool peer = c->nranks > 1 && c->peer_mode;
   const bool shard = peer && plan != nullptr && c->shard_mode && d->mean_out == nullptr && d->theta && P >= 2;
+  // full exchange pushed by K1 itself (top-k values; the q8 payload is finished after K1)
+  const bool push = peer && !shard && c->push_mode && d->compressor == PSB_COMP_TOPK && plan != nullptr;
   psb_status s;
   uint8_t* gb;
   if (peer) {
@@ -368,8 +371,10 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
     if (s) return s;
     gb = psb_peer_payload(c);
     psb_mark(c, st);
-    s = psb_peer_wait_ack(c, st);  // peers done with our previous payloads / update list
-    if (s) return s;
+    if (!push) {
+      s = psb_peer_wait_ack(c, st);  // peers done with our previous payloads / update list
+      if (s) return s;
+    }
     psb_mark(c, st);
   } else {
     s = ensure(c, &c->d_gather, &c->gather_bytes, blk * P, "payload gather buffer");
@@ -382,6 +387,10 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
     const void* g = reinterpret_cast<const uint8_t*>(d->g) + (size_t)w * d->n * es;
     void* r = d->r ? reinterpret_cast<uint8_t*>(d->r) + (size_t)w * d->n * es : nullptr;
     uint32_t* idx = reinterpret_cast<uint32_t*>(slot);
+    if (push) {
+      psb_peer_push_targets(c, (size_t)gid * blk);
+      c->push_wait = w == 0;  // K1 waits for the peers' acknowledgement before its first push
+    }
     if (d->compressor == PSB_COMP_TOPK) {
       if (fuse_apply)
         s = psb_topk_run_fused(c, d->dtype, w, g, r, d->n, d->k, idx, slot + psb_align16(d->k * 4),
@@ -394,6 +403,8 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
       s = psb_ef_topk_q8(c, w, (const float*)g, (float*)r, d->n, d->k, idx, codes, scales,
                          (psb_stream_t)st);
     }
+    c->push_n = 0;
+    c->push_wait = 0;
     if (s) return s;
   }
   psb_mark(c, st);
@@ -405,7 +416,20 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
                         tab, st);
     if (s) return s;
   }
-  if (shard) {
+  if (push) {
+    // payloads are already in every peer's arena; push the offset rows, signal, wait
+    const ShardPlan& sp = *plan;
+    s = psb_peer_put(c, sp.tab_off + sizeof(uint32_t) * (size_t)c->rank * W * (sp.nseg + 1),
+                     (size_t)W * (sp.nseg + 1), st);
+    if (s) return s;
+    s = psb_peer_signal(c, st);
+    if (s) return s;
+    s = psb_peer_wait_ready(c, st);
+    if (s) return s;
+    plan->tab_ready = true;
+    plan->ack_after_apply = true;
+    psb_mark(c, st);
+  } else if (shard) {
     s = psb_peer_signal(c, st);
     if (s) return s;
     psb_mark(c, st);
@@ -576,6 +600,7 @@ extern "C" psb_status psb_sync_step(psb_ctx* c, const psb_step_desc* d, psb_stre
       else
         s = psb_sparse_mean_sgd(c, d->compressor, d->dtype, P, pl, d->k, d->order, &d->topo, d->lr,
                                 d->theta, d->n, d->mean_out, stream);
+      if (!s && sp.ack_after_apply) s = psb_peer_ack(c, st);
       psb_mark(c, st);
       return s;
     }
@@ -650,9 +675,11 @@ extern "C" psb_status psb_async_round(psb_ctx* c, const psb_step_desc* d, uint32
     scale[p] = d->lr / (1.0 + (double)tau);  // strategies.hpp:127
   }
   if (sp.on) s = shard_apply(c, d, sp, scale.data(), true, st);
-  else if (sp.tab_ready)
+  else if (sp.tab_ready) {
     s = psb_sparse_apply_tab(c, d->compressor, d->dtype, P, pl, d->k, reinterpret_cast<const uint32_t*>(pl + sp.tab_off),
                              PSB_ORDER_NAIVE, nullptr, 0.0, scale.data(), 1, d->theta, d->n, nullptr, st);
+    if (!s && sp.ack_after_apply) s = psb_peer_ack(c, st);
+  }
   else s = psb_sparse_async_apply(c, d->compressor, d->dtype, P, pl, d->k, scale.data(), d->theta, d->n, stream);
   if (s) return s;
   *global_updates = g0 + (uint64_t)P;

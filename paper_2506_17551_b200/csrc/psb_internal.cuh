@@ -97,6 +97,13 @@ struct psb_ctx {
   size_t peer_bytes = 0;        // payload capacity of the arenas
   void* peer_base[PSB_MAX_P] = {};  // every rank's arena mapped here (own included)
   int shard_mode = 0;           // sharded multi-rank sparse apply (psb_peer_mode 2 / PSB_SHARD=1)
+  int push_mode = 0;            // full exchange: K1 pushes its payload to the peers (psb_peer_mode 3)
+  // set by the step driver around one worker's K1 call in push mode: the
+  // peers' payload-region bases and this worker's slot offset in them
+  int push_n = 0;
+  uint8_t* push_base[PSB_MAX_P] = {};
+  size_t push_slot_off = 0;
+  int push_wait = 0;            // K1 waits for the peers' acknowledgement before its write phase
   int no_stage = 0; // PSB_NO_STAGE=1: k_cand reads the list from global memory (diagnostics)
   int cand_smem[2] = {0, 0};  // dynamic shared memory of the cooperative k_cand (f32, f64)
   std::vector<cudaEvent_t> prof_ev;  // pairs (start, stop)
@@ -119,6 +126,10 @@ psb_status psb_peer_exchange(psb_ctx* c, size_t bytes_per_rank, size_t tab_off, 
 void psb_peer_destroy(psb_ctx* c);
 uint32_t* psb_peer_list_cnt(psb_ctx* c);
 psb_status psb_peer_signal(psb_ctx* c, cudaStream_t st);
+psb_status psb_peer_wait_ready(psb_ctx* c, cudaStream_t st);
+psb_status psb_peer_put(psb_ctx* c, size_t off, size_t words, cudaStream_t st);
+psb_status psb_peer_ack(psb_ctx* c, cudaStream_t st);
+void psb_peer_push_targets(psb_ctx* c, size_t slot_off);  // fills push_n / push_base / push_slot_off
 psb_status psb_shard_pull(psb_ctx* c, psb_dtype dt, int W, int q8, size_t blk, size_t voff, size_t soff,
                           size_t tab_off, uint32_t nseg, uint32_t* range, uint32_t* sidx, void* sval,
                           uint32_t* srow, size_t max_entries, cudaStream_t st);

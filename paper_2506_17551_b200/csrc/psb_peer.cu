@@ -471,6 +471,65 @@ psb_status psb_peer_exchange(psb_ctx* c, size_t bytes_per_rank, size_t tab_off, 
 
 void psb_peer_destroy(psb_ctx* c) { peer_release(c); }
 
+namespace {
+__global__ void k_peer_wait_ready(uint32_t* hdr, int R, int rank, uint32_t* flags) {
+  if (!wait_all(hdr, kReady, R, rank, hdr[kSeq])) atomicOr(flags, 8u);
+}
+// Done reading the peers' payloads (push mode: after the apply).
+__global__ void k_peer_ack(PeerPtrs pp, int R, int rank) {
+  const uint32_t s = reinterpret_cast<uint32_t*>(pp.base[rank])[kSeq];
+  __threadfence_system();
+  for (int p = 0; p < R; ++p) {
+    if (p == rank) continue;
+    uint32_t* ph = reinterpret_cast<uint32_t*>(pp.base[p]);
+    st_release_sys(ph + kAck + rank, s);
+    st_release_sys(ph + kAckU + rank, s);
+  }
+}
+}  // namespace
+
+namespace {
+// Stores [off, off + words) of our payload region into every peer's region.
+__global__ void k_peer_put(PeerPtrs pp, int R, int rank, size_t off, size_t words) {
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(pp.base[rank] + kHdrBytes + off);
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < words; t += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t v = src[t];
+    for (int p = 0; p < R; ++p)
+      if (p != rank) reinterpret_cast<uint32_t*>(pp.base[p] + kHdrBytes + off)[t] = v;
+  }
+  __threadfence_system();
+}
+}  // namespace
+
+psb_status psb_peer_put(psb_ctx* c, size_t off, size_t words, cudaStream_t st) {
+  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((words + 255) / 256, (size_t)c->num_sms));
+  k_peer_put<<<grid, 256, 0, st>>>(peer_ptrs(c), c->nranks, c->rank, off, words);
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "peer put");
+  return PSB_OK;
+}
+
+psb_status psb_peer_wait_ready(psb_ctx* c, cudaStream_t st) {
+  k_peer_wait_ready<<<1, 1, 0, st>>>(reinterpret_cast<uint32_t*>(c->peer_arena), c->nranks, c->rank, c->d_flags);
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "peer wait ready");
+  return PSB_OK;
+}
+
+psb_status psb_peer_ack(psb_ctx* c, cudaStream_t st) {
+  k_peer_ack<<<1, 1, 0, st>>>(peer_ptrs(c), c->nranks, c->rank);
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "peer ack");
+  return PSB_OK;
+}
+
+void psb_peer_push_targets(psb_ctx* c, size_t slot_off) {
+  c->push_n = 0;
+  for (int p = 0; p < c->nranks; ++p)
+    if (p != c->rank) c->push_base[c->push_n++] = reinterpret_cast<uint8_t*>(c->peer_base[p]) + kHdrBytes;
+  c->push_slot_off = slot_off;
+}
+
 uint32_t* psb_peer_list_cnt(psb_ctx* c) { return reinterpret_cast<uint32_t*>(c->peer_arena) + kListCnt; }
 
 psb_status psb_peer_signal(psb_ctx* c, cudaStream_t st) {
@@ -533,9 +592,10 @@ psb_status psb_shard_finish(psb_ctx* c, psb_dtype dt, size_t list_off, size_t li
 
 extern "C" psb_status psb_peer_mode(psb_ctx* c, int mode) {
   PSB_REQUIRE(c, c != nullptr, "null ctx");
-  PSB_REQUIRE(c, mode >= 0 && mode <= 2, "psb_peer_mode: mode must be 0, 1 or 2");
+  PSB_REQUIRE(c, mode >= 0 && mode <= 3, "psb_peer_mode: mode must be 0, 1, 2 or 3");
   c->peer_mode = mode > 0;
   c->shard_mode = mode == 2;
+  c->push_mode = mode == 3;
   return PSB_OK;
 }
 

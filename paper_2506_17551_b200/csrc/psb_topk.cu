@@ -538,6 +538,15 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   b.mean_out = mean_out;
   b.coef = (T)(-lr);
   b.flags = c->d_flags;
+  b.npush = c->push_n;
+  for (int q = 0; q < c->push_n; ++q) {
+    b.push_idx[q] = reinterpret_cast<uint32_t*>(c->push_base[q] + c->push_slot_off);
+    b.push_val[q] = reinterpret_cast<T*>(c->push_base[q] + c->push_slot_off + psb_align16(k * 4));
+  }
+  if (c->push_wait) {  // peers done reading this slot's previous payload
+    psb_status ws = psb_peer_wait_ack(c, st);
+    if (ws) return ws;
+  }
   // cooperative grid: one CTA per SM, the rest of shared memory stages the slice
   const int slot = sizeof(T) == 8;
   if (c->cand_smem[slot] == 0) {

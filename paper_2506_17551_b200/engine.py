@@ -148,9 +148,10 @@ class Context:
                  "psb_allgather")
 
     def peer_mode(self, mode) -> None:
-        """Multi-rank sparse exchange: 1 / "full" (default, NVLink, every rank
-        applies all payloads), 2 / "shard" (NVLink, sharded apply), 0 / "nccl"."""
-        m = {"shard": 2, "full": 1, "nccl": 0, True: 1, False: 0}.get(mode, mode)
+        """Multi-rank sparse exchange (psb_peer_mode): "pull" (1, default), "push"
+        (3: K1 stores its payload into the peers' NVLink arenas), "shard" (2),
+        "nccl" (0)."""
+        m = {"pull": 1, "full": 1, "push": 3, "shard": 2, "nccl": 0, True: 1, False: 0}.get(mode, mode)
         self._ck(self.lib.psb_peer_mode(self.h, int(m)), "psb_peer_mode")
 
     @property

@@ -120,11 +120,13 @@ def test_exchange_paths_match_oracle(comp, order, W):
     ("topk", "ring", 1, "nccl", 4), ("async", "naive", 2, "nccl", 4), ("topk_q8", "naive", 1, "nccl", 4),
     ("topk", "ring", 1, "shard", 4), ("async_q8", "naive", 2, "shard", 4), ("topk", "hierarchical", 2, "shard", 4),
     ("async", "naive", 1, "shard", 4), ("topk_q8", "ring", 2, "shard", 4),
-    ("topk_grow", "ring", 1, "shard", 6), ("topk_grow", "naive", 2, "full", 6), ("topk", "ring", 1, "full", 12),
+    ("topk_grow", "ring", 1, "shard", 6), ("topk_grow", "naive", 2, "pull", 6), ("topk", "ring", 1, "pull", 12),
+    ("topk", "ring", 1, "push", 4), ("async", "naive", 2, "push", 4), ("topk_grow", "ring", 2, "push", 6),
 ])
 def test_payload_exchange_modes(comp, order, W, peer, steps):
-    """NCCL all-gather fallback, the sharded NVLink apply, arena re-creation
-    when k grows, and a long run through the device-side sequence flags."""
+    """NCCL all-gather fallback, the NVLink push and sharded modes, arena
+    re-creation when k grows, and a long run through the device-side flags
+    (the default pull mode runs in test_exchange_paths_match_oracle)."""
     nr = min(torch.cuda.device_count(), 4)
     res = _run(nr, W, comp, order, steps=steps, peer=peer)
     assert all(v == "ok" for v in res.values()), res
