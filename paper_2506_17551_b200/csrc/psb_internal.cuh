@@ -90,6 +90,7 @@ struct psb_ctx {
   int prof = 0;
   int predict = 1;  // K1 threshold prediction (PSB_NO_PREDICT=1 disables)
   uint32_t apply_vcap = 4096;  // PSB_APPLY_VCAP: staged entries per apply segment
+  int q8_no_tma = 0;   // PSB_Q8_NO_TMA=1: register double-buffer kernel for the one-worker q8 step
   int q8_unfused = 0;  // PSB_Q8_UNFUSED=1: single-rank q8 step as quant + reduce (diagnostics)
   // NVLink peer exchange (psb_peer.cu)
   int peer_mode = 1;            // use it when nranks > 1 (PSB_NO_PEER=1 / psb_peer_mode(0): NCCL all-gather)

@@ -462,6 +462,177 @@ __global__ void __launch_bounds__(256) k_q8_step1(const float* __restrict__ g, s
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1u);
 }
 
+// ---- TMA-pipelined single-worker step (W = P = 1, the cfg3 bench shape) ----
+// The register double buffer of k_q8_step1 keeps ~64 B per lane in flight and
+// three CTAs per SM resident (72 registers), which leaves HBM at ~70 % of its
+// measured peak.  Here one elected thread streams tiles of 8 blocks (g, r and
+// theta: 3 x 8*B*4 bytes) into a ring of kQ8Stages shared-memory stages with
+// 1-D bulk copies (cp.async.bulk, mbarrier complete_tx), so the bytes in
+// flight no longer depend on registers; each warp then quantizes one block
+// of the stage exactly as k_q8_step1 does (same per-element operations, same
+// order) and stores r' and theta' straight to global memory.
+constexpr int kQ8Stages = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(256) k_q8_step1_tma(const float* __restrict__ g, float* __restrict__ r, size_t n,
+                                                      float coef, float* __restrict__ theta,
+                                                      float* __restrict__ mean_out, uint32_t* flags) {
+  constexpr int B = VPL * 128;
+  constexpr int TE = 8 * B;                    // elements per tile (one block per warp)
+  constexpr uint32_t kArr = TE * 4;            // bytes per array per stage
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* sg = reinterpret_cast<float*>(smem);                    // [stage][TE]
+  float* sr = sg + (size_t)kQ8Stages * TE;
+  float* sth = sr + (size_t)kQ8Stages * TE;
+  __shared__ __align__(8) uint64_t full[kQ8Stages];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t ntiles_full = n / TE;  // TMA streams full tiles; a ragged tail is read directly
+  const size_t my_tiles = ntiles_full > blockIdx.x ? (ntiles_full - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kQ8Stages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](size_t i) {  // local tile i -> stage i % kQ8Stages
+    const int s = (int)(i % kQ8Stages);
+    const size_t base = (blockIdx.x + i * gridDim.x) * (size_t)TE;
+    mbar_expect_tx(&full[s], 3 * kArr);
+    tma_load_1d(sg + (size_t)s * TE, g + base, kArr, &full[s]);
+    tma_load_1d(sr + (size_t)s * TE, r + base, kArr, &full[s]);
+    tma_load_1d(sth + (size_t)s * TE, theta + base, kArr, &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (size_t i = 0; i < my_tiles && i < (size_t)kQ8Stages; ++i) issue(i);
+  bool bad = false;
+  auto process = [&](const float* pg, const float* pr, const float* pth, size_t lo, bool from_smem) {
+    // one block of B elements at global offset lo; pg/pr/pth point at its first element
+    float p[VPL][4];
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+      const int o = it * 128 + lane * 4;
+      float4 gv, rv;
+      if (from_smem) {
+        gv = *reinterpret_cast<const float4*>(pg + o);
+        rv = *reinterpret_cast<const float4*>(pr + o);
+      } else {
+        gv = make_float4(0.f, 0.f, 0.f, 0.f);
+        rv = gv;
+        float* gp = &gv.x;
+        float* rp = &rv.x;
+        for (int c = 0; c < 4; ++c)
+          if (lo + o + c < n) {
+            gp[c] = pg[o + c];
+            rp[c] = pr[o + c];
+          }
+      }
+      p[it][0] = __fadd_rn(rv.x, gv.x);
+      p[it][1] = __fadd_rn(rv.y, gv.y);
+      p[it][2] = __fadd_rn(rv.z, gv.z);
+      p[it][3] = __fadd_rn(rv.w, gv.w);
+    }
+    float amax = 0.f;
+#pragma unroll
+    for (int it = 0; it < VPL; ++it)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        amax = fmaxf(amax, fabsf(p[it][c]));
+        bad |= !is_finite(p[it][c]);
+      }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const float scale = __fdiv_rn(amax, 127.0f);
+    const float inv = __frcp_rn(scale);
+    float m[VPL][4];
+    float mmax = 0.f;
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+      const size_t e = lo + (size_t)it * 128 + lane * 4;
+      float res[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float x = __fmul_rn((float)q8_code(p[it][c], scale, inv), scale);
+        res[c] = __fsub_rn(p[it][c], x);
+        m[it][c] = __fmul_rn(x, 1.0f);  // mean over P = 1: x * (1/1)
+        mmax = fmaxf(mmax, fabsf(m[it][c]));
+      }
+      if (from_smem) {
+        __stcs(reinterpret_cast<float4*>(r + e), make_float4(res[0], res[1], res[2], res[3]));
+      } else {
+        for (int c = 0; c < 4; ++c)
+          if (e + c < n) r[e + c] = res[c];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mmax = fmaxf(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
+    const float ms = __fdiv_rn(mmax, 127.0f);
+    const float minv = __frcp_rn(ms);
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+      const int o = it * 128 + lane * 4;
+      const size_t e = lo + o;
+      float mh[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) mh[c] = __fmul_rn((float)q8_code(m[it][c], ms, minv), ms);
+      if (from_smem) {
+        float4 th = *reinterpret_cast<const float4*>(pth + o);
+        th.x = __fadd_rn(__fmul_rn(coef, mh[0]), th.x);
+        th.y = __fadd_rn(__fmul_rn(coef, mh[1]), th.y);
+        th.z = __fadd_rn(__fmul_rn(coef, mh[2]), th.z);
+        th.w = __fadd_rn(__fmul_rn(coef, mh[3]), th.w);
+        __stcs(reinterpret_cast<float4*>(theta + e), th);
+        if (mean_out) *reinterpret_cast<float4*>(mean_out + e) = make_float4(mh[0], mh[1], mh[2], mh[3]);
+        bad |= !is_finite(th.x) || !is_finite(th.y) || !is_finite(th.z) || !is_finite(th.w);
+      } else {
+        for (int c = 0; c < 4; ++c) {
+          if (e + c >= n) continue;
+          const float t2 = __fadd_rn(__fmul_rn(coef, mh[c]), pth[o + c]);
+          theta[e + c] = t2;
+          if (mean_out) mean_out[e + c] = mh[c];
+          bad |= !is_finite(t2);
+        }
+      }
+    }
+  };
+  for (size_t i = 0; i < my_tiles; ++i) {
+    const int s = (int)(i % kQ8Stages);
+    mbar_wait(&full[s], (uint32_t)((i / kQ8Stages) & 1));
+    const size_t base = (blockIdx.x + i * gridDim.x) * (size_t)TE;
+    const size_t off = (size_t)s * TE + (size_t)wid * B;
+    process(sg + off, sr + off, sth + off, base + (size_t)wid * B, true);
+    __syncthreads();  // every warp is done with stage s
+    if (threadIdx.x == 0 && i + kQ8Stages < my_tiles) issue(i + kQ8Stages);
+  }
+  // ragged tail (blocks past the last full tile): CTA 0, one block per warp
+  if (blockIdx.x == 0) {
+    for (size_t lo = ntiles_full * TE + (size_t)wid * B; lo < n; lo += 8 * (size_t)B)
+      process(g + lo, r + lo, theta + lo, lo, false);
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1u);
+}
+
 __global__ void __launch_bounds__(256) k_q8_apply(const int8_t* __restrict__ mcodes,
                                                   const float* __restrict__ mscales, size_t n,
                                                   uint32_t B, float coef, float* __restrict__ theta,
@@ -554,6 +725,29 @@ psb_status psb_q8_step1_launch(psb_ctx* c, const float* g, size_t gstride, float
   const float coef = (float)(-lr);
   if (c->prof) cudaEventRecord(psb_prof_event(c), st);
   const bool hier = order == PSB_ORDER_HIER && dpn < (uint32_t)P;
+  const bool tma = P == 1 && r != nullptr && !c->q8_no_tma &&
+                   ((((uintptr_t)g) | ((uintptr_t)r) | ((uintptr_t)theta) | ((uintptr_t)mean_out)) & 15) == 0;
+  if (tma) {
+    const size_t smem = (size_t)kQ8Stages * 3 * 8 * B * sizeof(float);
+    const unsigned tgrid = (unsigned)std::max<size_t>(1, std::min<size_t>((n / (8 * B)) + 1, (size_t)c->num_sms * 2));
+#define PSB_T1(V)                                                                                         \
+  do {                                                                                                    \
+    cudaFuncSetAttribute(k_q8_step1_tma<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+    k_q8_step1_tma<V><<<tgrid, 256, smem, st>>>(g, r, n, coef, theta, mean_out, c->d_flags);              \
+  } while (0)
+    switch (B) {
+      case 128: PSB_T1(1); break;
+      case 256: PSB_T1(2); break;
+      case 512: PSB_T1(4); break;
+      case 1024: return psb_set_err(c, PSB_EINVAL, "q8: B=1024 tiles exceed shared memory");
+      default: return psb_set_err(c, PSB_EINVAL, "q8: block must be 128, 256, 512 or 1024");
+    }
+#undef PSB_T1
+    if (c->prof) cudaEventRecord(psb_prof_event(c), st);
+    c->launches += 1;
+    PSB_LAUNCH_CHECK(c, "q8 fused step (TMA)");
+    return PSB_OK;
+  }
 #define PSB_S1(V)                                                                                          \
   (hier ? k_q8_step1<V, true><<<grid, 256, 0, st>>>(g, gstride, r, rstride, P, n, (int)order, dpn, npr, coef, \
                                                      theta, mean_out, c->d_flags)                            \
