@@ -78,6 +78,7 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   if (const char* np = getenv("PSB_NO_PEER")) c->peer_mode = np[0] == '0';
   if (const char* sh = getenv("PSB_SHARD")) c->shard_mode = sh[0] != '0';
   if (const char* sm = getenv("PSB_STEP_MARKS")) c->marks_on = sm[0] != '0';
+  if (const char* sn = getenv("PSB_SCAN_TMA")) c->scan_tma = sn[0] != '0';
   if (const char* qt = getenv("PSB_Q8_NO_TMA")) c->q8_no_tma = qt[0] != '0';
   if (const char* qu = getenv("PSB_Q8_UNFUSED")) c->q8_unfused = qu[0] != '0';
   if (const char* vc = getenv("PSB_APPLY_VCAP")) c->apply_vcap = (uint32_t)std::min(16384l, std::max(0l, atol(vc))) & ~1u;

@@ -90,6 +90,7 @@ struct psb_ctx {
   int prof = 0;
   int predict = 1;  // K1 threshold prediction (PSB_NO_PREDICT=1 disables)
   uint32_t apply_vcap = 4096;  // PSB_APPLY_VCAP: staged entries per apply segment
+  int scan_tma = 0;  // PSB_SCAN_TMA=1: K1 streaming pass through a TMA stage ring (measured slower)
   int q8_no_tma = 0;   // PSB_Q8_NO_TMA=1: register double-buffer kernel for the one-worker q8 step
   int q8_unfused = 0;  // PSB_Q8_UNFUSED=1: single-rank q8 step as quant + reduce (diagnostics)
   // NVLink peer exchange (psb_peer.cu)
@@ -188,6 +189,30 @@ psb_status psb_cuda_err(psb_ctx* c, cudaError_t e, const char* where);
     if (r__ != ncclSuccess)                                                             \
       return psb_set_err((c), PSB_ENCCL, std::string(where) + ": " + ncclGetErrorString(r__)); \
   } while (0)
+
+// ---- 1-D TMA bulk copies into shared memory, completion on an mbarrier
+static __device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+static __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+static __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+static __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+static __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 
 static inline size_t psb_align16(size_t b) { return (b + 15) & ~(size_t)15; }
 

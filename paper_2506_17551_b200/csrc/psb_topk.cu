@@ -247,13 +247,26 @@ __global__ void k_topk_begin(TopkScratch* s, TopkWorker* w, uint32_t* hist1, uin
 }
 
 // ------------------------------------------------------------------ scan
-template <class T, int MODE>
+// TMA=true (opt-in, PSB_SCAN_TMA=1; MODE_A with EF, 16-byte aligned): one
+// elected thread streams the CTA's full tiles of g and r into a ring of
+// kScanStages shared-memory stages with 1-D bulk copies (mbarrier
+// complete_tx).  Measured slower than the register path at 125M (285 vs
+// 276 us): the ring halves the resident CTAs and this pass is bound by its
+// per-tile compaction, not by bytes in flight.  Everything else is identical.
+constexpr int kScanStages = 2;
+
+template <class T, int MODE, bool TMA = false>
 __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
   typedef KeyOf<T> KO;
   typedef typename KO::K K;
   constexpr int VW = VecOf<T>::W;
   constexpr int TILE = tile_elems<T>();
   constexpr int SH1 = KO::shift(0);
+  constexpr uint32_t kTileBytes = TILE * sizeof(T);
+  extern __shared__ __align__(128) unsigned char scan_smem[];
+  T* st_g = reinterpret_cast<T*>(scan_smem);   // [kScanStages][TILE]
+  T* st_r = st_g + (size_t)kScanStages * TILE;  // [kScanStages][TILE]
+  __shared__ __align__(8) uint64_t sh_full[TMA ? kScanStages : 1];
 
   __shared__ uint32_t sh_hist[PSB_HIST_BINS];
   __shared__ unsigned long long sh_warp[32];
@@ -294,13 +307,55 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
   const uint32_t t_lo = blockIdx.x * a.tpc;
   const uint32_t t_hi = min(a.ntiles, t_lo + a.tpc);
   const size_t seg_base = (size_t)t_lo * TILE;
+  // TMA ring: tiles [t_lo, t_full) are full and streamed through shared memory
+  const uint32_t t_full = TMA ? min(t_hi, (uint32_t)(a.n / TILE)) : t_lo;
+  auto issue = [&](uint32_t tile) {
+    const int sidx = (int)((tile - t_lo) % kScanStages);
+    const size_t base = (size_t)tile * TILE;
+    mbar_expect_tx(&sh_full[sidx], 2 * kTileBytes);
+    tma_load_1d(st_g + (size_t)sidx * TILE, src + base, kTileBytes, &sh_full[sidx]);
+    tma_load_1d(st_r + (size_t)sidx * TILE, rr + base, kTileBytes, &sh_full[sidx]);
+  };
+  if (TMA) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < kScanStages; ++i) mbar_init(&sh_full[i], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (uint32_t t = t_lo; t < t_full && t < t_lo + kScanStages; ++t) issue(t);
+  }
   uint32_t run = 0;  // candidates appended so far (uniform across the CTA)
   for (uint32_t tile = t_lo; tile < t_hi; ++tile) {
     const size_t base = (size_t)tile * TILE;
     const bool full = a.vec_ok && (base + TILE <= a.n);
     T x[4][VW];
     uint32_t valid = 0;
-    if (MODE == MODE_A && threadIdx.x == 0 && tile + 1 < t_hi && base + 2 * (size_t)TILE <= a.n && a.vec_ok) {
+    if (TMA && tile < t_full) {
+      // p = r + g from the staged tile; residual out (speculative +0) to global
+      const uint32_t li = tile - t_lo;
+      const int sidx = (int)(li % kScanStages);
+      mbar_wait(&sh_full[sidx], (li / kScanStages) & 1u);
+      const T* sg = st_g + (size_t)sidx * TILE;
+      const T* sr = st_r + (size_t)sidx * TILE;
+      valid = 0xffffu;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int o = (j * PSB_SCAN_THREADS + threadIdx.x) * VW;
+        T gv[VW], rv[VW], out[VW];
+        ld_vec(sg + o, gv);
+        ld_vec(sr + o, rv);
+#pragma unroll
+        for (int c = 0; c < VW; ++c) {
+          x[j][c] = add_rn(rv[c], gv[c]);
+          out[c] = (spec && KO::key(x[j][c]) >= gk) ? T(0) : x[j][c];
+        }
+        st_vec_stream(rr + base + o, out);
+      }
+      __syncthreads();  // every thread has read stage sidx: refill it
+      if (threadIdx.x == 0 && tile + kScanStages < t_full) issue(tile + kScanStages);
+    } else if (!TMA && MODE == MODE_A && threadIdx.x == 0 && tile + 1 < t_hi &&
+               base + 2 * (size_t)TILE <= a.n && a.vec_ok) {
       // TMA bulk prefetch of the next tile into L2: its loads then hit L2
       // while this tile's scan and stores run
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + base + TILE),
@@ -309,7 +364,9 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rr + base + TILE),
                      "r"((uint32_t)(TILE * sizeof(T))) : "memory");
     }
-    if (full) {
+    if (TMA && tile < t_full) {
+      // staged above
+    } else if (full) {
       valid = 0xffffu;
       if (MODE == MODE_A && rr != nullptr) {
         T gv[4][VW], rv[4][VW];
@@ -506,7 +563,17 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   a.s = s;
   a.w = w;
   a.hist1 = c->d_hist1;
-  const uint32_t scan_grid0 = (uint32_t)std::min<size_t>(ntiles, (size_t)c->num_sms * 4);
+  // TMA streaming (EF, aligned): as many CTAs per SM as the stage ring allows
+  const bool tma = r != nullptr && vec_ok && c->scan_tma && (size_t)ntiles >= (size_t)c->num_sms;
+  const size_t tma_smem = (size_t)2 * kScanStages * TILE * sizeof(T);
+  int per_sm = 4;
+  if (tma) {
+    cudaFuncSetAttribute(k_scan<T, MODE_A, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<T, MODE_A, true>, PSB_SCAN_THREADS, tma_smem);
+    per_sm = std::max(1, occ);
+  }
+  const uint32_t scan_grid0 = (uint32_t)std::min<size_t>(ntiles, (size_t)c->num_sms * per_sm);
   a.tpc = (ntiles + scan_grid0 - 1) / scan_grid0;
   const uint32_t scan_grid = (ntiles + a.tpc - 1) / a.tpc;
   a.seg_cnt = c->d_seg_cnt;
@@ -515,7 +582,8 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   a.cand_val = reinterpret_cast<T*>(c->d_stage_val);
   a.flags = c->d_flags;
   if (c->prof) cudaEventRecord(psb_prof_event(c), st);
-  k_scan<T, MODE_A><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
+  if (tma) k_scan<T, MODE_A, true><<<scan_grid, PSB_SCAN_THREADS, tma_smem, st>>>(a);
+  else k_scan<T, MODE_A><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
   if (c->prof) cudaEventRecord(psb_prof_event(c), st);
   k_restore<T><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
   k_scan<T, MODE_A2><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
