@@ -197,7 +197,9 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   };
 
   const bool pred = s->g_key != 0 && !s->need_full_hist;  // predicted candidate set valid
-  const bool spec = pred && s->spec_ok;                    // pass A zeroed all candidates
+  const bool spec = pred && s->spec_ok;  // pass A zeroed the residual of candidates with key >= zk
+  const K zk = (K)s->z_key;
+  auto zeroed = [&](T v) { return spec && KO::key(v) >= zk; };
   uint32_t level = s->start_level;
   K prefix = (K)s->prefix;
   unsigned long long need = s->need, match = s->match;
@@ -309,6 +311,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       w->rho = rho;
       w->t_prev = T_key;
       w->g_key = (T_key == 0 || T_key >= KO::kInf) ? 0ull : scale_key(T_key, f * rho, T(0));
+      w->z_key = (T_key == 0 || T_key >= KO::kInf) ? 0ull : scale_key(T_key, rho, T(0));
     }
   }
   __syncthreads();
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   bool bad = false;
   auto scatter = [&](uint32_t id, T v, bool sel) {
     if (sel) {
-      if (a.r && !spec) a.r[id] = T(0);  // cold mode: pass A stored p
+      if (a.r && !zeroed(v)) a.r[id] = T(0);  // pass A stored p
       if (a.theta) {
         const T mean = mul_rn(v, T(1));  // P = 1: mean = v * (1/1)
         const T t2 = add_rn(mul_rn(a.coef, mean), a.theta[id]);
@@ -327,7 +330,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
         if (a.mean_out) a.mean_out[id] = mean;
         bad |= !is_finite(t2);
       }
-    } else if (spec && a.r) {
+    } else if (a.r && zeroed(v)) {
       a.r[id] = v;  // unselected candidate: undo the speculative +0
     }
   };
@@ -413,7 +416,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       for (int u = 0; u < U; ++u) {
         if (!((actm >> u) & 1u)) continue;
         if ((selm >> u) & 1u) {
-          if (a.r && !spec) a.r[id[u]] = T(0);
+          if (a.r && !zeroed(v[u])) a.r[id[u]] = T(0);
           if (a.theta) {
             const T mean = mul_rn(v[u], T(1));  // P = 1: mean = v * (1/1)
             const T t2 = add_rn(mul_rn(a.coef, mean), th[u]);
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
             if (a.mean_out) a.mean_out[id[u]] = mean;
             bad |= !is_finite(t2);
           }
-        } else if (spec && a.r) {
+        } else if (a.r && zeroed(v[u])) {
           a.r[id[u]] = v[u];  // unselected candidate: undo the speculative +0
         }
       }

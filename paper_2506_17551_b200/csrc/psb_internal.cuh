@@ -35,6 +35,7 @@ struct TopkScratch {
   unsigned long long g_key;       // predicted key threshold used by this call (0 = none)
   uint32_t start_level;           // first radix level resolved over the candidates
   uint32_t spec_ok;               // predicted mode may pre-zero candidate residuals
+  unsigned long long z_key;       // pass A pre-zeroes the residual of keys >= z_key (>= g_key)
   unsigned long long phase_ns[16];  // k_cand phase timestamps (globaltimer, CTA 0)
 };
 
@@ -48,6 +49,7 @@ struct TopkWorker {
   uint32_t calls, misses;
   float last_ratio;          // candidates / k of the previous call
   uint32_t pad;
+  unsigned long long z_key;  // predicted T without the safety margin (pre-zero boundary)
 };
 
 struct psb_ctx {

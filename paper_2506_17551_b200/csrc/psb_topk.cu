@@ -240,6 +240,7 @@ __global__ void k_topk_begin(TopkScratch* s, TopkWorker* w, uint32_t* hist1, uin
     s->cand_count = 0;
     s->start_level = 1;
     s->g_key = predict ? w->g_key : 0ull;
+    s->z_key = w->z_key > w->g_key ? w->z_key : w->g_key;
     // pre-zeroing the candidates' residual pays off while most candidates are
     // selected (restores C - k < zero-writes k)
     s->spec_ok = w->last_ratio < 2.0f ? 1u : 0u;
@@ -290,8 +291,10 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
     compact = gk > 0;
     hist = !compact;
   }
-  // speculative +0 residual for candidates (predicted mode, EF pass only)
+  // speculative +0 residual for the candidates likely to be selected: keys
+  // >= z (the predicted T without margin; predicted mode, EF pass only)
   const bool spec = MODE == MODE_A && compact && a.s->spec_ok;
+  const K zk = (K)a.s->z_key;
 
   if (hist)
     for (int b = threadIdx.x; b < PSB_HIST_BINS; b += blockDim.x) sh_hist[b] = 0;
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
 #pragma unroll
         for (int c = 0; c < VW; ++c) {
           x[j][c] = add_rn(rv[c], gv[c]);
-          out[c] = (spec && KO::key(x[j][c]) >= gk) ? T(0) : x[j][c];
+          out[c] = (spec && KO::key(x[j][c]) >= zk) ? T(0) : x[j][c];
         }
         st_vec_stream(rr + base + o, out);
       }
@@ -382,7 +385,7 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
 #pragma unroll
           for (int c = 0; c < VW; ++c) {
             x[j][c] = add_rn(rv[j][c], gv[j][c]);
-            out[c] = (spec && KO::key(x[j][c]) >= gk) ? T(0) : x[j][c];
+            out[c] = (spec && KO::key(x[j][c]) >= zk) ? T(0) : x[j][c];
           }
           const size_t e = base + (size_t)(j * PSB_SCAN_THREADS + threadIdx.x) * VW;
           st_vec_stream(rr + e, out);
@@ -405,7 +408,7 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
             valid |= 1u << (j * VW + c);
             if (MODE == MODE_A && rr != nullptr) {
               v = add_rn(rr[e], src[e]);
-              rr[e] = (spec && KO::key(v) >= gk) ? T(0) : v;
+              rr[e] = (spec && KO::key(v) >= zk) ? T(0) : v;
             } else {
               v = src[e];
             }
