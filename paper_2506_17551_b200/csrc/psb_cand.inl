@@ -121,18 +121,17 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   const uint32_t cnt = hi - lo;
   const bool staged = cnt <= a.stage_cap;
   if (staged && cnt) {
-    // copy the slice segment piece by segment piece with cp.async (LDGSTS):
-    // every thread keeps all of its copies in flight, no register round trip
-    uint32_t e = lo, sg = m.seg_of(lo);
-    while (e < hi) {
+    // copy the slice with cp.async (LDGSTS), all copies in flight at once.
+    // Thread t takes entries t, t + blockDim, ... and walks the k_scan
+    // segments forward as it goes (one binary search per thread), so a slice
+    // spanning hundreds of sparse segments costs no per-segment round trip.
+    uint32_t sg = m.seg_of(min(lo + threadIdx.x, hi > 0 ? hi - 1 : 0));
+    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
+      const uint32_t e = lo + j;
       while (sh_pre[sg + 1] <= e) ++sg;
-      const uint32_t pe = min(hi, sh_pre[sg + 1]);
       const size_t src = (size_t)sg * m.cap + (e - sh_pre[sg]);
-      for (uint32_t j = threadIdx.x; j < pe - e; j += blockDim.x) {
-        __pipeline_memcpy_async(st_val + (e - lo + j), a.cand_val + src + j, sizeof(T));
-        __pipeline_memcpy_async(st_idx + (e - lo + j), a.cand_idx + src + j, 4);
-      }
-      e = pe;
+      __pipeline_memcpy_async(st_val + j, a.cand_val + src, sizeof(T));
+      __pipeline_memcpy_async(st_idx + j, a.cand_idx + src, 4);
     }
     __pipeline_commit();
     __pipeline_wait_prior(0);
