@@ -254,8 +254,22 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   const K T_key = prefix;
   const unsigned long long need_eq = need;
 
-  // ---- (gt, eq) counts per CTA; every CTA sums the totals of the CTAs before it
-  {
+  // ---- (gt, eq) counts per CTA; every CTA sums the totals of the CTAs before it.
+  // Staged slices: thread t owns the contiguous run [r0, r1) of the slice, so
+  // ONE block scan gives every thread its starting (gt, eq) for the write.
+  const uint32_t per = (cnt + kCandThreads - 1) / kCandThreads;
+  const uint32_t r0 = min(cnt, threadIdx.x * per), r1 = min(cnt, r0 + per);
+  unsigned long long my_ex = 0, cta_total = 0;
+  if (staged) {
+    uint32_t gt = 0, eq = 0;
+    for (uint32_t j = r0; j < r1; ++j) {
+      const K key = KO::key(st_val[j]);
+      gt += key > T_key;
+      eq += key == T_key;
+    }
+    my_ex = block_exscan_u64((unsigned long long)gt | ((unsigned long long)eq << 32), sh_warp, &cta_total);
+    if (threadIdx.x == 0) a.cta[blockIdx.x] = cta_total;
+  } else {
     uint32_t gt = 0, eq = 0;
     for (uint32_t base = 0; base < cnt; base += 4 * kCandThreads) {
       const uint32_t j0 = base + 4 * threadIdx.x;
@@ -282,9 +296,11 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
     block_exscan_u64(part, sh_warp, &total);
     if (threadIdx.x == 0) sh_base = total;
   }
+  // every CTA has read the level histograms: clear them for the next call
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < kNumLevelHists * kLevelHist;
+       b += gridDim.x * blockDim.x)
+    a.hlev[b] = 0;
   if (blockIdx.x == 0) {
-    // every CTA has read the level histograms: clear them for the next call
-    for (uint32_t b = threadIdx.x; b < kNumLevelHists * kLevelHist; b += blockDim.x) a.hlev[b] = 0;
     if (threadIdx.x == 0) {
       s->prefix = T_key;  // diagnostics (psb_topk_stats)
       s->need = need_eq;
@@ -333,7 +349,26 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       a.r[id] = v;  // unselected candidate: undo the speculative +0
     }
   };
-  for (uint32_t base = 0; base < cnt; base += 4 * kCandThreads) {
+  if (staged) {
+    // the thread's run, in index order: slot = gt_before + min(eq_before, need_eq)
+    unsigned long long before = run + my_ex;
+    for (uint32_t j = r0; j < r1; ++j) {
+      const T v = st_val[j];
+      const K key = KO::key(v);
+      const bool gt = key > T_key, eq = key == T_key;
+      const unsigned long long gt_b = before & 0xffffffffull, eq_b = before >> 32;
+      const bool sel = gt || (eq && eq_b < need_eq);
+      if (sel) {
+        const unsigned long long slot = gt_b + (eq_b < need_eq ? eq_b : need_eq);
+        a.idx_out[slot] = st_idx[j];
+        a.val_out[slot] = v;
+      }
+      st_slot[j] = sel ? 1u : kNoSlot;
+      before += (unsigned long long)gt | ((unsigned long long)eq << 32);
+    }
+    run += cta_total;
+  }
+  for (uint32_t base = 0; base < (staged ? 0u : cnt); base += 4 * kCandThreads) {
     const uint32_t j0 = base + 4 * threadIdx.x;
     T v[4];
     uint32_t id[4];
