@@ -35,7 +35,7 @@ struct CandArgs {
   uint32_t* hlev;  // kNumLevelHists x kLevelHist global histograms (zero between calls)
   const uint32_t* cand_idx;
   const T* cand_val;
-  const uint32_t* seg_pre;  // nseg + 1 exclusive prefixes of the k_scan CTA segments
+  const uint32_t* seg_cnt;  // candidates per k_scan CTA segment (nseg)
   uint32_t nseg;
   size_t seg_cap;           // segment stride (= elements streamed by one k_scan CTA)
   uint32_t stage_cap;       // entries of the shared-memory staging area
@@ -107,8 +107,24 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   phase();
 
   // ---- this CTA's slice [lo, hi) of the logical list (multiple of 4 entries)
-  for (uint32_t b = threadIdx.x; b <= a.nseg; b += blockDim.x) sh_pre[b] = a.seg_pre[b];
-  if (threadIdx.x == 0) sh_bad = 0;
+  // exclusive prefix of the k_scan segment counts, computed by every CTA
+  // (no serial last-block pass at the end of k_scan)
+  {
+    const uint32_t q = (a.nseg + blockDim.x - 1) / blockDim.x;
+    const uint32_t b0 = min(a.nseg, threadIdx.x * q), b1 = min(a.nseg, b0 + q);
+    unsigned long long loc = 0;
+    for (uint32_t b = b0; b < b1; ++b) loc += __ldcg(a.seg_cnt + b);
+    unsigned long long tot;
+    unsigned long long run0 = block_exscan_u64(loc, sh_warp, &tot);
+    for (uint32_t b = b0; b < b1; ++b) {
+      sh_pre[b] = (uint32_t)run0;
+      run0 += __ldcg(a.seg_cnt + b);
+    }
+    if (threadIdx.x == 0) {
+      sh_pre[a.nseg] = (uint32_t)tot;
+      sh_bad = 0;
+    }
+  }
   __syncthreads();
   FlatMap m;
   m.pre = sh_pre;

@@ -106,7 +106,6 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   ALLOC(c->d_histr, sizeof(uint32_t) * PSB_HIST_BINS * 10);  // k_cand level histograms
   ALLOC(c->d_histd, sizeof(uint32_t) * 16384);
   ALLOC(c->d_seg_cnt, sizeof(uint32_t) * PSB_FINAL_TPC_MAX);
-  ALLOC(c->d_seg_pre, sizeof(uint32_t) * (PSB_FINAL_TPC_MAX + 1));
   ALLOC(c->d_cta, sizeof(unsigned long long) * PSB_FINAL_TPC_MAX);
   ALLOC(c->d_stage_idx, sizeof(uint32_t) * stage_cap);
   c->stage_val_bytes = sizeof(double) * stage_cap;
@@ -127,7 +126,7 @@ extern "C" void psb_ctx_destroy(psb_ctx* c) {
   cudaDeviceSynchronize();
   psb_peer_destroy(c);
   void* ptrs[] = {c->d_flags,    c->d_tk,        c->d_tw,        c->d_hist1,   c->d_histr,
-                  c->d_seg_cnt,  c->d_seg_pre,   c->d_cta,       c->d_histd,       c->d_stage_idx, c->d_stage_val,
+                  c->d_seg_cnt,  c->d_cta,       c->d_histd,       c->d_stage_idx, c->d_stage_val,
                   c->d_seg_off,  c->d_partials,  c->d_gather,    c->d_work,    c->d_qmean};
   for (void* p : ptrs)
     if (p) cudaFree(p);

@@ -71,7 +71,6 @@ struct psb_ctx {
   uint32_t* d_histr = nullptr;   // refine-level histogram
   uint32_t* d_histd = nullptr;   // (key - G) histogram of the predicted mode
   uint32_t* d_seg_cnt = nullptr;          // candidates per k_scan CTA segment
-  uint32_t* d_seg_pre = nullptr;          // exclusive prefix of d_seg_cnt
   unsigned long long* d_cta = nullptr;    // per-CTA totals / prefixes
   uint32_t* d_stage_idx = nullptr;  // candidate staging, tile-segmented, capacity max_n
   void* d_stage_val = nullptr;      // f64 capacity

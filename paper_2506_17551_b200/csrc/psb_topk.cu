@@ -66,7 +66,7 @@ __host__ __device__ constexpr int tile_elems() {
 }
 
 enum { MODE_A = 0, MODE_A2 = 1, MODE_D = 2 };
-enum { DONE_A = 0, DONE_A2 = 1, DONE_D = 4 };
+enum { DONE_A = 0, DONE_A2 = 1 };
 
 
 // key <-> magnitude value, for the predicted threshold key(T * f)
@@ -96,7 +96,6 @@ struct ScanArgs {
   uint32_t* hist1;
   uint32_t tpc;       // tiles per CTA: CTA b streams tiles [b*tpc, (b+1)*tpc)
   uint32_t* seg_cnt;  // candidates written by CTA b (segment b of the list)
-  uint32_t* seg_pre;  // exclusive prefix of seg_cnt (nseg + 1 entries)
   uint32_t* cand_idx;
   T* cand_val;
   uint32_t* flags;
@@ -198,26 +197,6 @@ __device__ __forceinline__ bool last_block(uint32_t* counter) {
   __syncthreads();
   if (am_last) __threadfence();
   return am_last;
-}
-
-// Exclusive prefix of the per-CTA segment counts (run by one whole CTA);
-// pre[nseg] = total.  `sh` must hold >= nseg words.
-__device__ void seg_prefix(const uint32_t* cnt, uint32_t nseg, uint32_t* pre, uint32_t* sh,
-                           unsigned long long* sh_warp) {
-  __syncthreads();
-  for (uint32_t b = threadIdx.x; b < nseg; b += blockDim.x) sh[b] = __ldcg(cnt + b);
-  __syncthreads();
-  const uint32_t q = (nseg + blockDim.x - 1) / blockDim.x;
-  const uint32_t b0 = threadIdx.x * q, b1 = min(nseg, b0 + q);
-  unsigned long long local = 0;
-  for (uint32_t b = b0; b < b1; ++b) local += sh[b];
-  unsigned long long total;
-  unsigned long long run = block_exscan_u64(local, sh_warp, &total);
-  for (uint32_t b = b0; b < b1; ++b) {
-    pre[b] = (uint32_t)run;
-    run += sh[b];
-  }
-  if (threadIdx.x == 0) pre[nseg] = (uint32_t)total;
 }
 
 __global__ void k_topk_begin(TopkScratch* s, TopkWorker* w, uint32_t* hist1, uint32_t* histr,
@@ -478,10 +457,7 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
       if (h) atomicAdd(&a.hist1[b], h);
     }
   }
-  if (MODE == MODE_D) {
-    if (last_block(&a.s->done[DONE_D])) seg_prefix(a.seg_cnt, gridDim.x, a.seg_pre, sh_hist, sh_warp);
-    return;
-  }
+  if (MODE == MODE_D) return;  // k_cand prefix-sums the segment counts itself
 
   if (!last_block(&a.s->done[MODE == MODE_A ? DONE_A : DONE_A2])) return;
 
@@ -496,7 +472,6 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
         a.s->need = k;
         a.s->match = C;
       }
-      seg_prefix(a.seg_cnt, gridDim.x, a.seg_pre, sh_hist, sh_warp);
     } else if (threadIdx.x == 0) {
       a.s->need_full_hist = 1;  // miss: restore, rerun level 1 on all of p, then compact
       a.s->cand_count = 0;
@@ -580,7 +555,6 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   a.tpc = (ntiles + scan_grid0 - 1) / scan_grid0;
   const uint32_t scan_grid = (ntiles + a.tpc - 1) / a.tpc;
   a.seg_cnt = c->d_seg_cnt;
-  a.seg_pre = c->d_seg_pre;
   a.cand_idx = c->d_stage_idx;
   a.cand_val = reinterpret_cast<T*>(c->d_stage_val);
   a.flags = c->d_flags;
@@ -598,7 +572,7 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   b.hlev = c->d_histr;
   b.cand_idx = c->d_stage_idx;
   b.cand_val = reinterpret_cast<const T*>(c->d_stage_val);
-  b.seg_pre = c->d_seg_pre;
+  b.seg_cnt = c->d_seg_cnt;
   b.nseg = scan_grid;
   b.seg_cap = (size_t)a.tpc * TILE;
   b.cta = c->d_cta;
