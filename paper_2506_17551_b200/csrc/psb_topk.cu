@@ -236,7 +236,7 @@ __global__ void k_topk_begin(TopkScratch* s, TopkWorker* w, uint32_t* hist1, uin
 constexpr int kScanStages = 2;
 
 template <class T, int MODE, bool TMA = false>
-__global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
+__device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
   typedef KeyOf<T> KO;
   typedef typename KO::K K;
   constexpr int VW = VecOf<T>::W;
@@ -505,16 +505,43 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
   }
 }
 
+template <class T, int MODE, bool TMA = false>
+__global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
+  scan_body<T, MODE, TMA>(a);
+}
+
 // Prediction missed: pass A speculatively stored +0 for its candidates; put p
 // back (segment b holds exactly those written by k_scan CTA b) before the
 // cold path re-reads p from r.
 template <class T>
-__global__ void __launch_bounds__(PSB_SCAN_THREADS) k_restore(ScanArgs<T> a) {
+__device__ __forceinline__ void restore_body(const ScanArgs<T>& a) {
   constexpr int TILE = tile_elems<T>();
   if (!a.s->need_full_hist || !a.s->spec_ok || a.r == nullptr) return;
   const size_t base = (size_t)blockIdx.x * a.tpc * TILE;
   const uint32_t cnt = a.seg_cnt[blockIdx.x];
   for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) a.r[a.cand_idx[base + j]] = a.cand_val[base + j];
+}
+
+template <class T>
+__global__ void __launch_bounds__(PSB_SCAN_THREADS) k_restore(ScanArgs<T> a) {
+  restore_body(a);
+}
+
+// The miss / cold fallback (restore, full level-1 histogram, compaction) as
+// ONE cooperative launch on the k_scan grid (co-resident): in steady state it
+// is a single node that exits at once instead of three.
+template <class T>
+__global__ void __launch_bounds__(PSB_SCAN_THREADS) k_fallback(ScanArgs<T> a) {
+  cg::grid_group grid = cg::this_grid();
+  const bool miss = a.s->need_full_hist != 0;
+  if (!miss && !a.s->need_compact) return;  // uniform: flags from the previous kernel
+  if (miss) {
+    restore_body(a);
+    grid.sync();
+    scan_body<T, MODE_A2>(a);  // full histogram; its last CTA resolves b1 and sets need_compact
+    grid.sync();
+  }
+  scan_body<T, MODE_D>(a);
 }
 
 // ---------------------------------------------------- candidate phase
@@ -562,9 +589,22 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   if (tma) k_scan<T, MODE_A, true><<<scan_grid, PSB_SCAN_THREADS, tma_smem, st>>>(a);
   else k_scan<T, MODE_A><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
   if (c->prof) cudaEventRecord(psb_prof_event(c), st);
-  k_restore<T><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
-  k_scan<T, MODE_A2><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
-  k_scan<T, MODE_D><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
+  // fallback: one cooperative node when the k_scan grid is co-resident
+  int fb_occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fb_occ, k_fallback<T>, PSB_SCAN_THREADS, 0);
+  bool fused_fb = false;
+  if ((size_t)fb_occ * c->num_sms >= scan_grid) {
+    void* fargs[] = {&a};
+    fused_fb = cudaLaunchCooperativeKernel((const void*)k_fallback<T>, dim3(scan_grid), dim3(PSB_SCAN_THREADS),
+                                           fargs, 0, st) == cudaSuccess;
+  }
+  if (!fused_fb) {
+    (void)cudaGetLastError();
+    k_restore<T><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
+    k_scan<T, MODE_A2><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
+    k_scan<T, MODE_D><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
+    c->launches += 2;
+  }
 
   CandArgs<T> b;
   b.s = s;
@@ -611,7 +651,7 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_cand<T>, dim3(cgrid), dim3(kCandThreads),
                                               kargs, (size_t)dyn, st);
   if (e != cudaSuccess) return psb_cuda_err(c, e, "psb_ef_topk (cooperative launch)");
-  c->launches += 6;
+  c->launches += 4;
   PSB_LAUNCH_CHECK(c, "psb_ef_topk");
   return PSB_OK;
 }

@@ -2,6 +2,8 @@
 
 Bar: indices, values and residuals bit-exact (SURVEY.md 8c parity statement).
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -191,6 +193,7 @@ def test_full_size_properties_125m(cuda):
     c.close()
 
 
+@pytest.mark.skipif(os.environ.get("PSB_NO_PREDICT", "0") != "0", reason="prediction disabled by PSB_NO_PREDICT")
 def test_threshold_prediction_engages_and_stays_exact(cuda):
     """After the first (cold) call the worker predicts its threshold; the
     predicted candidate set must be valid in steady state and results exact."""
