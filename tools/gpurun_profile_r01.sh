@@ -12,14 +12,14 @@ python bench.py > $OUT/bench_cfg2.json 2> $OUT/bench_cfg2.err
 python bench.py --config cfg3 --no-cpu-baseline > $OUT/bench_cfg3.json 2>&1
 python bench.py --config cfg4 --no-cpu-baseline > $OUT/bench_cfg4.json 2>&1
 export PSB_BENCH_NO_CLOCKS=1
-# eager steps, 30 warm-up steps skipped (cfg2: ~6 launches/step, cfg3: 1, cfg4: ~8)
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 190 --launch-count 60 --csv \
+# eager steps, 30 warm-up steps skipped (cfg2: 4 launches/step, cfg3: 1, cfg4: 6)
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 125 --launch-count 40 --csv \
   --log-file $OUT/launches_cfg2.csv python bench.py --config cfg2 --steps 10 --warmup 30 --no-cpu-baseline --eager \
   > $OUT/ncu_launch_cfg2.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 33 --launch-count 10 --csv \
   --log-file $OUT/launches_cfg3.csv python bench.py --config cfg3 --steps 10 --warmup 30 --no-cpu-baseline --eager \
   > $OUT/ncu_launch_cfg3.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 250 --launch-count 80 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 185 --launch-count 60 --csv \
   --log-file $OUT/launches_cfg4.csv python bench.py --config cfg4 --steps 10 --warmup 30 --no-cpu-baseline --eager \
   > $OUT/ncu_launch_cfg4.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base mangled -k regex:k_scanIfLi0E --launch-skip 30 --launch-count 1 \
