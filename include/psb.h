@@ -151,6 +151,27 @@ PSB_API psb_status psb_peer_mode(psb_ctx* ctx, int mode);
 /* 1 once the peer arenas are mapped. */
 PSB_API int psb_peer_active(const psb_ctx* ctx);
 
+/* -------------------------------------------------------- wire format
+ * wire_encode / wire_decode (parsim/compression.hpp:159-239), little-endian:
+ *   DENSE   u64 dim | dim x f64
+ *   SIGNBIT u64 dim | f64 scale | ceil(dim/8) sign bytes (bit i%8 of byte i/8)
+ *   TOPK    u64 dim | u64 count | count x (u64 index, f64 value)
+ * Device buffers; values widen to f64 on encode, round to the payload dtype
+ * on decode.  Encode outputs 16-byte aligned (dense: 8). */
+typedef enum { PSB_WIRE_DENSE = 0, PSB_WIRE_SIGNBIT = 1, PSB_WIRE_TOPK = 2 } psb_wire_kind;
+PSB_API size_t psb_wire_bytes(psb_wire_kind kind, uint64_t dim, size_t k);
+PSB_API psb_status psb_wire_encode_topk(psb_ctx* ctx, psb_dtype dt, uint64_t dim, const uint32_t* idx,
+                                const void* val, size_t k, void* out, psb_stream_t stream);
+/* Synchronizes the stream; errors as the reference: "wire_decode: truncated
+ * input", plus capacity (count > k_cap) and the 32-bit index range. */
+PSB_API psb_status psb_wire_decode_topk(psb_ctx* ctx, psb_dtype dt, const void* in, size_t nbytes, size_t k_cap,
+                                uint32_t* idx, void* val, uint64_t* dim_out, size_t* count_out,
+                                psb_stream_t stream);
+PSB_API psb_status psb_wire_encode_signbit(psb_ctx* ctx, uint64_t dim, const uint32_t* words, const double* scale,
+                                   void* out, psb_stream_t stream);
+PSB_API psb_status psb_wire_encode_dense(psb_ctx* ctx, psb_dtype dt, const void* x, uint64_t dim, void* out,
+                                 psb_stream_t stream);
+
 /* ---------------------------------------------------------- generator
  * Counter-based synthetic gradients, identical bits to
  * oracle/psb_oracle.c:orc_generate.  Input generation only. */

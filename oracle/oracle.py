@@ -66,6 +66,10 @@ def orc() -> ctypes.CDLL:
             "orc_async_scale": (_D, [_D, _U64]),
             "orc_q8_quant": (_I, [_P, _P, _SZ, _U32, _P, _P]),
             "orc_q8_dequant": (None, [_P, _P, _SZ, _U32, _P]),
+            "orc_wire_encode_topk": (_SZ, [_U64, _P, _P, _SZ, _P]),
+            "orc_wire_decode_topk": (ctypes.c_longlong, [_P, _SZ, _P, _P, _P]),
+            "orc_wire_encode_signbit": (_SZ, [_U64, _D, _P, _P]),
+            "orc_wire_encode_dense": (_SZ, [_U64, _P, _P]),
         }
         for k, (res, args) in sig.items():
             f = getattr(lib, k)
@@ -97,6 +101,9 @@ def ref() -> ctypes.CDLL:
             "ref_async_step": (_I, [_P, _P, _SZ, _SZ, _D, _P]),
             "ref_vec_axpy": (_I, [_D, _P, _P, _SZ, _P]),
             "ref_decompress_topk": (_I, [_SZ, _P, _P, _SZ, _P]),
+            "ref_wire_encode_topk": (_SZ, [_U64, _P, _P, _SZ, _P]),
+            "ref_wire_decode_topk": (ctypes.c_longlong, [_P, _SZ, _P, _P, _P]),
+            "ref_wire_encode_onebit": (_SZ, [_P, _SZ, _P]),
         }
         for k, (res, args) in sig.items():
             f = getattr(lib, k)
@@ -292,6 +299,72 @@ def async_round(grads: np.ndarray, theta: np.ndarray, lr: float, k: int, residua
         axpy_(-float(orc().orc_async_scale(lr, tau)), g, theta)
         global_updates += 1
     return global_updates
+
+
+# ------------------------------------------------------------ wire format
+def wire_encode_topk(dim: int, idx: np.ndarray, val: np.ndarray) -> np.ndarray:
+    """parsim/compression.hpp:188-209 (TopK): u64 dim | u64 count | (u64 idx, f64 val) x count."""
+    idx = np.ascontiguousarray(idx, dtype=np.uint32)
+    val = np.ascontiguousarray(val, dtype=np.float64)
+    out = np.empty(16 + 16 * idx.size, dtype=np.uint8)
+    orc().orc_wire_encode_topk(dim, _p(idx), _p(val), idx.size, _p(out))
+    return out
+
+
+def wire_decode_topk(buf: np.ndarray):
+    """parsim/compression.hpp:213-239 (TopK); ValueError on truncated input."""
+    buf = np.ascontiguousarray(buf, dtype=np.uint8)
+    dim = np.zeros(1, dtype=np.uint64)
+    cnt = orc().orc_wire_decode_topk(_p(buf), buf.size, _p(dim), None, None)
+    if cnt < 0:
+        raise ValueError("wire_decode: truncated input")
+    idx = np.empty(cnt, dtype=np.uint64)
+    val = np.empty(cnt, dtype=np.float64)
+    orc().orc_wire_decode_topk(_p(buf), buf.size, _p(dim), _p(idx), _p(val))
+    return int(dim[0]), idx, val
+
+
+def wire_encode_signbit(dim: int, scale: float, words: np.ndarray) -> np.ndarray:
+    words = np.ascontiguousarray(words, dtype=np.uint32)
+    out = np.empty(16 + (dim + 7) // 8, dtype=np.uint8)
+    orc().orc_wire_encode_signbit(dim, scale, _p(words), _p(out))
+    return out
+
+
+def wire_encode_dense(x: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty(8 + 8 * x.size, dtype=np.uint8)
+    orc().orc_wire_encode_dense(x.size, _p(x), _p(out))
+    return out
+
+
+def ref_wire_encode_topk(dim: int, idx: np.ndarray, val: np.ndarray) -> np.ndarray:
+    idx = np.ascontiguousarray(idx, dtype=np.uint64)
+    val = np.ascontiguousarray(val, dtype=np.float64)
+    n = ref().ref_wire_encode_topk(dim, _p(idx), _p(val), idx.size, None)
+    out = np.empty(n, dtype=np.uint8)
+    ref().ref_wire_encode_topk(dim, _p(idx), _p(val), idx.size, _p(out))
+    return out
+
+
+def ref_wire_decode_topk(buf: np.ndarray):
+    buf = np.ascontiguousarray(buf, dtype=np.uint8)
+    dim = np.zeros(1, dtype=np.uint64)
+    cnt = ref().ref_wire_decode_topk(_p(buf), buf.size, _p(dim), None, None)
+    if cnt < 0:
+        raise ValueError(ref().ref_last_error().decode())
+    idx = np.empty(cnt, dtype=np.uint64)
+    val = np.empty(cnt, dtype=np.float64)
+    ref().ref_wire_decode_topk(_p(buf), buf.size, _p(dim), _p(idx), _p(val))
+    return int(dim[0]), idx, val
+
+
+def ref_wire_encode_onebit(g: np.ndarray) -> np.ndarray:
+    g = np.ascontiguousarray(g, dtype=np.float64)
+    n = ref().ref_wire_encode_onebit(_p(g), g.size, None)
+    out = np.empty(n, dtype=np.uint8)
+    ref().ref_wire_encode_onebit(_p(g), g.size, _p(out))
+    return out
 
 
 # ---------------------------------------------------------------- reference

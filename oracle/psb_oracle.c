@@ -391,3 +391,68 @@ int orc_q8_quant(const float* x, float* r, size_t n, uint32_t block, int8_t* cod
 void orc_q8_dequant(const int8_t* codes, const float* scales, size_t n, uint32_t block, float* out) {
   for (size_t i = 0; i < n; ++i) out[i] = (float)codes[i] * scales[i / block];
 }
+
+/* ------------------------------------------------------------ wire format
+ * parsim/compression.hpp:159-239, little-endian throughout:
+ *   Dense:   u64 dim | dim x f64
+ *   SignBit: u64 dim | f64 scale | ceil(dim/8) sign bytes (bit i%8 of byte i/8)
+ *   TopK:    u64 dim | u64 count | count x (u64 index, f64 value)
+ * Values are carried as f64 (the reference's DenseVector); f32 payloads widen
+ * exactly.  Decoders return -1 on truncation ("wire_decode: truncated ..."). */
+static void put_u64(uint8_t* o, uint64_t v) {
+  for (int b = 0; b < 8; ++b) o[b] = (uint8_t)(v >> (8 * b));
+}
+static uint64_t get_u64(const uint8_t* i) {
+  uint64_t v = 0;
+  for (int b = 0; b < 8; ++b) v |= (uint64_t)i[b] << (8 * b);
+  return v;
+}
+static void put_f64(uint8_t* o, double v) {
+  uint64_t u;
+  memcpy(&u, &v, 8);
+  put_u64(o, u);
+}
+static double get_f64(const uint8_t* i) {
+  uint64_t u = get_u64(i);
+  double v;
+  memcpy(&v, &u, 8);
+  return v;
+}
+
+size_t orc_wire_encode_topk(uint64_t dim, const uint32_t* idx, const double* val, size_t k, uint8_t* out) {
+  put_u64(out, dim);
+  put_u64(out + 8, (uint64_t)k);
+  for (size_t j = 0; j < k; ++j) {
+    put_u64(out + 16 + 16 * j, idx[j]);
+    put_f64(out + 24 + 16 * j, val[j]);
+  }
+  return 16 + 16 * k;
+}
+
+/* count of the message, or -1 if truncated; idx/val may be NULL to query */
+long long orc_wire_decode_topk(const uint8_t* in, size_t nbytes, uint64_t* dim, uint64_t* idx, double* val) {
+  if (nbytes < 16) return -1;
+  *dim = get_u64(in);
+  const uint64_t count = get_u64(in + 8);
+  if (count > (nbytes - 16) / 16) return -1;
+  if (idx && val)
+    for (uint64_t j = 0; j < count; ++j) {
+      idx[j] = get_u64(in + 16 + 16 * j);
+      val[j] = get_f64(in + 24 + 16 * j);
+    }
+  return (long long)count;
+}
+
+size_t orc_wire_encode_signbit(uint64_t dim, double scale, const uint32_t* words, uint8_t* out) {
+  put_u64(out, dim);
+  put_f64(out + 8, scale);
+  const size_t nb = (size_t)((dim + 7) / 8);
+  for (size_t b = 0; b < nb; ++b) out[16 + b] = (uint8_t)(words[b / 4] >> (8 * (b % 4)));
+  return 16 + nb;
+}
+
+size_t orc_wire_encode_dense(uint64_t dim, const double* x, uint8_t* out) {
+  put_u64(out, dim);
+  for (uint64_t i = 0; i < dim; ++i) put_f64(out + 8 + 8 * i, x[i]);
+  return 8 + 8 * (size_t)dim;
+}

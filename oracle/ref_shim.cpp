@@ -17,6 +17,7 @@
 //   async_step           parsim/strategies.hpp:125-129
 //   vec_axpy             parsim/numerics.hpp:70-78
 //   SeededRng            parsim/numerics.hpp:152-178
+//   wire_encode / wire_decode  parsim/compression.hpp:188-239
 
 #include <cstring>
 #include <exception>
@@ -278,3 +279,44 @@ int ref_decompress_topk(std::size_t dim, const std::uint64_t* idx, const double*
 }
 
 }  // extern "C"
+
+// wire_encode of a TopKPayload{dim, idx, val} (parsim/compression.hpp:188-209);
+// returns the byte count (out may be null to query it).
+extern "C" size_t ref_wire_encode_topk(uint64_t dim, const uint64_t* idx, const double* val, size_t k, uint8_t* out) {
+  TopKPayload t;
+  t.dim = dim;
+  t.indices.assign(idx, idx + k);
+  t.values.assign(val, val + k);
+  const std::vector<std::uint8_t> w = wire_encode(CompressedGradient{t});
+  if (out) std::memcpy(out, w.data(), w.size());
+  return w.size();
+}
+
+// wire_decode(topk) (parsim/compression.hpp:213-239): count, or -1 with the
+// reference's message in ref_last_error() on truncated input.
+extern "C" long long ref_wire_decode_topk(const uint8_t* in, size_t nbytes, uint64_t* dim, uint64_t* idx,
+                                          double* val) {
+  try {
+    const std::vector<std::uint8_t> w(in, in + nbytes);
+    const CompressedGradient c = wire_decode(WireKind::topk, w);
+    const auto& t = std::get<TopKPayload>(c.payload);
+    *dim = t.dim;
+    if (idx && val)
+      for (std::size_t j = 0; j < t.indices.size(); ++j) {
+        idx[j] = t.indices[j];
+        val[j] = t.values[j];
+      }
+    return (long long)t.indices.size();
+  } catch (const std::exception& e) {
+    fail_with(e);
+    return -1;
+  }
+}
+
+// wire_encode of a SignBitPayload built by compress_onebit(g) (compression.hpp:67-77).
+extern "C" size_t ref_wire_encode_onebit(const double* g, size_t n, uint8_t* out) {
+  const DenseVector x(g, g + n);
+  const std::vector<std::uint8_t> w = wire_encode(compress_onebit(x));
+  if (out) std::memcpy(out, w.data(), w.size());
+  return w.size();
+}

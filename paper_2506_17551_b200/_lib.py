@@ -63,6 +63,8 @@ class StepDesc(ctypes.Structure):
     ]
 
 
+PSB_WIRE_DENSE, PSB_WIRE_SIGNBIT, PSB_WIRE_TOPK = 0, 1, 2
+
 _vp = ctypes.c_void_p
 _sz = ctypes.c_size_t
 _i = ctypes.c_int
@@ -97,6 +99,12 @@ _SIGS = {
     "psb_q8_quantize": (_i, [_vp, _vp, _vp, _sz, _u32, _vp, _vp, _vp]),
     "psb_q8_dequantize": (_i, [_vp, _vp, _vp, _sz, _u32, _vp, _vp]),
     "psb_decompress_topk": (_i, [_vp, _i, _vp, _vp, _sz, _sz, _vp, _vp]),
+    "psb_wire_bytes": (_sz, [_i, _u64, _sz]),
+    "psb_wire_encode_topk": (_i, [_vp, _i, _u64, _vp, _vp, _sz, _vp, _vp]),
+    "psb_wire_decode_topk": (_i, [_vp, _i, _vp, _sz, _sz, _vp, _vp, ctypes.POINTER(_u64), ctypes.POINTER(_sz),
+                                  _vp]),
+    "psb_wire_encode_signbit": (_i, [_vp, _u64, _vp, _vp, _vp, _vp]),
+    "psb_wire_encode_dense": (_i, [_vp, _i, _vp, _u64, _vp, _vp]),
     "psb_sparse_mean_sgd": (_i, [_vp, _i, _i, _i, _vp, _sz, _i, ctypes.POINTER(Topology), _d, _vp,
                                  _sz, _vp, _vp]),
     "psb_sparse_async_apply": (_i, [_vp, _i, _i, _i, _vp, _sz, ctypes.POINTER(_d), _vp, _sz, _vp]),

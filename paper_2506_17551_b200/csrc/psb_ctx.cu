@@ -204,6 +204,9 @@ extern "C" psb_status psb_check(psb_ctx* c, psb_stream_t stream) {
   if (flags) {
     CUDA_TRY(c, cudaMemset(c->d_flags, 0, sizeof(uint32_t)), "psb_check");
     if (flags & 8u) return psb_set_err(c, PSB_ESTATE, "peer exchange: timed out waiting for a peer rank");
+    if (flags & 16u) return psb_set_err(c, PSB_EINVAL, "wire_decode: truncated input");
+    if (flags & 32u) return psb_set_err(c, PSB_EINVAL, "wire_decode: message exceeds the output capacity");
+    if (flags & 64u) return psb_set_err(c, PSB_EINVAL, "wire_decode: index exceeds the 32-bit range");
     if (flags & 2u) return psb_set_err(c, PSB_EINVAL, "decompress: index out of range for dim");
     if (flags & 4u) return psb_set_err(c, PSB_EINVAL, "decompress: indices not strictly increasing");
     return psb_set_err(c, PSB_ENONFINITE, "ef_compress_step residual: non-finite entry");

@@ -220,6 +220,41 @@ class Context:
                  "decompress")
         return out
 
+    # ---------------------------------------------------------- wire format
+    def wire_encode_topk(self, dim: int, idx: torch.Tensor, val: torch.Tensor) -> torch.Tensor:
+        """parsim wire_encode(TopKPayload): u64 dim | u64 count | (u64 idx, f64 val) x count."""
+        k = idx.numel()
+        out = torch.empty(int(self.lib.psb_wire_bytes(L.PSB_WIRE_TOPK, dim, k)), dtype=torch.uint8,
+                          device=val.device)
+        self._ck(self.lib.psb_wire_encode_topk(self.h, _dtype_code(val), dim, _ptr(idx), _ptr(val), k,
+                                               out.data_ptr(), self.stream()), "wire_encode")
+        return out
+
+    def wire_decode_topk(self, buf: torch.Tensor, dtype: torch.dtype = torch.float32, k_cap: Optional[int] = None):
+        """parsim wire_decode(topk) -> (dim, idx u32, val); ValueError on truncated input."""
+        cap = k_cap if k_cap is not None else max(0, (buf.numel() - 16) // 16)
+        idx = torch.empty(max(cap, 1), dtype=torch.int32, device=buf.device)
+        val = torch.empty(max(cap, 1), dtype=dtype, device=buf.device)
+        dim, cnt = L._u64(0), L._sz(0)
+        self._ck(self.lib.psb_wire_decode_topk(self.h, _DT[dtype], buf.data_ptr(), buf.numel(), cap,
+                                               idx.data_ptr(), val.data_ptr(), ctypes.byref(dim),
+                                               ctypes.byref(cnt), self.stream()), "wire_decode")
+        return int(dim.value), idx[:cnt.value], val[:cnt.value]
+
+    def wire_encode_signbit(self, dim: int, words: torch.Tensor, scale: torch.Tensor) -> torch.Tensor:
+        out = torch.empty(int(self.lib.psb_wire_bytes(L.PSB_WIRE_SIGNBIT, dim, 0)), dtype=torch.uint8,
+                          device=words.device)
+        self._ck(self.lib.psb_wire_encode_signbit(self.h, dim, words.data_ptr(), scale.data_ptr(), out.data_ptr(),
+                                                  self.stream()), "wire_encode")
+        return out
+
+    def wire_encode_dense(self, x: torch.Tensor) -> torch.Tensor:
+        out = torch.empty(int(self.lib.psb_wire_bytes(L.PSB_WIRE_DENSE, x.numel(), 0)), dtype=torch.uint8,
+                          device=x.device)
+        self._ck(self.lib.psb_wire_encode_dense(self.h, _dtype_code(x), x.data_ptr(), x.numel(), out.data_ptr(),
+                                                self.stream()), "wire_encode")
+        return out
+
     # ------------------------------------------------------ aggregate+apply
     def sparse_mean_sgd(self, payloads: torch.Tensor, P: int, k: int, dtype: torch.dtype,
                         order: str, lr: float, theta: Optional[torch.Tensor], n: int,

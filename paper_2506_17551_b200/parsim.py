@@ -19,6 +19,8 @@ analogue of std::invalid_argument.
   async_step               parsim/strategies.hpp:125-129
   vec_axpy                 parsim/numerics.hpp:70-78
   StalenessTracker         parsim/strategies.hpp:65-77
+  wire_encode/wire_decode  parsim/compression.hpp:159-239 (device codec, psb_wire.cu)
+  compression_ratio(_for)  parsim/compression.hpp:243-271
 """
 from __future__ import annotations
 
@@ -372,3 +374,83 @@ def async_step(params: Vector, g_p: Vector, tau: int, eta: float) -> torch.Tenso
     """params - eta/(1+tau) * g (scale computed in f64, strategies.hpp:127)."""
     scale = eta / (1.0 + float(tau))
     return vec_axpy(-scale, g_p, params)
+
+
+# ------------------------------------------------------------ wire format
+class WireKind(enum.Enum):
+    """parsim/compression.hpp:211: the caller states which payload kind the bytes carry."""
+    dense = 0
+    signbit = 1
+    topk = 2
+
+
+def wire_encode(c: CompressedGradient) -> torch.Tensor:
+    """parsim/compression.hpp:188-209: little-endian bytes (uint8 CUDA tensor), encoded on the device."""
+    p = c.payload
+    if isinstance(p, DensePayload):
+        x = as_vector(p.values)
+        return _ctx(x.numel()).wire_encode_dense(x)
+    if isinstance(p, SignBitPayload):
+        nw = (p.dim + 31) // 32
+        words = torch.zeros(nw, dtype=torch.int32, device="cuda")
+        words.view(torch.uint8)[:p.sign_bytes.numel()] = p.sign_bytes.to(device="cuda", dtype=torch.uint8)
+        scale = torch.tensor([p.scale], dtype=torch.float64, device="cuda")
+        return _ctx(p.dim).wire_encode_signbit(p.dim, words, scale)
+    idx = p.indices.to(device="cuda", dtype=torch.int64)
+    if idx.numel() and int(idx.max()) >= 1 << 32:
+        raise L.PsbInvalidArgument("wire_encode: index exceeds the 32-bit range")
+    vals = as_vector(p.values)
+    c0 = _ctx(max(p.dim, 1), max(idx.numel(), 1))
+    return c0.wire_encode_topk(p.dim, idx.to(torch.int32), vals)
+
+
+def wire_decode(kind: WireKind, data: Union[torch.Tensor, bytes]) -> CompressedGradient:
+    """parsim/compression.hpp:213-239; 'wire_decode: truncated input' on short data."""
+    buf = data if isinstance(data, torch.Tensor) else torch.frombuffer(bytearray(data), dtype=torch.uint8)
+    buf = buf.to(device="cuda", dtype=torch.uint8).contiguous()
+    if kind == WireKind.topk:
+        c0 = _ctx(1, max((buf.numel() - 16) // 16, 1))
+        dim, idx, val = c0.wire_decode_topk(buf, torch.float64)
+        return CompressedGradient(TopKPayload(dim, idx.to(torch.int64) & 0xFFFFFFFF, val))
+    host = buf.cpu()
+    if host.numel() < 8:
+        raise L.PsbInvalidArgument("wire_decode: truncated input")
+    dim = int(host[:8].view(torch.int64).item())
+    if kind == WireKind.dense:
+        if host.numel() < 8 + 8 * dim:
+            raise L.PsbInvalidArgument("wire_decode: truncated input")
+        return CompressedGradient(DensePayload(buf[8:8 + 8 * dim].view(torch.float64).clone()))
+    if host.numel() < 16:
+        raise L.PsbInvalidArgument("wire_decode: truncated input")
+    scale = float(host[8:16].view(torch.float64).item())
+    nb = (dim + 7) // 8
+    if host.numel() < 16 + nb:
+        raise L.PsbInvalidArgument("wire_decode: truncated sign bytes")
+    return CompressedGradient(SignBitPayload(dim, scale, buf[16:16 + nb].clone()))
+
+
+def compression_ratio(c: CompressedGradient) -> float:
+    """parsim/compression.hpp:243-253: raw 8-byte entries over wire bytes."""
+    p = c.payload
+    dense = 8.0 * c.dim()
+    if isinstance(p, DensePayload):
+        return 1.0
+    if isinstance(p, SignBitPayload):
+        return dense / (8.0 + 8.0 + float((p.dim + 7) // 8))
+    return dense / (8.0 + 8.0 + 16.0 * float(p.indices.numel()))
+
+
+def compression_ratio_for(cfg: CompressorConfig, dim: int) -> float:
+    """parsim/compression.hpp:256-271."""
+    if dim < 1:
+        raise L.PsbInvalidArgument("compression_ratio_for: dim must be >= 1")
+    if cfg.kind == CompressorKind.none:
+        return 1.0
+    if cfg.kind == CompressorKind.onebit:
+        return 8.0 * dim / (16.0 + float((dim + 7) // 8))
+    if cfg.kind == CompressorKind.topk:
+        k = min(cfg.top_k, dim)
+        if k < 1:
+            raise L.PsbInvalidArgument("compression_ratio_for: top_k must be >= 1")
+        return 8.0 * dim / (16.0 + 16.0 * k)
+    raise L.PsbInvalidArgument("compression_ratio_for: unknown compressor kind")

@@ -192,3 +192,36 @@ def test_q8_spec_properties():
     sc = np.repeat(scales, 256)[: p.size]
     assert np.all(np.abs(p - xhat) <= sc * 0.5000001 + 1e-30)
     assert np.allclose(r2 + xhat, p, rtol=0, atol=np.spacing(np.abs(p)).max())
+
+
+# ------------------------------------------------------------ wire format
+@pytest.mark.skipif(not O.ref_available(), reason="reference headers not built (oracle/_ref)")
+def test_wire_codec_matches_reference():
+    """parsim wire_encode / wire_decode (compression.hpp:159-239): the C
+    restatement is byte-identical to the reference on random top-k payloads,
+    decodes the reference's bytes, and fails on truncation with its message."""
+    rng = np.random.default_rng(7)
+    for dim, k in [(1, 1), (40, 7), (1000, 50), (1 << 20, 4096)]:
+        idx = np.sort(rng.choice(dim, k, replace=False)).astype(np.uint32)
+        val = rng.standard_normal(k)
+        ours = O.wire_encode_topk(dim, idx, val)
+        theirs = O.ref_wire_encode_topk(dim, idx.astype(np.uint64), val)
+        assert np.array_equal(ours, theirs)
+        d, i2, v2 = O.wire_decode_topk(theirs)
+        assert d == dim and np.array_equal(i2, idx.astype(np.uint64)) and np.array_equal(v2.view(np.uint64),
+                                                                                         val.view(np.uint64))
+        for cut in (1, 8, 15):
+            with pytest.raises(ValueError, match="wire_decode: truncated input"):
+                O.ref_wire_decode_topk(theirs[:-cut] if cut < theirs.size else theirs[:0])
+            with pytest.raises(ValueError, match="wire_decode: truncated input"):
+                O.wire_decode_topk(theirs[:-cut] if cut < theirs.size else theirs[:0])
+    # sign-bit body: the oracle's sign words (u32 LE) are the reference's sign bytes
+    for n in (1, 7, 8, 9, 37, 1000):
+        g = rng.standard_normal(n)
+        sb, sc = O.ref_compress_onebit(g)
+        words = np.zeros((n + 31) // 32, dtype=np.uint32)
+        words.view(np.uint8)[:sb.size] = sb
+        assert np.array_equal(O.wire_encode_signbit(n, sc, words), O.ref_wire_encode_onebit(g))
+    # dense layout (test_compression.cpp:215-218)
+    b = O.wire_encode_dense(np.array([1.0, 2.0]))
+    assert b.size == 8 + 16 and b[0] == 2
