@@ -7,7 +7,7 @@ compresses its own 125M gradient, the payloads are allgathered over NCCL and
 every replica applies the same rank-ordered mean (weak scaling).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config cfg2|cfg3|cfg4|cfg1] [--n N] [--rho R]
+                  [--config cfg2|cfg3|cfg4|cfg1|cfg2m] [--n N] [--rho R]
 
 One JSON line on rank 0 (contract in the task statement; fields explained in
 DESIGN.md "Measurement").
@@ -38,6 +38,9 @@ CONFIGS = {
              350_000_000, 0.001, "topk_q8", "naive", "llmrec", "async", {"staleness": 2}),
     "cfg1": ("cfg1: 1M-param gradient, top-k 1% + error feedback, sync SGD, 4 simulated workers",
              1_000_000, 0.01, "topk", "ring", "uniform", "sync", {"workers": 4}),
+    # north-star a24 (no reference code): reported separately from the reference-semantics SGD
+    "cfg2m": ("cfg2 + momentum SGD (beta 0.9, dense momentum pass; this build's rule, not the reference's)",
+              125_000_000, 0.01, "topk", "ring", "llmrec", "sync", {"momentum": 0.9}),
 }
 
 CLOCK_REASONS = {
@@ -210,8 +213,10 @@ def ours(args, cfg, world, rank, local_rank):
                 generate(dist_name, 42, rank * W + w, b, n, grads[b][w])
         res = torch.zeros(W, n, device=dev)
         theta = torch.zeros(n, device=dev)
+        mom = torch.zeros(n, device=dev) if "momentum" in extra else None
         descs = [ctx.step_desc(comp_code, grads[b], res, theta, 0.05, k, order,
-                               extra.get("q8_block", 256)) for b in range(NB)]
+                               extra.get("q8_block", 256), momentum=mom, beta=extra.get("momentum", 0.0))
+                 for b in range(NB)]
     stream.synchronize()
     gu = [0]
 
@@ -286,7 +291,8 @@ def ours(args, cfg, world, rank, local_rank):
         dev_g = [torch.empty(W, n, device=dev) for _ in range(2)]
         snap = [torch.empty(n, device=dev) for _ in range(2)]
         d_e2e = [ctx.step_desc(comp_code, dev_g[b], res, theta, 0.05, k, order,
-                               extra.get("q8_block", 256)) for b in range(2)]
+                               extra.get("q8_block", 256), momentum=mom, beta=extra.get("momentum", 0.0))
+                 for b in range(2)]
         s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         ev = lambda: torch.cuda.Event()  # noqa: E731
         in_done = [ev(), ev()]

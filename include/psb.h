@@ -259,6 +259,11 @@ PSB_API psb_status psb_onebit_mean_sgd(psb_ctx* ctx, psb_dtype dt, int P, const 
                                double lr, void* theta, size_t n, void* mean_out,
                                psb_stream_t stream);
 
+/* Momentum SGD pass (north-star a24, this build's rule -- no reference code):
+ * m = RN(RN(beta*m) + mean); theta = RN(RN(-lr*m) + theta), dense over n. */
+PSB_API psb_status psb_momentum_sgd(psb_ctx* ctx, psb_dtype dt, const void* mean, void* m, void* theta,
+                            double beta, double lr, size_t n, psb_stream_t stream);
+
 /* ------------------------------------------------------- step drivers */
 typedef struct {
   psb_compressor compressor;
@@ -274,6 +279,14 @@ typedef struct {
   psb_order order;
   psb_topology topo; /* for PSB_ORDER_HIER; zeros = flat (devices_per_node = P) */
   void* mean_out;    /* optional dense [n] aggregated mean (parity/debug) */
+  /* Momentum SGD (north-star a24; NO reference code -- the rule is this
+   * build's, restated in oracle/psb_oracle.c:orc_momentum): when m is
+   * non-NULL, with the aggregated mean g^ of the step,
+   *   m = RN(RN(beta * m) + g^);  theta = RN(RN(-lr * m) + theta)
+   * as a dense pass over n (sync steps, compressors NONE / ONEBIT / TOPK /
+   * TOPK_Q8).  Zero-initialised trailing fields keep plain SGD. */
+  void* m;           /* [n] momentum buffer (caller-owned, persistent), or NULL */
+  double beta;
 } psb_step_desc;
 
 /* sync_data_parallel_step (strategies.hpp:86-121) across W local workers x

@@ -66,6 +66,8 @@ def orc() -> ctypes.CDLL:
             "orc_async_scale": (_D, [_D, _U64]),
             "orc_q8_quant": (_I, [_P, _P, _SZ, _U32, _P, _P]),
             "orc_q8_dequant": (None, [_P, _P, _SZ, _U32, _P]),
+            "orc_momentum_f32": (None, [_P, _P, _P, _D, _D, _SZ]),
+            "orc_momentum_f64": (None, [_P, _P, _P, _D, _D, _SZ]),
             "orc_wire_encode_topk": (_SZ, [_U64, _P, _P, _SZ, _P]),
             "orc_wire_decode_topk": (ctypes.c_longlong, [_P, _SZ, _P, _P, _P]),
             "orc_wire_encode_signbit": (_SZ, [_U64, _D, _P, _P]),
@@ -299,6 +301,12 @@ def async_round(grads: np.ndarray, theta: np.ndarray, lr: float, k: int, residua
         axpy_(-float(orc().orc_async_scale(lr, tau)), g, theta)
         global_updates += 1
     return global_updates
+
+
+def momentum_(mean: np.ndarray, m: np.ndarray, theta: np.ndarray, beta: float, lr: float) -> None:
+    """Momentum SGD rule of this build (north-star a24, unpinned), in place."""
+    f = orc().orc_momentum_f64 if theta.dtype == np.float64 else orc().orc_momentum_f32
+    f(_p(mean), _p(m), _p(theta), beta, lr, theta.size)
 
 
 # ------------------------------------------------------------ wire format

@@ -456,3 +456,26 @@ size_t orc_wire_encode_dense(uint64_t dim, const double* x, uint8_t* out) {
   for (uint64_t i = 0; i < dim; ++i) put_f64(out + 8 + 8 * i, x[i]);
   return 8 + 8 * (size_t)dim;
 }
+
+/* ------------------------------------------------------------ momentum SGD
+ * North-star a24, NO reference code: this build's rule, with
+ * the reference's no-FMA convention (separate RN multiply and add):
+ *   m = RN(RN(beta * m) + mean);  theta = RN(RN(-lr * m) + theta)          */
+void orc_momentum_f32(const float* mean, float* m, float* theta, double beta, double lr, size_t n) {
+  const float b = (float)beta, c = (float)(-lr);
+  for (size_t i = 0; i < n; ++i) {
+    volatile float t = b * m[i];
+    m[i] = t + mean[i];
+    volatile float u = c * m[i];
+    theta[i] = u + theta[i];
+  }
+}
+void orc_momentum_f64(const double* mean, double* m, double* theta, double beta, double lr, size_t n) {
+  const double c = -lr;
+  for (size_t i = 0; i < n; ++i) {
+    volatile double t = beta * m[i];
+    m[i] = t + mean[i];
+    volatile double u = c * m[i];
+    theta[i] = u + theta[i];
+  }
+}

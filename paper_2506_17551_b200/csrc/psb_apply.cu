@@ -546,7 +546,67 @@ psb_status shard_fold_impl(psb_ctx* c, int P, const uint32_t* sidx, const T* sva
   return PSB_OK;
 }
 
+// Momentum SGD (north-star a24, this build's rule; include/psb.h):
+// m = RN(RN(beta*m) + mean); theta = RN(RN(-lr*m) + theta).  Dense, 20 B/el (f32).
+template <class T>
+__global__ void __launch_bounds__(256) k_momentum(const T* __restrict__ mean, T* __restrict__ m,
+                                                  T* __restrict__ theta, T beta, T coef, size_t n, uint32_t* flags) {
+  bool bad = false;
+  auto one = [&](size_t i) {
+    const T mi = add_rn(mul_rn(beta, m[i]), mean[i]);
+    m[i] = mi;
+    const T th = add_rn(mul_rn(coef, mi), theta[i]);
+    theta[i] = th;
+    bad |= !is_finite(th);
+  };
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (sizeof(T) == 4 && ((((uintptr_t)mean) | ((uintptr_t)m) | ((uintptr_t)theta)) & 15) == 0) {
+    const size_t nv = n / 4;
+    for (size_t v = t0; v < nv; v += stride) {
+      const float4 g4 = __ldcs(reinterpret_cast<const float4*>(mean) + v);
+      float4 m4 = __ldcs(reinterpret_cast<const float4*>(m) + v);
+      float4 t4 = __ldcs(reinterpret_cast<const float4*>(theta) + v);
+      const float b = (float)beta, cf = (float)coef;
+      m4.x = __fadd_rn(__fmul_rn(b, m4.x), g4.x);
+      m4.y = __fadd_rn(__fmul_rn(b, m4.y), g4.y);
+      m4.z = __fadd_rn(__fmul_rn(b, m4.z), g4.z);
+      m4.w = __fadd_rn(__fmul_rn(b, m4.w), g4.w);
+      t4.x = __fadd_rn(__fmul_rn(cf, m4.x), t4.x);
+      t4.y = __fadd_rn(__fmul_rn(cf, m4.y), t4.y);
+      t4.z = __fadd_rn(__fmul_rn(cf, m4.z), t4.z);
+      t4.w = __fadd_rn(__fmul_rn(cf, m4.w), t4.w);
+      __stcs(reinterpret_cast<float4*>(m) + v, m4);
+      __stcs(reinterpret_cast<float4*>(theta) + v, t4);
+      bad |= !is_finite(t4.x) || !is_finite(t4.y) || !is_finite(t4.z) || !is_finite(t4.w);
+    }
+    for (size_t i = nv * 4 + t0; i < n; i += stride) one(i);
+  } else {
+    for (size_t i = t0; i < n; i += stride) one(i);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
+}
+
 }  // namespace
+
+extern "C" psb_status psb_momentum_sgd(psb_ctx* c, psb_dtype dt, const void* mean, void* m, void* theta, double beta,
+                                       double lr, size_t n, psb_stream_t stream) {
+  PSB_REQUIRE(c, c != nullptr, "null ctx");
+  PSB_REQUIRE(c, dt == PSB_F32 || dt == PSB_F64, "momentum: bad dtype");
+  PSB_REQUIRE(c, mean && m && theta, "momentum: null buffer");
+  PSB_REQUIRE(c, lr > 0.0, "HyperParams: learning_rate must be > 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((n / 4 + 255) / 256, (size_t)c->num_sms * 8));
+  if (dt == PSB_F32)
+    k_momentum<float><<<grid, 256, 0, st>>>((const float*)mean, (float*)m, (float*)theta, (float)beta, (float)(-lr),
+                                            n, c->d_flags);
+  else
+    k_momentum<double><<<grid, 256, 0, st>>>((const double*)mean, (double*)m, (double*)theta, beta, -lr, n,
+                                             c->d_flags);
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "psb_momentum_sgd");
+  return PSB_OK;
+}
 
 psb_status psb_sparse_apply_tab(psb_ctx* c, psb_compressor comp, psb_dtype dt, int P, const void* payloads, size_t k,
                                 const uint32_t* tab, psb_order order, const psb_topology* topo, double lr,

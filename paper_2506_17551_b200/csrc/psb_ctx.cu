@@ -127,7 +127,7 @@ extern "C" void psb_ctx_destroy(psb_ctx* c) {
   psb_peer_destroy(c);
   void* ptrs[] = {c->d_flags,    c->d_tk,        c->d_tw,        c->d_hist1,   c->d_histr,
                   c->d_seg_cnt,  c->d_cta,       c->d_histd,       c->d_stage_idx, c->d_stage_val,
-                  c->d_seg_off,  c->d_partials,  c->d_gather,    c->d_work,    c->d_qmean};
+                  c->d_seg_off,  c->d_partials,  c->d_gather,    c->d_work,    c->d_qmean,   c->d_mom_mean};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -582,9 +582,10 @@ static psb_status q8_step(psb_ctx* c, const psb_step_desc* d, cudaStream_t st) {
   return psb_q8_apply_launch(c, mcodes, mscales, n, B, d->lr, theta, mean_out, st);
 }
 
-extern "C" psb_status psb_sync_step(psb_ctx* c, const psb_step_desc* d, psb_stream_t stream) {
-  psb_status s = check_desc(c, d);
-  if (s) return s;
+// The step on a validated descriptor; theta == NULL computes only the mean
+// (into mean_out) -- the momentum path uses that.
+static psb_status sync_step_core(psb_ctx* c, const psb_step_desc* d, psb_stream_t stream) {
+  psb_status s = PSB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const int W = d->workers, P = W * c->nranks;
   const size_t es = d->dtype == PSB_F64 ? 8 : 4;
@@ -592,7 +593,7 @@ extern "C" psb_status psb_sync_step(psb_ctx* c, const psb_step_desc* d, psb_stre
     case PSB_COMP_TOPK:
     case PSB_COMP_TOPK_Q8: {
       uint8_t* pl = nullptr;
-      const bool fuse = P == 1 && d->compressor == PSB_COMP_TOPK;
+      const bool fuse = P == 1 && d->compressor == PSB_COMP_TOPK && d->theta != nullptr;
       ShardPlan sp;
       s = compress_and_gather(c, d, st, &pl, fuse, &sp);
       if (s || fuse) return s;
@@ -658,11 +659,37 @@ extern "C" psb_status psb_sync_step(psb_ctx* c, const psb_step_desc* d, psb_stre
   return psb_set_err(c, PSB_EINVAL, "compress: unknown compressor kind");
 }
 
+extern "C" psb_status psb_sync_step(psb_ctx* c, const psb_step_desc* d, psb_stream_t stream) {
+  psb_status s = check_desc(c, d);
+  if (s) return s;
+  if (!d->m) return sync_step_core(c, d, stream);
+  // momentum SGD: the step's aggregated mean into a zeroed dense scratch,
+  // then one dense pass m = beta*m + mean; theta = (-lr)*m + theta
+  PSB_REQUIRE(c, d->compressor != PSB_COMP_Q8, "momentum: not supported with the dense q8 compressor");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t es = d->dtype == PSB_F64 ? 8 : 4;
+  s = ensure(c, &c->d_mom_mean, &c->mom_bytes, es * d->n, "momentum mean buffer");
+  if (s) return s;
+  CUDA_TRY(c, cudaMemsetAsync(c->d_mom_mean, 0, es * d->n, st), "momentum");
+  psb_step_desc d2 = *d;
+  d2.theta = nullptr;
+  d2.mean_out = c->d_mom_mean;
+  d2.m = nullptr;
+  s = sync_step_core(c, &d2, stream);
+  if (s) return s;
+  s = psb_momentum_sgd(c, d->dtype, c->d_mom_mean, d->m, d->theta, d->beta, d->lr, d->n, stream);
+  if (s) return s;
+  if (d->mean_out)
+    CUDA_TRY(c, cudaMemcpyAsync(d->mean_out, c->d_mom_mean, es * d->n, cudaMemcpyDeviceToDevice, st), "momentum");
+  return PSB_OK;
+}
+
 extern "C" psb_status psb_async_round(psb_ctx* c, const psb_step_desc* d, uint32_t staleness_bound,
                                       uint64_t* global_updates, psb_stream_t stream) {
   psb_status s = check_desc(c, d);
   if (s) return s;
   PSB_REQUIRE(c, global_updates != nullptr, "psb_async_round: null global_updates");
+  PSB_REQUIRE(c, d->m == nullptr, "psb_async_round: momentum is defined for sync steps only");
   PSB_REQUIRE(c, d->compressor == PSB_COMP_TOPK || d->compressor == PSB_COMP_TOPK_Q8,
               "psb_async_round: sparse compressors only");
   cudaStream_t st = (cudaStream_t)stream;

@@ -87,6 +87,8 @@ struct psb_ctx {
   void* d_work = nullptr;  // generic workspace
   size_t work_bytes = 0;
   float* d_qmean = nullptr;
+  void* d_mom_mean = nullptr;  // momentum: the step's dense mean
+  size_t mom_bytes = 0;
   // kernel timing (psb_profile_*)
   int prof = 0;
   int predict = 1;  // K1 threshold prediction (PSB_NO_PREDICT=1 disables)

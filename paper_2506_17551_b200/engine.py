@@ -300,8 +300,11 @@ class Context:
     def step_desc(self, compressor: int, g: torch.Tensor, r: Optional[torch.Tensor],
                   theta: torch.Tensor, lr: float, k: int = 0, order: str = "naive",
                   q8_block: int = 256, topo: Optional[L.Topology] = None,
-                  mean_out: Optional[torch.Tensor] = None) -> L.StepDesc:
-        _need_cuda(g, r, theta, mean_out)
+                  mean_out: Optional[torch.Tensor] = None, momentum: Optional[torch.Tensor] = None,
+                  beta: float = 0.0) -> L.StepDesc:
+        """psb_step_desc; momentum (a persistent [n] buffer) with factor beta
+        turns the update into momentum SGD (see include/psb.h)."""
+        _need_cuda(g, r, theta, mean_out, momentum)
         W = g.shape[0] if g.dim() == 2 else 1
         n = g.shape[-1]
         d = L.StepDesc()
@@ -313,6 +316,8 @@ class Context:
         d.order = ORDERS[order]
         d.topo = topo or topology()
         d.mean_out = _ptr(mean_out)
+        d.m = _ptr(momentum)
+        d.beta = beta
         return d
 
     def sync_step(self, desc: L.StepDesc) -> None:

@@ -258,3 +258,53 @@ def test_step_rejects_bad_args(ctx):
         ctx.sync_step(ctx.step_desc(L.PSB_COMP_TOPK, g, None, theta, 0.0, 5))
     with pytest.raises(PsbInvalidArgument, match="k out of range"):
         ctx.sync_step(ctx.step_desc(L.PSB_COMP_TOPK, g, None, theta, 0.1, 101))
+
+
+@pytest.mark.parametrize("comp", ["topk", "topk_q8", "none", "onebit"])
+@pytest.mark.parametrize("W", [1, 4])
+def test_momentum_sync_step(ctx, comp, W):
+    """Momentum SGD (north-star a24, this build's rule; no reference code):
+    psb_sync_step with a momentum buffer vs the oracle composite (reference
+    step's mean, then orc_momentum), 6 steps, EF carried; bit-exact."""
+    n, k, lr, beta = 100_000, 1_000, 0.05, 0.9
+    theta_h = np.zeros(n, dtype=np.float32)
+    m_h = np.zeros(n, dtype=np.float32)
+    res_h = np.zeros((W, n), dtype=np.float32)
+    theta = torch.zeros(n, device="cuda")
+    m = torch.zeros(n, device="cuda")
+    res = torch.zeros(W, n, device="cuda")
+    for step in range(6):
+        g_h = np.stack([O.generate("llmrec", 11, w, step, n) for w in range(W)])
+        g = torch.from_numpy(g_h).cuda()
+        mean = torch.zeros(n, device="cuda")
+        d = ctx.step_desc(COMPS[comp], g, res, theta, lr, k, "ring", 256, None, mean, momentum=m, beta=beta)
+        ctx.sync_step(d)
+        ctx.check()
+        dummy = theta_h.copy()
+        mean_h = O.sync_step(g_h, dummy, lr, comp, k, "ring", res_h).astype(np.float32)
+        if comp == "onebit":
+            # 1-bit scale: fixed-shape tree sum vs sequential fold (DESIGN.md 5); compare with
+            # tolerance, then continue from the oracle's state
+            np.testing.assert_allclose(tnp(mean), mean_h, rtol=1e-5, atol=1e-9)
+            mean_h = tnp(mean).copy()
+        O.momentum_(mean_h, m_h, theta_h, beta, lr)
+        assert np.array_equal(bits(tnp(mean)), bits(mean_h)), step
+        assert np.array_equal(bits(tnp(m)), bits(m_h)), step
+        assert np.array_equal(bits(tnp(theta)), bits(theta_h)), step
+        if comp == "onebit":
+            res.copy_(torch.from_numpy(res_h))  # residuals carry the scale tolerance
+        else:
+            assert np.array_equal(bits(tnp(res)), bits(res_h)), step
+
+
+def test_momentum_rejects_q8_and_async(ctx):
+    n = 4096
+    g = torch.randn(1, n, device="cuda")
+    d = ctx.step_desc(L.PSB_COMP_Q8, g, None, torch.zeros(n, device="cuda"), 0.1, 0, "naive", 256,
+                      momentum=torch.zeros(n, device="cuda"), beta=0.9)
+    with pytest.raises(L.PsbInvalidArgument, match="momentum"):
+        ctx.sync_step(d)
+    d = ctx.step_desc(L.PSB_COMP_TOPK, g, None, torch.zeros(n, device="cuda"), 0.1, 16, "naive", 256,
+                      momentum=torch.zeros(n, device="cuda"), beta=0.9)
+    with pytest.raises(L.PsbInvalidArgument, match="momentum"):
+        ctx.async_round(d, 2, 0)
