@@ -172,6 +172,18 @@ PSB_API psb_status psb_wire_encode_signbit(psb_ctx* ctx, uint64_t dim, const uin
 PSB_API psb_status psb_wire_encode_dense(psb_ctx* ctx, psb_dtype dt, const void* x, uint64_t dim, void* out,
                                  psb_stream_t stream);
 
+/* ------------------------------------------- gradient producer (BPR)
+ * bpr_batch_gradient + bpr_batch_loss (parsim/trainer.hpp:98-138) for the
+ * reference's matrix-factorisation recommender; flat theta = user rows then
+ * item rows, dim columns (trainer.hpp:86-91).  Triples (user, pos, neg) are
+ * device u32 arrays of length B.  grad ([users+items][dim], dtype) is fully
+ * written (zeros outside the touched rows); loss_out (device double, nullable)
+ * gets the batch-mean loss.  Every row's contributions are folded in batch
+ * order as the reference does; exp() is the device's (<= 1 ulp from glibc). */
+PSB_API psb_status psb_bpr_gradient(psb_ctx* ctx, psb_dtype dt, const void* theta, uint32_t users, uint32_t items,
+                            uint32_t dim, const uint32_t* user, const uint32_t* pos, const uint32_t* neg,
+                            uint32_t B, void* grad, double* loss_out, psb_stream_t stream);
+
 /* ---------------------------------------------------------- generator
  * Counter-based synthetic gradients, identical bits to
  * oracle/psb_oracle.c:orc_generate.  Input generation only. */

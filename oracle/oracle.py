@@ -106,6 +106,7 @@ def ref() -> ctypes.CDLL:
             "ref_wire_encode_topk": (_SZ, [_U64, _P, _P, _SZ, _P]),
             "ref_wire_decode_topk": (ctypes.c_longlong, [_P, _SZ, _P, _P, _P]),
             "ref_wire_encode_onebit": (_SZ, [_P, _SZ, _P]),
+            "ref_bpr_batch_gradient": (_I, [_P, _SZ, _SZ, _SZ, _P, _P, _P, _SZ, _P, _P]),
         }
         for k, (res, args) in sig.items():
             f = getattr(lib, k)
@@ -373,6 +374,18 @@ def ref_wire_encode_onebit(g: np.ndarray) -> np.ndarray:
     out = np.empty(n, dtype=np.uint8)
     ref().ref_wire_encode_onebit(_p(g), g.size, _p(out))
     return out
+
+
+def ref_bpr_batch_gradient(theta: np.ndarray, users: int, items: int, dim: int, u: np.ndarray, p: np.ndarray,
+                           q: np.ndarray):
+    """The reference's bpr_batch_gradient / bpr_batch_loss (trainer.hpp:98-138), f64."""
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    u, p, q = (np.ascontiguousarray(a, dtype=np.uint32) for a in (u, p, q))
+    grad = np.empty_like(theta)
+    loss = np.zeros(1, dtype=np.float64)
+    _ref_ck(ref().ref_bpr_batch_gradient(_p(theta), users, items, dim, _p(u), _p(p), _p(q), u.size, _p(grad),
+                                         _p(loss)))
+    return grad, float(loss[0])
 
 
 # ---------------------------------------------------------------- reference

@@ -18,6 +18,7 @@
 //   vec_axpy             parsim/numerics.hpp:70-78
 //   SeededRng            parsim/numerics.hpp:152-178
 //   wire_encode / wire_decode  parsim/compression.hpp:188-239
+//   bpr_batch_gradient / bpr_batch_loss  parsim/trainer.hpp:98-138
 
 #include <cstring>
 #include <exception>
@@ -28,6 +29,7 @@
 #include "parsim/compression.hpp"
 #include "parsim/numerics.hpp"
 #include "parsim/strategies.hpp"
+#include "parsim/trainer.hpp"
 
 using namespace parsim;
 
@@ -319,4 +321,21 @@ extern "C" size_t ref_wire_encode_onebit(const double* g, size_t n, uint8_t* out
   const std::vector<std::uint8_t> w = wire_encode(compress_onebit(x));
   if (out) std::memcpy(out, w.data(), w.size());
   return w.size();
+}
+
+// bpr_batch_gradient + bpr_batch_loss on flat f64 theta (trainer.hpp:98-138).
+extern "C" int ref_bpr_batch_gradient(const double* theta, size_t users, size_t items, size_t dim,
+                                      const uint32_t* u, const uint32_t* p, const uint32_t* q, size_t B,
+                                      double* grad_out, double* loss_out) {
+  try {
+    const DenseVector th(theta, theta + (users + items) * dim);
+    std::vector<BprTriple> batch(B);
+    for (size_t t = 0; t < B; ++t) batch[t] = {u[t], p[t], q[t]};
+    const DenseVector g = bpr_batch_gradient(th, users, items, dim, batch);
+    std::memcpy(grad_out, g.data(), g.size() * sizeof(double));
+    if (loss_out) *loss_out = bpr_batch_loss(th, users, items, dim, batch);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
 }

@@ -207,6 +207,7 @@ extern "C" psb_status psb_check(psb_ctx* c, psb_stream_t stream) {
     if (flags & 16u) return psb_set_err(c, PSB_EINVAL, "wire_decode: truncated input");
     if (flags & 32u) return psb_set_err(c, PSB_EINVAL, "wire_decode: message exceeds the output capacity");
     if (flags & 64u) return psb_set_err(c, PSB_EINVAL, "wire_decode: index exceeds the 32-bit range");
+    if (flags & 128u) return psb_set_err(c, PSB_EINVAL, "bpr_batch_gradient: triple index out of range");
     if (flags & 2u) return psb_set_err(c, PSB_EINVAL, "decompress: index out of range for dim");
     if (flags & 4u) return psb_set_err(c, PSB_EINVAL, "decompress: indices not strictly increasing");
     return psb_set_err(c, PSB_ENONFINITE, "ef_compress_step residual: non-finite entry");

@@ -220,6 +220,21 @@ class Context:
                  "decompress")
         return out
 
+    # ----------------------------------------------------- gradient producer
+    def bpr_gradient(self, theta: torch.Tensor, users: int, items: int, dim: int, user: torch.Tensor,
+                     pos: torch.Tensor, neg: torch.Tensor, grad: Optional[torch.Tensor] = None,
+                     want_loss: bool = True):
+        """bpr_batch_gradient / bpr_batch_loss (parsim/trainer.hpp:98-138) on the device."""
+        _need_cuda(theta, user, pos, neg, grad)
+        if grad is None:
+            grad = torch.empty_like(theta)
+        loss = torch.zeros(1, dtype=torch.float64, device=theta.device) if want_loss else None
+        B = user.numel()
+        self._ck(self.lib.psb_bpr_gradient(self.h, _dtype_code(theta), theta.data_ptr(), users, items, dim,
+                                           user.data_ptr(), pos.data_ptr(), neg.data_ptr(), B, grad.data_ptr(),
+                                           _ptr(loss), self.stream()), "bpr_batch_gradient")
+        return grad, loss
+
     # ---------------------------------------------------------- wire format
     def wire_encode_topk(self, dim: int, idx: torch.Tensor, val: torch.Tensor) -> torch.Tensor:
         """parsim wire_encode(TopKPayload): u64 dim | u64 count | (u64 idx, f64 val) x count."""
