@@ -234,6 +234,9 @@ __global__ void k_topk_begin(TopkScratch* s, TopkWorker* w, uint32_t* hist1, uin
 // 276 us): the ring halves the resident CTAs and this pass is bound by its
 // per-tile compaction, not by bytes in flight.  Everything else is identical.
 constexpr int kScanStages = 2;
+#ifndef PSB_PF
+#define PSB_PF 1  // L2 prefetch distance of the streaming pass, in tiles
+#endif
 
 template <class T, int MODE, bool TMA = false>
 __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
@@ -336,15 +339,22 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
       }
       __syncthreads();  // every thread has read stage sidx: refill it
       if (threadIdx.x == 0 && tile + kScanStages < t_full) issue(tile + kScanStages);
-    } else if (!TMA && MODE == MODE_A && threadIdx.x == 0 && tile + 1 < t_hi &&
-               base + 2 * (size_t)TILE <= a.n && a.vec_ok) {
-      // TMA bulk prefetch of the next tile into L2: its loads then hit L2
-      // while this tile's scan and stores run
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + base + TILE),
-                   "r"((uint32_t)(TILE * sizeof(T))) : "memory");
-      if (rr != nullptr)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rr + base + TILE),
-                     "r"((uint32_t)(TILE * sizeof(T))) : "memory");
+    } else if (!TMA && MODE == MODE_A && threadIdx.x == 0 && a.vec_ok) {
+      // TMA bulk prefetch into L2, PSB_PF tiles ahead (the first tile also
+      // primes the ones before): those loads then hit L2 while this tile's
+      // scan and stores run
+      auto pf = [&](uint32_t t2) {
+        if (t2 < t_hi && (size_t)(t2 + 1) * TILE <= a.n) {
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + (size_t)t2 * TILE),
+                       "r"((uint32_t)(TILE * sizeof(T))) : "memory");
+          if (rr != nullptr)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rr + (size_t)t2 * TILE),
+                         "r"((uint32_t)(TILE * sizeof(T))) : "memory");
+        }
+      };
+      if (tile == t_lo)
+        for (uint32_t d = 1; d < PSB_PF; ++d) pf(tile + d);
+      pf(tile + PSB_PF);
     }
     if (TMA && tile < t_full) {
       // staged above
@@ -506,7 +516,10 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
 }
 
 template <class T, int MODE, bool TMA = false>
-__global__ void __launch_bounds__(PSB_SCAN_THREADS) k_scan(ScanArgs<T> a) {
+#ifndef PSB_SCAN_MINB
+#define PSB_SCAN_MINB 4
+#endif
+__global__ void __launch_bounds__(PSB_SCAN_THREADS, PSB_SCAN_MINB) k_scan(ScanArgs<T> a) {
   scan_body<T, MODE, TMA>(a);
 }
 
@@ -571,7 +584,7 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   // TMA streaming (EF, aligned): as many CTAs per SM as the stage ring allows
   const bool tma = r != nullptr && vec_ok && c->scan_tma && (size_t)ntiles >= (size_t)c->num_sms;
   const size_t tma_smem = (size_t)2 * kScanStages * TILE * sizeof(T);
-  int per_sm = 4;
+  int per_sm = PSB_SCAN_MINB;
   if (tma) {
     cudaFuncSetAttribute(k_scan<T, MODE_A, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem);
     int occ = 0;
