@@ -116,7 +116,10 @@ __global__ void __launch_bounds__(256) k_seg_offsets(PayloadView v, int P, uint3
 #define PSB_APPLY_MINB 4
 #endif
 template <class T, bool ASYNC, int PT>
-__global__ void __launch_bounds__(256, PSB_APPLY_MINB)
+#ifndef PSB_APPLY_THREADS
+#define PSB_APPLY_THREADS 256
+#endif
+__global__ void __launch_bounds__(PSB_APPLY_THREADS, PSB_APPLY_MINB)
     k_sparse_apply_bm(PayloadView v, int P_rt, uint32_t nseg, uint32_t seg_lo, const uint32_t* __restrict__ range,
                       int seg_shift, uint32_t vcap,
                       const uint32_t* __restrict__ seg_off, int order, uint32_t dpn, uint32_t npr, T coef,
@@ -464,7 +467,7 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
   const unsigned grid = (unsigned)std::min<size_t>(nseg, 1u << 20);
   auto launch = [&](auto kern, T* mo) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, 256, smem, st>>>(v, P, nseg, 0u, nullptr, seg_shift, vcap, tab, (int)order, dpn, npr, coef, ws,
+    kern<<<grid, PSB_APPLY_THREADS, smem, st>>>(v, P, nseg, 0u, nullptr, seg_shift, vcap, tab, (int)order, dpn, npr, coef, ws,
                                   theta, n, mo, nullptr, nullptr, nullptr, c->d_flags);
   };
   if (async_mode) {
@@ -523,7 +526,7 @@ psb_status shard_fold_impl(psb_ctx* c, int P, const uint32_t* sidx, const T* sva
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // persistent CTAs over the device-decided segment range
-    kern<<<c->num_sms * 4, 256, smem, st>>>(v, P, 0u, 0u, range, seg_shift, vcap, srow, (int)order, dpn, npr, coef,
+    kern<<<c->num_sms * 4, PSB_APPLY_THREADS, smem, st>>>(v, P, 0u, 0u, range, seg_shift, vcap, srow, (int)order, dpn, npr, coef,
                                             ws, theta, n, nullptr, list_idx, list_val, list_cnt, c->d_flags);
   };
   if (async_mode) {
