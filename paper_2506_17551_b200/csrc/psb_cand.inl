@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   // One histogram pass over the slice (digit(key) for matching keys), flushed
   // into global histogram `g`; then the grid barrier; then every CTA resolves
   // the level from `g`: bin holding the need-th largest (bin 0 implicit).
+  bool pf_theta = a.theta != nullptr && staged;  // first level pass only
   auto level_pass = [&](uint32_t* g, uint32_t nbins, unsigned long long need, unsigned long long match,
                         auto digit_of, uint32_t* bin, unsigned long long* above,
                         unsigned long long* bcnt) {
@@ -190,7 +191,14 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       const uint32_t j0 = base + 4 * threadIdx.x;
       T v[4];
       uint32_t id[4];
-      load4(j0, v, id, false);
+      load4(j0, v, id, pf_theta);
+      if (pf_theta) {
+        // the fused SGD at the end updates theta at the selected indices:
+        // pull those sectors into L2 while this pass (sync/atomic-bound) runs
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (j0 + c < cnt) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.theta + id[c]));
+      }
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t d = 0;
@@ -203,6 +211,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       const uint32_t h = sh_h[b];
       if (h) atomicAdd(&g[b], h);
     }
+    pf_theta = false;
     grid.sync();
     phase();
     resolve_level(g, nbins, 1, need, sh_warp, &sh_res, sh_h);
