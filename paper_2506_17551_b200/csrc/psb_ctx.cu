@@ -420,6 +420,7 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
     s = psb_seg_offsets(c, d->compressor, d->dtype, W, gb + (size_t)c->rank * W * blk, d->k, sp.nseg, sp.seg_shift,
                         tab, st);
     if (s) return s;
+    psb_mark(c, st);
   }
   if (push) {
     // payloads are already in every peer's arena; push the offset rows, signal, wait

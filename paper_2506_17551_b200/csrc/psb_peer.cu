@@ -662,3 +662,19 @@ extern "C" PSB_API int psb_debug_scatter(float* theta, const uint32_t* idx, cons
   k_debug_scatter<<<ctas, 256, 0, (cudaStream_t)stream>>>(theta, idx, val, cnt);
   return (int)cudaGetLastError();
 }
+
+// Diagnostics: `iters` bare payload exchanges of bytes_per_rank (arena set up
+// on first use; every rank must call it together).
+extern "C" PSB_API psb_status psb_debug_exchange(psb_ctx* c, size_t bytes_per_rank, int iters, psb_stream_t stream) {
+  PSB_REQUIRE(c, c != nullptr && c->nranks > 1, "debug exchange: needs a multi-rank ctx");
+  cudaStream_t st = (cudaStream_t)stream;
+  psb_status s = psb_peer_ensure(c, bytes_per_rank * c->nranks, st);
+  if (s) return s;
+  for (int i = 0; i < iters; ++i) {
+    s = psb_peer_wait_ack(c, st);
+    if (s) return s;
+    s = psb_peer_exchange(c, bytes_per_rank, 0, 0, st);
+    if (s) return s;
+  }
+  return PSB_OK;
+}
