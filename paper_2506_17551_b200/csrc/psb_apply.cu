@@ -112,14 +112,13 @@ __global__ void __launch_bounds__(256) k_seg_offsets(PayloadView v, int P, uint3
 // in order).  Dependent global round trips per segment: segment offsets,
 // entry loads, theta -- the rest is shared memory.  PT > 0 fixes P at
 // compile time (worker lookup in registers); PT == 0 is the generic kernel.
-#ifndef PSB_APPLY_MINB
-#define PSB_APPLY_MINB 4
-#endif
+// CTA shape per compile-time P (measured on B200): 256 threads x 4 CTAs/SM,
+// and 128 x 6 for P = 8 (more segments in flight; P = 8 324 -> 269 us).
+__host__ __device__ constexpr int apply_threads(int PT) { return PT == 8 ? 128 : 256; }
+__host__ __device__ constexpr int apply_minb(int PT) { return PT == 8 ? 6 : 4; }
+
 template <class T, bool ASYNC, int PT>
-#ifndef PSB_APPLY_THREADS
-#define PSB_APPLY_THREADS 256
-#endif
-__global__ void __launch_bounds__(PSB_APPLY_THREADS, PSB_APPLY_MINB)
+__global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
     k_sparse_apply_bm(PayloadView v, int P_rt, uint32_t nseg, uint32_t seg_lo, const uint32_t* __restrict__ range,
                       int seg_shift, uint32_t vcap,
                       const uint32_t* __restrict__ seg_off, int order, uint32_t dpn, uint32_t npr, T coef,
@@ -467,7 +466,8 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
   const unsigned grid = (unsigned)std::min<size_t>(nseg, 1u << 20);
   auto launch = [&](auto kern, T* mo) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, PSB_APPLY_THREADS, smem, st>>>(v, P, nseg, 0u, nullptr, seg_shift, vcap, tab, (int)order, dpn, npr, coef, ws,
+    kern<<<grid, apply_threads(P == 2 || P == 4 || P == 8 ? P : 0), smem, st>>>(v, P, nseg, 0u, nullptr, seg_shift,
+                                                                               vcap, tab, (int)order, dpn, npr, coef, ws,
                                   theta, n, mo, nullptr, nullptr, nullptr, c->d_flags);
   };
   if (async_mode) {
@@ -526,7 +526,7 @@ psb_status shard_fold_impl(psb_ctx* c, int P, const uint32_t* sidx, const T* sva
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // persistent CTAs over the device-decided segment range
-    kern<<<c->num_sms * 4, PSB_APPLY_THREADS, smem, st>>>(v, P, 0u, 0u, range, seg_shift, vcap, srow, (int)order, dpn, npr, coef,
+    kern<<<c->num_sms * 4, apply_threads(P == 2 || P == 4 || P == 8 ? P : 0), smem, st>>>(v, P, 0u, 0u, range, seg_shift, vcap, srow, (int)order, dpn, npr, coef,
                                             ws, theta, n, nullptr, list_idx, list_val, list_cnt, c->d_flags);
   };
   if (async_mode) {
