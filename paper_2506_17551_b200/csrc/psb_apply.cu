@@ -112,6 +112,9 @@ __global__ void __launch_bounds__(256) k_seg_offsets(PayloadView v, int P, uint3
 // in order).  Dependent global round trips per segment: segment offsets,
 // entry loads, theta -- the rest is shared memory.  PT > 0 fixes P at
 // compile time (worker lookup in registers); PT == 0 is the generic kernel.
+#ifndef PSB_APPLY_U
+#define PSB_APPLY_U 2
+#endif
 // CTA shape per compile-time P (measured on B200): 256 threads x 4 CTAs/SM,
 // and 128 x 6 for P = 8 (more segments in flight; P = 8 324 -> 269 us).
 __host__ __device__ constexpr int apply_threads(int PT) { return PT == 8 ? 128 : 256; }
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
                       WorkerCoefs wscale, T* __restrict__ theta, size_t n, T* __restrict__ mean_out,
                       uint32_t* __restrict__ list_idx, T* __restrict__ list_val, uint32_t* list_cnt,
                       uint32_t* flags) {
-  constexpr int U = 4;  // entries per thread per batch
+  constexpr int U = PSB_APPLY_U;  // entries per thread per batch
   const int P = PT > 0 ? PT : P_rt;
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t NW = (1u << seg_shift) >> 5;  // bitmap words per worker

@@ -92,7 +92,7 @@ struct psb_ctx {
   // kernel timing (psb_profile_*)
   int prof = 0;
   int predict = 1;  // K1 threshold prediction (PSB_NO_PREDICT=1 disables)
-  uint32_t apply_vcap = 4096;  // PSB_APPLY_VCAP: staged entries per apply segment
+  uint32_t apply_vcap = 2048;  // PSB_APPLY_VCAP: staged entries per apply segment
   int scan_tma = 0;  // PSB_SCAN_TMA=1: K1 streaming pass through a TMA stage ring (measured slower)
   int q8_no_tma = 0;   // PSB_Q8_NO_TMA=1: register double-buffer kernel for the one-worker q8 step
   int q8_unfused = 0;  // PSB_Q8_UNFUSED=1: single-rank q8 step as quant + reduce (diagnostics)
