@@ -156,9 +156,12 @@ psb_status psb_shard_fold(psb_ctx* c, psb_dtype dt, int P, const uint32_t* sidx,
 
 // Segment size of the P-worker sparse apply: P bitmaps of S bits (x2 with the
 // word ranks) within 16 KB of shared memory, 2^10 <= S <= 2^15.
+#ifndef PSB_APPLY_BM_BYTES
+#define PSB_APPLY_BM_BYTES (16 * 1024)
+#endif
 static inline int psb_apply_seg_shift(int P) {
   int s = 15;
-  while (s > 10 && ((size_t)P * 8) << (s - 5) > 16 * 1024) --s;
+  while (s > 10 && ((size_t)P * 8) << (s - 5) > PSB_APPLY_BM_BYTES) --s;
   return s;
 }
 
