@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       for (int c = 0; c < 4; ++c) {
         uint32_t d = 0;
         const bool ok = digit_of(KO::key(v[c]), &d) && j0 + c < cnt;
-        hist_add_agg(sh_h, d, ok);
+        if (ok) atomicAdd(&sh_h[d], 1u);  // candidate keys spread over the bins: plain smem atomics
       }
     }
     __syncthreads();
