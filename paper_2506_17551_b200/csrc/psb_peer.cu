@@ -27,6 +27,12 @@
 namespace {
 
 constexpr size_t kHdrBytes = 4096;
+#ifndef PSB_PULL_U
+#define PSB_PULL_U 4  // int4 loads in flight per thread in the pull
+#endif
+#ifndef PSB_PULL_CTAS
+#define PSB_PULL_CTAS 4  // pull CTAs per SM
+#endif
 // header words: [0,32) ready[p]: p's payloads of seq are in place
 //               [32,64) ackp[p]: p has finished reading our payloads of seq
 //               [64,96) upd[p]: p's update list of seq is complete (sharded apply)
@@ -138,7 +144,7 @@ __global__ void __launch_bounds__(256) k_peer_pull(PeerPtrs pp, int R, int rank,
     const size_t stride = (size_t)ncta * blockDim.x;
     const uint8_t* src = pp.base[p] + kHdrBytes + (size_t)p * bpr;
     uint8_t* dst = pp.base[rank] + kHdrBytes + (size_t)p * bpr;
-    constexpr int U = 4;
+    constexpr int U = PSB_PULL_U;
     for (size_t t0 = (size_t)cta * blockDim.x + threadIdx.x; t0 < nv; t0 += U * stride) {
       int4 v[U];
 #pragma unroll
@@ -146,7 +152,7 @@ __global__ void __launch_bounds__(256) k_peer_pull(PeerPtrs pp, int R, int rank,
         if (t0 + u * stride < nv) v[u] = __ldcs(reinterpret_cast<const int4*>(src) + t0 + u * stride);
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (t0 + u * stride < nv) reinterpret_cast<int4*>(dst)[t0 + u * stride] = v[u];
+        if (t0 + u * stride < nv) __stcg(reinterpret_cast<int4*>(dst) + t0 + u * stride, v[u]);
     }
     if (tw) {
       const uint32_t* ts = reinterpret_cast<const uint32_t*>(pp.base[p] + kHdrBytes + tab_off) + (size_t)p * tw;
@@ -461,7 +467,7 @@ psb_status psb_peer_exchange(psb_ctx* c, size_t bytes_per_rank, size_t tab_off, 
   k_peer_signal<<<1, 1, 0, st>>>(pp, c->nranks, c->rank);
   const size_t npeer = (size_t)c->nranks - 1;
   const size_t per = std::max<size_t>(1, std::min<size_t>((bytes_per_rank / 16 + 1023) / 1024,
-                                                          (size_t)c->num_sms * 4 / npeer));
+                                                          (size_t)c->num_sms * PSB_PULL_CTAS / npeer));
   k_peer_pull<<<(unsigned)(per * npeer), 256, 0, st>>>(pp, c->nranks, c->rank, bytes_per_rank, tab_off,
                                                         tab_words_per_rank, c->d_flags);
   c->launches += 2;
