@@ -107,6 +107,7 @@ def ref() -> ctypes.CDLL:
             "ref_wire_decode_topk": (ctypes.c_longlong, [_P, _SZ, _P, _P, _P]),
             "ref_wire_encode_onebit": (_SZ, [_P, _SZ, _P]),
             "ref_bpr_batch_gradient": (_I, [_P, _SZ, _SZ, _SZ, _P, _P, _P, _SZ, _P, _P]),
+            "ref_train": (_I, [_SZ, _SZ, _SZ, _P, _P, _SZ, _SZ, _I, _SZ, _SZ, _D, _I, _SZ, _I, _U64, _P, _P, _SZ, _P]),
         }
         for k, (res, args) in sig.items():
             f = getattr(lib, k)
@@ -386,6 +387,22 @@ def ref_bpr_batch_gradient(theta: np.ndarray, users: int, items: int, dim: int, 
     _ref_ck(ref().ref_bpr_batch_gradient(_p(theta), users, items, dim, _p(u), _p(p), _p(q), u.size, _p(grad),
                                          _p(loss)))
     return grad, float(loss[0])
+
+
+def ref_train(users: int, items: int, dim: int, train_u: np.ndarray, train_i: np.ndarray, P: int, mode: str,
+              steps: int, batch: int, lr: float, kind: str, k: int, algo: str, seed: int):
+    """The reference trainer (trainer.hpp:197-261): final flat theta and loss curve."""
+    tu = np.ascontiguousarray(train_u, dtype=np.uint64)
+    ti = np.ascontiguousarray(train_i, dtype=np.uint64)
+    theta = np.empty((users + items) * dim, dtype=np.float64)
+    cap = steps // 100 + 2
+    curve = np.zeros(2 * cap, dtype=np.float64)
+    cn = np.zeros(1, dtype=np.uint64)
+    _ref_ck(ref().ref_train(users, items, dim, _p(tu), _p(ti), tu.size, P, 0 if mode == "sync" else 1, steps, batch,
+                            lr, {"none": 0, "onebit": 1, "topk": 2}[kind], k,
+                            {"naive": 0, "ring": 1, "hierarchical": 2}[algo], seed, _p(theta), _p(curve), cap, _p(cn)))
+    m = int(cn[0])
+    return theta, [(int(curve[2 * j]), float(curve[2 * j + 1])) for j in range(m)]
 
 
 # ---------------------------------------------------------------- reference

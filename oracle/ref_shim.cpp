@@ -339,3 +339,39 @@ extern "C" int ref_bpr_batch_gradient(const double* theta, size_t users, size_t 
     return fail_with(e);
   }
 }
+
+// The reference's data-parallel trainer (trainer.hpp:197-261) on a given
+// train split: RecModel::init(users, items, dim, seed), then `steps` steps of
+// `mode` (0 sync, 1 async); returns the final flat theta and the loss curve
+// (step, loss) every 100 steps (curve_out: 2 doubles per point, up to cap).
+extern "C" int ref_train(size_t users, size_t items, size_t dim, const uint64_t* tu, const uint64_t* ti, size_t ntrain,
+                         size_t P, int mode, size_t steps, size_t batch, double lr, int kind, size_t k, int algo,
+                         uint64_t seed, double* theta_out, double* curve_out, size_t curve_cap, size_t* curve_n) {
+  try {
+    ChronoSplit split;
+    for (size_t i = 0; i < ntrain; ++i) split.train.push_back({tu[i], ti[i], (std::int64_t)i});
+    StrategyConfig cfg;
+    cfg.data_degree = P;
+    cfg.mode = mode ? ExecutionMode::async : ExecutionMode::sync;
+    cfg.collective = make_algo(algo);
+    cfg.compressor = make_cfg(kind, k);
+    HyperParams h;
+    h.learning_rate = lr;
+    h.batch_size = batch;
+    h.steps = steps;
+    TrainResult r = train(RecModel::init(users, items, dim, seed), split, cfg, h, seed);
+    const DenseVector th = flatten_params(r.model);
+    std::memcpy(theta_out, th.data(), th.size() * sizeof(double));
+    size_t m = 0;
+    for (const auto& pt : r.loss_curve) {
+      if (m >= curve_cap) break;
+      curve_out[2 * m] = (double)pt.first;
+      curve_out[2 * m + 1] = pt.second;
+      ++m;
+    }
+    *curve_n = m;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
+}

@@ -1,0 +1,184 @@
+"""Data-parallel trainer around the device path.
+
+Mirrors parsim/trainer.hpp:197-261 (`train`, sync and async branches) for the
+reference's BPR matrix-factorisation recommender, with every gradient and
+update on the B200:
+
+  * RecModel::init (trainer.hpp:28-38) and TripleSampler (:143-179) are the
+    reference's host-side draws (SplitMix64 stream, rejection-sampled
+    negatives), restated here so the triple stream is identical;
+  * per step each of the P workers' contiguous batch shards gets its gradient
+    from psb_bpr_gradient (device) and the step is psb_sync_step (EF
+    compression + the reference fold order + SGD, all device kernels);
+  * async: worker p computes its gradient on the parameters from
+    tau = min(updates, p mod 4) updates ago (a device history ring of 3),
+    compresses with error feedback and applies eta/(1+tau) (psb_ef_topk /
+    psb_ef_onebit + the reference-order apply).
+
+Host work per step is the sampler and launch orchestration only.
+"""
+from __future__ import annotations
+
+from collections import deque
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import torch
+
+from . import _lib as L
+from .engine import Context
+
+
+class SeededRng:
+    """SplitMix64 (parsim/numerics.hpp:152-178), bit-exact."""
+
+    M = (1 << 64) - 1
+
+    def __init__(self, seed: int):
+        self.s = seed & self.M
+
+    def next_u64(self) -> int:
+        self.s = (self.s + 0x9E3779B97F4A7C15) & self.M
+        z = self.s
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & self.M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & self.M
+        return z ^ (z >> 31)
+
+    def next_double(self) -> float:
+        return float(self.next_u64() >> 11) * 2.0 ** -53
+
+    def uniform(self, lo: float, hi: float) -> float:
+        return lo + (hi - lo) * self.next_double()
+
+    def next_below(self, n: int) -> int:
+        if n <= 0:
+            raise L.PsbInvalidArgument("next_below: n must be positive")
+        return self.next_u64() % n
+
+
+def init_params(users: int, items: int, dim: int, seed: int) -> torch.Tensor:
+    """RecModel::init (trainer.hpp:28-38) flattened (user rows, then item rows), f64 CUDA."""
+    if users < 1 or items < 1 or dim < 1:
+        raise L.PsbInvalidArgument("RecModel: sizes must be >= 1")
+    rng = SeededRng(seed)
+    vals = [rng.uniform(-0.01, 0.01) for _ in range((users + items) * dim)]
+    return torch.tensor(vals, dtype=torch.float64, device="cuda")
+
+
+class TripleSampler:
+    """TripleSampler (trainer.hpp:143-179): positives uniform over the train
+    records, one negative per positive rejected against the user's positives
+    (up to 100 tries, else the positive itself)."""
+
+    def __init__(self, train_users: Sequence[int], train_items: Sequence[int], num_users: int, num_items: int,
+                 seed: int):
+        if len(train_users) == 0:
+            raise L.PsbInvalidArgument("TripleSampler: empty train split")
+        self.users = list(int(u) for u in train_users)
+        self.items = list(int(i) for i in train_items)
+        self.num_items = num_items
+        self.rng = SeededRng(seed)
+        self.pos = [set() for _ in range(num_users)]
+        for u, i in zip(self.users, self.items):
+            self.pos[u].add(i)
+
+    def next(self) -> Tuple[int, int, int]:
+        j = self.rng.next_below(len(self.users))
+        u, i = self.users[j], self.items[j]
+        neg = i
+        for _ in range(100):
+            cand = self.rng.next_below(self.num_items)
+            if cand not in self.pos[u]:
+                neg = cand
+                break
+        return u, i, neg
+
+    def next_batch(self, n: int) -> List[Tuple[int, int, int]]:
+        return [self.next() for _ in range(n)]
+
+
+@dataclass
+class TrainResult:
+    theta: torch.Tensor
+    loss_curve: List[Tuple[int, float]] = field(default_factory=list)
+
+
+_COMP = {"none": L.PSB_COMP_NONE, "onebit": L.PSB_COMP_ONEBIT, "topk": L.PSB_COMP_TOPK}
+
+
+def train(users: int, items: int, dim: int, train_users: Sequence[int], train_items: Sequence[int], P: int,
+          steps: int, batch_size: int, lr: float, compressor: str = "none", top_k: int = 0,
+          algo: str = "ring", mode: str = "sync", seed: int = 42,
+          ctx: Optional[Context] = None) -> TrainResult:
+    """parsim train() (trainer.hpp:197-261) with the gradients and updates on the device (f64)."""
+    if lr <= 0.0:
+        raise L.PsbInvalidArgument("HyperParams: learning_rate must be > 0")
+    if batch_size < P:
+        raise L.PsbInvalidArgument("train: batch_size must be >= data_degree")
+    n = (users + items) * dim
+    theta = init_params(users, items, dim, seed)
+    sampler = TripleSampler(train_users, train_items, users, items, seed)
+    own = ctx is None
+    if own:
+        ctx = Context(n, max(top_k, 1), max(P, 1))
+    compressed = compressor != "none"
+    res = torch.zeros(P, n, dtype=torch.float64, device="cuda")
+    grads = torch.empty(P, n, dtype=torch.float64, device="cuda")
+    history: deque = deque()
+    updates = 0
+    out = TrainResult(theta)
+
+    def shard(p: int) -> Tuple[int, int]:
+        base, rem = batch_size // P, batch_size % P
+        lo = p * base + min(p, rem)
+        return lo, lo + base + (1 if p < rem else 0)
+
+    def dev(triples):
+        u = torch.tensor([t[0] for t in triples], dtype=torch.int32, device="cuda")
+        ip = torch.tensor([t[1] for t in triples], dtype=torch.int32, device="cuda")
+        ineg = torch.tensor([t[2] for t in triples], dtype=torch.int32, device="cuda")
+        return u, ip, ineg
+
+    try:
+        for step in range(steps):
+            batch = sampler.next_batch(batch_size)
+            if step % 100 == 0:
+                scratch = torch.empty_like(theta)
+                _, loss = ctx.bpr_gradient(theta, users, items, dim, *dev(batch), grad=scratch)
+                out.loss_curve.append((step, float(loss.item())))
+            if mode == "sync":
+                for p in range(P):
+                    lo, hi = shard(p)
+                    ctx.bpr_gradient(theta, users, items, dim, *dev(batch[lo:hi]), grad=grads[p], want_loss=False)
+                d = ctx.step_desc(_COMP[compressor], grads, res if compressed else None, theta, lr, top_k, algo)
+                ctx.sync_step(d)
+            else:
+                for p in range(P):
+                    tau = min(updates, p % 4)
+                    snap = theta if tau == 0 else history[len(history) - tau]
+                    lo, hi = shard(p)
+                    g = grads[p]
+                    ctx.bpr_gradient(snap, users, items, dim, *dev(batch[lo:hi]), grad=g, want_loss=False)
+                    if compressed:  # ef_compress_step then decompress (trainer.hpp:248)
+                        if compressor == "topk":
+                            idx, val = ctx.ef_topk(g, res[p], top_k)
+                            g = ctx.decompress_topk(idx, val, n)
+                        else:
+                            words, scale = ctx.ef_onebit(g, res[p])
+                            bits = (words.view(torch.uint8).unsqueeze(1) >> torch.arange(
+                                8, device="cuda", dtype=torch.uint8)) & 1
+                            pos = bits.reshape(-1)[:n].bool()
+                            s = scale.to(torch.float64)
+                            g = torch.where(pos, s, -s)
+                    history.append(theta.clone())
+                    if len(history) > 3:
+                        history.popleft()
+                    # async_step: theta - eta/(1+tau) * g  (strategies.hpp:125-129)
+                    scale = lr / (1.0 + float(tau))
+                    ctx.dense_mean_sgd(g.unsqueeze(0), "naive", scale, theta)
+                    updates += 1
+        ctx.check()
+    finally:
+        if own:
+            ctx.close()
+    return out

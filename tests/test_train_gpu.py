@@ -1,0 +1,36 @@
+"""The trainer around the device path against the
+reference's own train() (parsim/trainer.hpp:197-261, via oracle/_ref): same
+RecModel init, same triple stream, gradients and updates on the B200.
+Tolerance: the device exp() may differ from glibc's by an ulp per triple."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2506_17551_b200 import train as T
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")]
+
+
+def test_sampler_and_init_match_reference_stream():
+    """The host draws are the reference's: RecModel::init values and the
+    SplitMix64 KAT (test_numerics.cpp:66-77 seed 0)."""
+    rng = T.SeededRng(0)
+    ref = np.empty(4, dtype=np.uint64)
+    O.ref().ref_splitmix_stream(0, 4, ref.ctypes.data)
+    assert [rng.next_u64() for _ in range(4)] == [int(x) for x in ref]
+
+
+@pytest.mark.parametrize("mode,kind,k,P", [("sync", "none", 0, 2), ("sync", "topk", 30, 2), ("sync", "topk", 30, 4),
+                                           ("async", "topk", 30, 4), ("async", "none", 0, 2)])
+def test_train_matches_reference(mode, kind, k, P):
+    users, items, dim, steps, batch, lr, seed = 30, 50, 8, 120, 32, 0.05, 7
+    rng = np.random.default_rng(1)
+    tu = rng.integers(0, users, 300)
+    ti = rng.integers(0, items, 300)
+    theta_ref, curve_ref = O.ref_train(users, items, dim, tu, ti, P, mode, steps, batch, lr, kind, k, "ring", seed)
+    out = T.train(users, items, dim, tu, ti, P, steps, batch, lr, kind, k, "ring", mode, seed)
+    got = out.theta.cpu().numpy()
+    np.testing.assert_allclose(got, theta_ref, rtol=1e-9, atol=1e-13)
+    assert [s for s, _ in out.loss_curve] == [s for s, _ in curve_ref]
+    for (_, a), (_, b) in zip(out.loss_curve, curve_ref):
+        assert a == pytest.approx(b, rel=1e-12)
