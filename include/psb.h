@@ -184,6 +184,14 @@ PSB_API psb_status psb_bpr_gradient(psb_ctx* ctx, psb_dtype dt, const void* thet
                             uint32_t dim, const uint32_t* user, const uint32_t* pos, const uint32_t* neg,
                             uint32_t B, void* grad, double* loss_out, psb_stream_t stream);
 
+/* Sampled ranking of evaluate_topk (trainer.hpp:269-324): for each of R test
+ * records (user, true item) and its ncand candidate items (u32, 0xffffffff =
+ * padding), rank = 1 + #{c : s(c) > s(true) or (s(c) == s(true) and c < true)}
+ * with the reference's sequential f64 dot-product scores (bit-exact). */
+PSB_API psb_status psb_rank_candidates(psb_ctx* ctx, psb_dtype dt, const void* theta, uint32_t users, uint32_t dim,
+                               uint32_t R, const uint32_t* rec_user, const uint32_t* rec_item,
+                               const uint32_t* cands, uint32_t ncand, uint32_t* rank_out, psb_stream_t stream);
+
 /* ---------------------------------------------------------- generator
  * Counter-based synthetic gradients, identical bits to
  * oracle/psb_oracle.c:orc_generate.  Input generation only. */

@@ -107,6 +107,7 @@ def ref() -> ctypes.CDLL:
             "ref_wire_decode_topk": (ctypes.c_longlong, [_P, _SZ, _P, _P, _P]),
             "ref_wire_encode_onebit": (_SZ, [_P, _SZ, _P]),
             "ref_bpr_batch_gradient": (_I, [_P, _SZ, _SZ, _SZ, _P, _P, _P, _SZ, _P, _P]),
+            "ref_evaluate_topk": (_I, [_SZ, _SZ, _SZ, _P, _P, _P, _SZ, _P, _P, _SZ, _P, _P, _SZ, _SZ, _SZ, _U64, _P]),
             "ref_train": (_I, [_SZ, _SZ, _SZ, _P, _P, _SZ, _SZ, _I, _SZ, _SZ, _D, _I, _SZ, _I, _U64, _P, _P, _SZ, _P]),
         }
         for k, (res, args) in sig.items():
@@ -403,6 +404,17 @@ def ref_train(users: int, items: int, dim: int, train_u: np.ndarray, train_i: np
                             {"naive": 0, "ring": 1, "hierarchical": 2}[algo], seed, _p(theta), _p(curve), cap, _p(cn)))
     m = int(cn[0])
     return theta, [(int(curve[2 * j]), float(curve[2 * j + 1])) for j in range(m)]
+
+
+def ref_evaluate_topk(users, items, dim, theta, train, val, test, K=10, negatives=99, seed=42):
+    """The reference's evaluate_topk (trainer.hpp:269-324): (hr, ndcg, evaluated, skipped)."""
+    th = np.ascontiguousarray(theta, dtype=np.float64)
+    arrs = [np.ascontiguousarray(a, dtype=np.uint64) for part in (train, val, test) for a in part]
+    out = np.zeros(4, dtype=np.float64)
+    _ref_ck(ref().ref_evaluate_topk(users, items, dim, _p(th), _p(arrs[0]), _p(arrs[1]), arrs[0].size, _p(arrs[2]),
+                                    _p(arrs[3]), arrs[2].size, _p(arrs[4]), _p(arrs[5]), arrs[4].size, K, negatives,
+                                    seed, _p(out)))
+    return float(out[0]), float(out[1]), int(out[2]), int(out[3])
 
 
 # ---------------------------------------------------------------- reference

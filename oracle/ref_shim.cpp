@@ -375,3 +375,26 @@ extern "C" int ref_train(size_t users, size_t items, size_t dim, const uint64_t*
     return fail_with(e);
   }
 }
+
+// evaluate_topk (trainer.hpp:269-324) of a flat theta on given splits.
+extern "C" int ref_evaluate_topk(size_t users, size_t items, size_t dim, const double* theta, const uint64_t* tu,
+                                 const uint64_t* ti, size_t ntrain, const uint64_t* vu, const uint64_t* vi, size_t nval,
+                                 const uint64_t* su, const uint64_t* si, size_t ntest, size_t K, size_t negatives,
+                                 uint64_t seed, double* out4) {
+  try {
+    RecModel m = RecModel::init(users, items, dim, 1);
+    unflatten_params(DenseVector(theta, theta + (users + items) * dim), m);
+    ChronoSplit split;
+    for (size_t i = 0; i < ntrain; ++i) split.train.push_back({tu[i], ti[i], (std::int64_t)i});
+    for (size_t i = 0; i < nval; ++i) split.validation.push_back({vu[i], vi[i], (std::int64_t)i});
+    for (size_t i = 0; i < ntest; ++i) split.test.push_back({su[i], si[i], (std::int64_t)i});
+    const EvalResult r = evaluate_topk(m, split, K, negatives, seed);
+    out4[0] = r.hr_at_10;
+    out4[1] = r.ndcg_at_10;
+    out4[2] = (double)r.num_eval_users;
+    out4[3] = (double)r.skipped;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
+}

@@ -104,6 +104,7 @@ _SIGS = {
     "psb_wire_bytes": (_sz, [_i, _u64, _sz]),
     "psb_momentum_sgd": (_i, [_vp, _i, _vp, _vp, _vp, _d, _d, _sz, _vp]),
     "psb_bpr_gradient": (_i, [_vp, _i, _vp, _u32, _u32, _u32, _vp, _vp, _vp, _u32, _vp, _vp, _vp]),
+    "psb_rank_candidates": (_i, [_vp, _i, _vp, _u32, _u32, _u32, _vp, _vp, _vp, _u32, _vp, _vp]),
     "psb_wire_encode_topk": (_i, [_vp, _i, _u64, _vp, _vp, _sz, _vp, _vp]),
     "psb_wire_decode_topk": (_i, [_vp, _i, _vp, _sz, _sz, _vp, _vp, ctypes.POINTER(_u64), ctypes.POINTER(_sz),
                                   _vp]),

@@ -164,3 +164,60 @@ extern "C" psb_status psb_bpr_gradient(psb_ctx* c, psb_dtype dt, const void* the
   PSB_LAUNCH_CHECK(c, "psb_bpr_gradient");
   return PSB_OK;
 }
+
+// ------------------------------------------------- sampled ranking (HR/NDCG)
+namespace {
+// One warp per test record: rank = 1 + #{candidates c : s(c) > s(true) or
+// (s(c) == s(true) and c < true item)} (trainer.hpp:307-312); scores are the
+// reference's sequential f64 dot products (RecModel::score, :40-47).
+template <class T>
+__global__ void k_rank_candidates(const T* __restrict__ theta, uint32_t users, uint32_t dim, uint32_t R,
+                                  const uint32_t* __restrict__ ru, const uint32_t* __restrict__ ri,
+                                  const uint32_t* __restrict__ cands, uint32_t ncand, uint32_t* __restrict__ rank) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  auto score = [&](uint32_t u, uint32_t item) {
+    const T* ur = theta + (size_t)u * dim;
+    const T* ir = theta + ((size_t)users + item) * dim;
+    double s = 0.0;
+    for (uint32_t k = 0; k < dim; ++k) s = __dadd_rn(s, __dmul_rn((double)ur[k], (double)ir[k]));
+    return s;
+  };
+  for (uint32_t r = warp; r < R; r += nwarps) {
+    const uint32_t u = ru[r], it = ri[r];
+    const double ts = score(u, it);
+    uint32_t cnt = 0;
+    for (uint32_t j = lane; j < ncand; j += 32) {
+      const uint32_t c = cands[(size_t)r * ncand + j];
+      if (c == 0xffffffffu) continue;  // padding
+      const double s = score(u, c);
+      cnt += (s > ts || (s == ts && c < it)) ? 1u : 0u;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) rank[r] = 1 + cnt;
+  }
+}
+}  // namespace
+
+extern "C" psb_status psb_rank_candidates(psb_ctx* c, psb_dtype dt, const void* theta, uint32_t users, uint32_t dim,
+                                          uint32_t R, const uint32_t* rec_user, const uint32_t* rec_item,
+                                          const uint32_t* cands, uint32_t ncand, uint32_t* rank_out,
+                                          psb_stream_t stream) {
+  PSB_REQUIRE(c, c != nullptr, "null ctx");
+  PSB_REQUIRE(c, dt == PSB_F32 || dt == PSB_F64, "evaluate_topk: bad dtype");
+  PSB_REQUIRE(c, R >= 1, "evaluate_topk: empty test split");
+  PSB_REQUIRE(c, theta && rec_user && rec_item && rank_out && (ncand == 0 || cands), "evaluate_topk: null buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)std::max<uint32_t>(1, std::min<uint32_t>((R + 7) / 8, c->num_sms * 16));
+  if (dt == PSB_F64)
+    k_rank_candidates<double><<<grid, 256, 0, st>>>((const double*)theta, users, dim, R, rec_user, rec_item, cands,
+                                                    ncand, rank_out);
+  else
+    k_rank_candidates<float><<<grid, 256, 0, st>>>((const float*)theta, users, dim, R, rec_user, rec_item, cands,
+                                                   ncand, rank_out);
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "psb_rank_candidates");
+  return PSB_OK;
+}

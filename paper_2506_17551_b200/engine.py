@@ -235,6 +235,18 @@ class Context:
                                            _ptr(loss), self.stream()), "bpr_batch_gradient")
         return grad, loss
 
+    def rank_candidates(self, theta: torch.Tensor, users: int, dim: int, rec_user: torch.Tensor,
+                        rec_item: torch.Tensor, cands: torch.Tensor) -> torch.Tensor:
+        """evaluate_topk's sampled ranks (trainer.hpp:307-312); cands [R][m] int32 (-1 = padding)."""
+        _need_cuda(theta, rec_user, rec_item, cands)
+        R = rec_user.numel()
+        rank = torch.empty(R, dtype=torch.int32, device=theta.device)
+        self._ck(self.lib.psb_rank_candidates(self.h, _dtype_code(theta), theta.data_ptr(), users, dim, R,
+                                              rec_user.data_ptr(), rec_item.data_ptr(), cands.data_ptr(),
+                                              cands.shape[1] if cands.dim() == 2 else 0, rank.data_ptr(),
+                                              self.stream()), "evaluate_topk")
+        return rank
+
     # ---------------------------------------------------------- wire format
     def wire_encode_topk(self, dim: int, idx: torch.Tensor, val: torch.Tensor) -> torch.Tensor:
         """parsim wire_encode(TopKPayload): u64 dim | u64 count | (u64 idx, f64 val) x count."""

@@ -182,3 +182,85 @@ def train(users: int, items: int, dim: int, train_users: Sequence[int], train_it
         if own:
             ctx.close()
     return out
+
+
+def mix64(z: int) -> int:
+    """parsim/numerics.hpp:181-186."""
+    M = (1 << 64) - 1
+    z = (z + 0x9E3779B97F4A7C15) & M
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+    return z ^ (z >> 31)
+
+
+@dataclass
+class EvalResult:
+    hr_at_10: float
+    ndcg_at_10: float
+    num_eval_users: int
+    skipped: int
+
+
+def evaluate_topk(theta: torch.Tensor, users: int, items: int, dim: int, train: Tuple[Sequence[int], Sequence[int]],
+                  validation: Tuple[Sequence[int], Sequence[int]], test: Tuple[Sequence[int], Sequence[int]],
+                  K: int = 10, negatives: int = 99, seed: int = 42, ctx: Optional[Context] = None) -> EvalResult:
+    """evaluate_topk (trainer.hpp:269-324): the per-record negatives are the
+    reference's host draws (SeededRng(seed ^ mix64(rec_idx)), rejection against
+    everything the user interacted with, deterministic fallback); the scores
+    and ranks of all records are one device launch (psb_rank_candidates)."""
+    import math
+    tu, ti = test
+    if len(tu) == 0:
+        raise L.PsbInvalidArgument("evaluate_topk: empty test split")
+    if K < 1 or negatives < 1:
+        raise L.PsbInvalidArgument("evaluate_topk: K and negatives must be >= 1")
+    seen = [set() for _ in range(users)]
+    for us, its in (train, validation, test):
+        for u, i in zip(us, its):
+            seen[int(u)].add(int(i))
+    rec_u, rec_i, cands, skipped = [], [], [], 0
+    for rec_idx, (u, it) in enumerate(zip(tu, ti)):
+        u, it = int(u), int(it)
+        s = seen[u]
+        available = items - len(s)
+        if available == 0:
+            skipped += 1
+            continue
+        rng = SeededRng(seed ^ mix64(rec_idx))
+        want = min(negatives, available)
+        negs, attempts, cap = set(), 0, 100 * (negatives + 1)
+        while len(negs) < want and attempts < cap:
+            attempts += 1
+            c = rng.next_below(items)
+            if c in s or c == it:
+                continue
+            negs.add(c)
+        if len(negs) < want:
+            for c in range(items):
+                if len(negs) >= want:
+                    break
+                if c not in s and c != it:
+                    negs.add(c)
+        rec_u.append(u)
+        rec_i.append(it)
+        cands.append(sorted(negs) + [-1] * (negatives - len(negs)))
+    if not rec_u:
+        raise L.PsbInvalidArgument("evaluate_topk: all test records were skipped")
+    own = ctx is None
+    if own:
+        ctx = Context(max(theta.numel(), 1), 1, 1)
+    try:
+        ranks = ctx.rank_candidates(theta, users, dim, torch.tensor(rec_u, dtype=torch.int32, device="cuda"),
+                                    torch.tensor(rec_i, dtype=torch.int32, device="cuda"),
+                                    torch.tensor(cands, dtype=torch.int32, device="cuda")).cpu().tolist()
+        ctx.check()
+    finally:
+        if own:
+            ctx.close()
+    hits, ndcg = 0, 0.0
+    for r in ranks:
+        if r <= K:
+            hits += 1
+            ndcg += 1.0 / math.log2(float(r) + 1.0)
+    n = len(ranks)
+    return EvalResult(hits / n, ndcg / n, n, skipped)

@@ -34,3 +34,21 @@ def test_train_matches_reference(mode, kind, k, P):
     assert [s for s, _ in out.loss_curve] == [s for s, _ in curve_ref]
     for (_, a), (_, b) in zip(out.loss_curve, curve_ref):
         assert a == pytest.approx(b, rel=1e-12)
+
+
+@pytest.mark.parametrize("items,negatives", [(50, 20), (12, 99)])
+def test_evaluate_topk_matches_reference(items, negatives):
+    """Sampled HR@10 / NDCG@10 (trainer.hpp:269-324) on a trained model,
+    bit-exact against the reference (incl. the small-pool fallback and
+    skipped users)."""
+    users, dim, seed = 30, 8, 7
+    rng = np.random.default_rng(5)
+    tu, ti = rng.integers(0, users, 300), rng.integers(0, items, 300)
+    vu, vi = rng.integers(0, users, 40), rng.integers(0, items, 40)
+    su, si = rng.integers(0, users, 60), rng.integers(0, items, 60)
+    out = T.train(users, items, dim, tu, ti, 2, 60, 32, 0.05, "topk", 30, "ring", "sync", seed)
+    hr, ndcg, ne, sk = O.ref_evaluate_topk(users, items, dim, out.theta.cpu().numpy(), (tu, ti), (vu, vi), (su, si),
+                                           10, negatives, 42)
+    r = T.evaluate_topk(out.theta, users, items, dim, (tu, ti), (vu, vi), (su, si), 10, negatives, 42)
+    assert (r.num_eval_users, r.skipped) == (ne, sk)
+    assert r.hr_at_10 == hr and r.ndcg_at_10 == ndcg
