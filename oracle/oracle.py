@@ -108,7 +108,9 @@ def ref() -> ctypes.CDLL:
             "ref_wire_encode_onebit": (_SZ, [_P, _SZ, _P]),
             "ref_bpr_batch_gradient": (_I, [_P, _SZ, _SZ, _SZ, _P, _P, _P, _SZ, _P, _P]),
             "ref_evaluate_topk": (_I, [_SZ, _SZ, _SZ, _P, _P, _P, _SZ, _P, _P, _SZ, _P, _P, _SZ, _SZ, _SZ, _U64, _P]),
-            "ref_train": (_I, [_SZ, _SZ, _SZ, _P, _P, _SZ, _SZ, _I, _SZ, _SZ, _D, _I, _SZ, _I, _U64, _P, _P, _SZ, _P]),
+            "ref_synthetic_split": (_I, [_SZ, _SZ, _SZ, _U64, _P, _P, _P, _P, _P, _P, _P]),
+            "ref_train": (_I, [_SZ, _SZ, _SZ, _P, _P, _SZ, _SZ, _I, _SZ, _SZ, _D, _I, _SZ, _I, _U64, _U64, _P, _P, _SZ,
+                               _P]),
         }
         for k, (res, args) in sig.items():
             f = getattr(lib, k)
@@ -391,7 +393,7 @@ def ref_bpr_batch_gradient(theta: np.ndarray, users: int, items: int, dim: int, 
 
 
 def ref_train(users: int, items: int, dim: int, train_u: np.ndarray, train_i: np.ndarray, P: int, mode: str,
-              steps: int, batch: int, lr: float, kind: str, k: int, algo: str, seed: int):
+              steps: int, batch: int, lr: float, kind: str, k: int, algo: str, seed: int, init_seed=None):
     """The reference trainer (trainer.hpp:197-261): final flat theta and loss curve."""
     tu = np.ascontiguousarray(train_u, dtype=np.uint64)
     ti = np.ascontiguousarray(train_i, dtype=np.uint64)
@@ -401,9 +403,19 @@ def ref_train(users: int, items: int, dim: int, train_u: np.ndarray, train_i: np
     cn = np.zeros(1, dtype=np.uint64)
     _ref_ck(ref().ref_train(users, items, dim, _p(tu), _p(ti), tu.size, P, 0 if mode == "sync" else 1, steps, batch,
                             lr, {"none": 0, "onebit": 1, "topk": 2}[kind], k,
-                            {"naive": 0, "ring": 1, "hierarchical": 2}[algo], seed, _p(theta), _p(curve), cap, _p(cn)))
+                            {"naive": 0, "ring": 1, "hierarchical": 2}[algo], seed,
+                            seed if init_seed is None else init_seed, _p(theta), _p(curve), cap, _p(cn)))
     m = int(cn[0])
     return theta, [(int(curve[2 * j]), float(curve[2 * j + 1])) for j in range(m)]
+
+
+def ref_synthetic_split(users: int, items: int, interactions: int, seed: int):
+    """The reference's generate_synthetic + chrono_split: ((tu, ti), (vu, vi), (su, si))."""
+    bufs = [np.zeros(interactions, dtype=np.uint64) for _ in range(6)]
+    n3 = np.zeros(3, dtype=np.uint64)
+    _ref_ck(ref().ref_synthetic_split(users, items, interactions, seed, *[_p(b) for b in bufs], _p(n3)))
+    a, b, c = (int(x) for x in n3)
+    return (bufs[0][:a], bufs[1][:a]), (bufs[2][:b], bufs[3][:b]), (bufs[4][:c], bufs[5][:c])
 
 
 def ref_evaluate_topk(users, items, dim, theta, train, val, test, K=10, negatives=99, seed=42):

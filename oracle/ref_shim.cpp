@@ -346,7 +346,8 @@ extern "C" int ref_bpr_batch_gradient(const double* theta, size_t users, size_t 
 // (step, loss) every 100 steps (curve_out: 2 doubles per point, up to cap).
 extern "C" int ref_train(size_t users, size_t items, size_t dim, const uint64_t* tu, const uint64_t* ti, size_t ntrain,
                          size_t P, int mode, size_t steps, size_t batch, double lr, int kind, size_t k, int algo,
-                         uint64_t seed, double* theta_out, double* curve_out, size_t curve_cap, size_t* curve_n) {
+                         uint64_t seed, uint64_t init_seed, double* theta_out, double* curve_out, size_t curve_cap,
+                         size_t* curve_n) {
   try {
     ChronoSplit split;
     for (size_t i = 0; i < ntrain; ++i) split.train.push_back({tu[i], ti[i], (std::int64_t)i});
@@ -359,7 +360,7 @@ extern "C" int ref_train(size_t users, size_t items, size_t dim, const uint64_t*
     h.learning_rate = lr;
     h.batch_size = batch;
     h.steps = steps;
-    TrainResult r = train(RecModel::init(users, items, dim, seed), split, cfg, h, seed);
+    TrainResult r = train(RecModel::init(users, items, dim, init_seed), split, cfg, h, seed);
     const DenseVector th = flatten_params(r.model);
     std::memcpy(theta_out, th.data(), th.size() * sizeof(double));
     size_t m = 0;
@@ -393,6 +394,30 @@ extern "C" int ref_evaluate_topk(size_t users, size_t items, size_t dim, const d
     out4[1] = r.ndcg_at_10;
     out4[2] = (double)r.num_eval_users;
     out4[3] = (double)r.skipped;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
+}
+
+// generate_synthetic + chrono_split (dataset.hpp:115-176): the split's
+// (user, item) columns; sizes in n3[3] (train, validation, test).
+extern "C" int ref_synthetic_split(size_t users, size_t items, size_t interactions, uint64_t seed, uint64_t* tu,
+                                   uint64_t* ti, uint64_t* vu, uint64_t* vi, uint64_t* su, uint64_t* si, size_t* n3) {
+  try {
+    const ChronoSplit sp = chrono_split(generate_synthetic(users, items, interactions, seed));
+    auto put = [](const std::vector<Interaction>& v, uint64_t* u, uint64_t* i) {
+      for (size_t j = 0; j < v.size(); ++j) {
+        u[j] = v[j].user;
+        i[j] = v[j].item;
+      }
+    };
+    put(sp.train, tu, ti);
+    put(sp.validation, vu, vi);
+    put(sp.test, su, si);
+    n3[0] = sp.train.size();
+    n3[1] = sp.validation.size();
+    n3[2] = sp.test.size();
     return 0;
   } catch (const std::exception& e) {
     return fail_with(e);

@@ -109,14 +109,16 @@ _COMP = {"none": L.PSB_COMP_NONE, "onebit": L.PSB_COMP_ONEBIT, "topk": L.PSB_COM
 def train(users: int, items: int, dim: int, train_users: Sequence[int], train_items: Sequence[int], P: int,
           steps: int, batch_size: int, lr: float, compressor: str = "none", top_k: int = 0,
           algo: str = "ring", mode: str = "sync", seed: int = 42,
-          ctx: Optional[Context] = None) -> TrainResult:
-    """parsim train() (trainer.hpp:197-261) with the gradients and updates on the device (f64)."""
+          ctx: Optional[Context] = None, init_seed: Optional[int] = None) -> TrainResult:
+    """parsim train() (trainer.hpp:197-261) with the gradients and updates on the
+    device (f64).  init_seed: RecModel::init seed (default: seed, as the tests
+    call it; the reference CLI uses seed for init and seed + 1 for training)."""
     if lr <= 0.0:
         raise L.PsbInvalidArgument("HyperParams: learning_rate must be > 0")
     if batch_size < P:
         raise L.PsbInvalidArgument("train: batch_size must be >= data_degree")
     n = (users + items) * dim
-    theta = init_params(users, items, dim, seed)
+    theta = init_params(users, items, dim, seed if init_seed is None else init_seed)
     sampler = TripleSampler(train_users, train_items, users, items, seed)
     own = ctx is None
     if own:
