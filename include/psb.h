@@ -143,10 +143,13 @@ PSB_API psb_status psb_allgather(psb_ctx* ctx, void* buf, size_t bytes_per_rank,
  *   2 sharded: each rank pulls only the payload entries of its share of the
  *     index space (balanced on the device), folds them into theta and an
  *     update list, then applies the other ranks' lists;
+ *   4 direct: no copy -- the apply reads every peer's payload and offset
+ *     rows in place from its arena over NVLink (measured slower: the apply
+ *     is latency-bound and remote loads lengthen its chains);
  *   0 NCCL all-gather of the payloads, then the full apply.
  * Results are bitwise identical in every mode (1 is the fastest measured on
  * B200: DESIGN.md section 4).  Environment at ctx creation: PSB_NO_PEER=1 -> 0,
- * PSB_SHARD=1 -> 2.  Steps with mean_out never shard. */
+ * PSB_SHARD=1 -> 2, PSB_PEER_MODE=<n> -> n.  Steps with mean_out never shard. */
 PSB_API psb_status psb_peer_mode(psb_ctx* ctx, int mode);
 /* 1 once the peer arenas are mapped. */
 PSB_API int psb_peer_active(const psb_ctx* ctx);

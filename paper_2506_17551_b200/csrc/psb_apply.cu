@@ -30,15 +30,25 @@ struct PayloadView {
   size_t val_off;    // byte offset of values (or int8 codes) inside a block
   size_t scale_off;  // TOPK_Q8: byte offset of the f32 scales
   int q8;
+  // direct multi-rank mode (wpr > 0): worker q's block lives in rank q / wpr's
+  // NVLink-mapped arena at rank_base[q / wpr] + q * block_bytes, its segment
+  // offset rows at rank_base[q / wpr] + tab_off + q * (nseg + 1) words
+  int wpr;
+  size_t tab_off;
+  const uint8_t* rank_base[PSB_MAX_P];
 };
 
+__device__ __forceinline__ const uint8_t* pl_block(const PayloadView& v, int q) {
+  return (v.wpr ? v.rank_base[q / v.wpr] : v.base) + (size_t)q * v.block_bytes;
+}
+
 __device__ __forceinline__ const uint32_t* pl_idx(const PayloadView& v, int q) {
-  return reinterpret_cast<const uint32_t*>(v.base + (size_t)q * v.block_bytes);
+  return reinterpret_cast<const uint32_t*>(pl_block(v, q));
 }
 
 template <class T>
 __device__ __forceinline__ T pl_val(const PayloadView& v, int q, size_t j) {
-  const uint8_t* b = v.base + (size_t)q * v.block_bytes;
+  const uint8_t* b = pl_block(v, q);
   if (v.q8) {
     const int8_t code = reinterpret_cast<const int8_t*>(b + v.val_off)[j];
     const float sc = reinterpret_cast<const float*>(b + v.scale_off)[j >> 7];
@@ -157,7 +167,9 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
     if (threadIdx.x < 32) {
       uint32_t l = 0, cnt = 0;
       if (lane < (uint32_t)P) {
-        const uint32_t* row = seg_off + (size_t)lane * (nseg + 1);
+        const uint32_t* row = v.wpr ? reinterpret_cast<const uint32_t*>(v.rank_base[lane / v.wpr] + v.tab_off) +
+                                          (size_t)lane * (nseg + 1)
+                                    : seg_off + (size_t)lane * (nseg + 1);
         l = row[seg];
         cnt = row[seg + 1] - l;
       }
@@ -408,7 +420,7 @@ __global__ void k_decompress_topk(const uint32_t* __restrict__ idx, const T* __r
 }
 
 PayloadView make_view(psb_compressor c, psb_dtype dt, const void* payloads, size_t k) {
-  PayloadView v;
+  PayloadView v{};
   v.base = reinterpret_cast<const uint8_t*>(payloads);
   v.block_bytes = psb_payload_bytes(c, dt, k);
   v.val_off = psb_align16(k * 4);
@@ -431,8 +443,8 @@ template <class T>
 psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* payloads, size_t k,
                        psb_order order, const psb_topology* topo, double lr,
                        const double* wscale_host, bool async_mode, T* theta, size_t n, T* mean_out,
-                       cudaStream_t st, const uint32_t* tab = nullptr) {
-  PayloadView v = make_view(comp, sizeof(T) == 8 ? PSB_F64 : PSB_F32, payloads, k);
+                       cudaStream_t st, const uint32_t* tab = nullptr, const PayloadView* vdirect = nullptr) {
+  PayloadView v = vdirect ? *vdirect : make_view(comp, sizeof(T) == 8 ? PSB_F64 : PSB_F32, payloads, k);
   uint32_t dpn, npr;
   topo_fields(topo, P, &dpn, &npr);
   const T coef = (T)(-lr);
@@ -512,7 +524,7 @@ psb_status shard_fold_impl(psb_ctx* c, int P, const uint32_t* sidx, const T* sva
                            const uint32_t* range, int seg_shift, psb_order order, const psb_topology* topo,
                            double lr, const double* wscale_host, bool async_mode, T* theta, size_t n,
                            uint32_t* list_idx, T* list_val, uint32_t* list_cnt, cudaStream_t st) {
-  PayloadView v;  // flat view: every worker's slice lives in one (idx, val) array pair
+  PayloadView v{};  // flat view: every worker's slice lives in one (idx, val) array pair
   v.base = reinterpret_cast<const uint8_t*>(sidx);
   v.block_bytes = 0;
   v.val_off = (size_t)(reinterpret_cast<const uint8_t*>(sval) - v.base);
@@ -623,6 +635,24 @@ psb_status psb_sparse_apply_tab(psb_ctx* c, psb_compressor comp, psb_dtype dt, i
                                (double*)mean_out, st, tab);
   return sparse_impl<float>(c, comp, P, payloads, k, order, topo, lr, wscale, async_mode != 0, (float*)theta, n,
                             (float*)mean_out, st, tab);
+}
+
+// Direct multi-rank apply: the P payloads and their offset rows are read in
+// place from every rank's NVLink-mapped arena (no pull copy).
+psb_status psb_sparse_apply_direct(psb_ctx* c, psb_compressor comp, psb_dtype dt, int P, int W,
+                                   const uint8_t* const* rank_region, size_t k, size_t tab_off, psb_order order,
+                                   const psb_topology* topo, double lr, const double* wscale, int async_mode,
+                                   void* theta, size_t n, void* mean_out, cudaStream_t st) {
+  PayloadView v = make_view(comp, dt, rank_region[c->rank], k);
+  v.wpr = W;
+  v.tab_off = tab_off;
+  for (int r = 0; r < c->nranks; ++r) v.rank_base[r] = rank_region[r];
+  const uint32_t* dummy_tab = reinterpret_cast<const uint32_t*>(rank_region[c->rank] + tab_off);
+  if (dt == PSB_F64)
+    return sparse_impl<double>(c, comp, P, nullptr, k, order, topo, lr, wscale, async_mode != 0, (double*)theta, n,
+                               (double*)mean_out, st, dummy_tab, &v);
+  return sparse_impl<float>(c, comp, P, nullptr, k, order, topo, lr, wscale, async_mode != 0, (float*)theta, n,
+                            (float*)mean_out, st, dummy_tab, &v);
 }
 
 psb_status psb_seg_offsets(psb_ctx* c, psb_compressor comp, psb_dtype dt, int nw, const void* payloads, size_t k,

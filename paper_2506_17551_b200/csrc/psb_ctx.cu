@@ -77,6 +77,13 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   if (const char* ns = getenv("PSB_NO_STAGE")) c->no_stage = ns[0] != '0';
   if (const char* np = getenv("PSB_NO_PEER")) c->peer_mode = np[0] == '0';
   if (const char* sh = getenv("PSB_SHARD")) c->shard_mode = sh[0] != '0';
+  if (const char* pm = getenv("PSB_PEER_MODE")) {  // 0 nccl, 1 pull, 2 shard, 3 push, 4 direct
+    const int m = atoi(pm);
+    c->peer_mode = m > 0;
+    c->shard_mode = m == 2;
+    c->push_mode = m == 3;
+    c->direct_mode = m == 4;
+  }
   if (const char* sm = getenv("PSB_STEP_MARKS")) c->marks_on = sm[0] != '0';
   if (const char* sn = getenv("PSB_SCAN_TMA")) c->scan_tma = sn[0] != '0';
   if (const char* qt = getenv("PSB_Q8_NO_TMA")) c->q8_no_tma = qt[0] != '0';
@@ -331,6 +338,7 @@ struct ShardPlan {
   bool on = false;         // sharded apply
   bool tab_ready = false;  // full exchange: every worker's offset rows are in the arena
   bool ack_after_apply = false;  // push mode: acknowledge the peers' payloads once applied
+  bool direct = false;           // direct mode: apply from the peers' arenas in place
   int seg_shift = 0;
   uint32_t nseg = 0;
   size_t blk = 0, tab_off = 0, list_off = 0, list_voff = 0, cap = 0;
@@ -348,6 +356,8 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
   const bool shard = peer && plan != nullptr && c->shard_mode && d->mean_out == nullptr && d->theta && P >= 2;
   // full exchange pushed by K1 itself (top-k values; the q8 payload is finished after K1)
   const bool push = peer && !shard && c->push_mode && d->compressor == PSB_COMP_TOPK && plan != nullptr;
+  // direct: the apply reads every peer's arena in place (no pull copy)
+  const bool direct = peer && !shard && !push && c->direct_mode && plan != nullptr && P >= 2;
   psb_status s;
   uint8_t* gb;
   if (peer) {
@@ -380,6 +390,7 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
       s = psb_peer_wait_ack(c, st);  // peers done with our previous payloads / update list
       if (s) return s;
     }
+    if (direct) plan->direct = true;
     psb_mark(c, st);
   } else {
     s = ensure(c, &c->d_gather, &c->gather_bytes, blk * P, "payload gather buffer");
@@ -438,6 +449,13 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
   } else if (shard) {
     s = psb_peer_signal(c, st);
     if (s) return s;
+    psb_mark(c, st);
+  } else if (direct) {
+    s = psb_peer_signal(c, st);
+    if (s) return s;
+    s = psb_peer_wait_ready(c, st);
+    if (s) return s;
+    plan->ack_after_apply = true;
     psb_mark(c, st);
   } else if (peer) {
     s = psb_peer_exchange(c, (size_t)W * blk, tabs ? plan->tab_off : 0,
@@ -600,7 +618,12 @@ static psb_status sync_step_core(psb_ctx* c, const psb_step_desc* d, psb_stream_
       s = compress_and_gather(c, d, st, &pl, fuse, &sp);
       if (s || fuse) return s;
       if (sp.on) return shard_apply(c, d, sp, nullptr, false, st);
-      if (sp.tab_ready)
+      if (sp.direct) {
+        const uint8_t* regions[PSB_MAX_P];
+        psb_peer_regions(c, regions);
+        s = psb_sparse_apply_direct(c, d->compressor, d->dtype, P, d->workers, regions, d->k, sp.tab_off, d->order,
+                                    &d->topo, d->lr, nullptr, 0, d->theta, d->n, d->mean_out, st);
+      } else if (sp.tab_ready)
         s = psb_sparse_apply_tab(c, d->compressor, d->dtype, P, pl, d->k,
                                  reinterpret_cast<const uint32_t*>(pl + sp.tab_off), d->order, &d->topo, d->lr,
                                  nullptr, 0, d->theta, d->n, d->mean_out, st);
@@ -708,7 +731,13 @@ extern "C" psb_status psb_async_round(psb_ctx* c, const psb_step_desc* d, uint32
     scale[p] = d->lr / (1.0 + (double)tau);  // strategies.hpp:127
   }
   if (sp.on) s = shard_apply(c, d, sp, scale.data(), true, st);
-  else if (sp.tab_ready) {
+  else if (sp.direct) {
+    const uint8_t* regions[PSB_MAX_P];
+    psb_peer_regions(c, regions);
+    s = psb_sparse_apply_direct(c, d->compressor, d->dtype, P, d->workers, regions, d->k, sp.tab_off, PSB_ORDER_NAIVE,
+                                nullptr, 0.0, scale.data(), 1, d->theta, d->n, nullptr, st);
+    if (!s) s = psb_peer_ack(c, st);
+  } else if (sp.tab_ready) {
     s = psb_sparse_apply_tab(c, d->compressor, d->dtype, P, pl, d->k, reinterpret_cast<const uint32_t*>(pl + sp.tab_off),
                              PSB_ORDER_NAIVE, nullptr, 0.0, scale.data(), 1, d->theta, d->n, nullptr, st);
     if (!s && sp.ack_after_apply) s = psb_peer_ack(c, st);

@@ -103,6 +103,7 @@ struct psb_ctx {
   void* peer_base[PSB_MAX_P] = {};  // every rank's arena mapped here (own included)
   int shard_mode = 0;           // sharded multi-rank sparse apply (psb_peer_mode 2 / PSB_SHARD=1)
   int push_mode = 0;            // full exchange: K1 pushes its payload to the peers (psb_peer_mode 3)
+  int direct_mode = 0;          // the apply reads the peers' arenas in place (psb_peer_mode 4)
   // set by the step driver around one worker's K1 call in push mode: the
   // peers' payload-region bases and this worker's slot offset in them
   int push_n = 0;
@@ -130,6 +131,7 @@ psb_status psb_peer_exchange(psb_ctx* c, size_t bytes_per_rank, size_t tab_off, 
                              cudaStream_t st);
 void psb_peer_destroy(psb_ctx* c);
 uint32_t* psb_peer_list_cnt(psb_ctx* c);
+void psb_peer_regions(psb_ctx* c, const uint8_t** out);  // every rank's payload region (mapped)
 psb_status psb_peer_signal(psb_ctx* c, cudaStream_t st);
 psb_status psb_peer_wait_ready(psb_ctx* c, cudaStream_t st);
 psb_status psb_peer_put(psb_ctx* c, size_t off, size_t words, cudaStream_t st);
@@ -149,6 +151,10 @@ psb_status psb_sparse_apply_tab(psb_ctx* c, psb_compressor comp, psb_dtype dt, i
                                 const uint32_t* tab, psb_order order, const psb_topology* topo, double lr,
                                 const double* wscale, int async_mode, void* theta, size_t n, void* mean_out,
                                 cudaStream_t st);
+psb_status psb_sparse_apply_direct(psb_ctx* c, psb_compressor comp, psb_dtype dt, int P, int W,
+                                   const uint8_t* const* rank_region, size_t k, size_t tab_off, psb_order order,
+                                   const psb_topology* topo, double lr, const double* wscale, int async_mode,
+                                   void* theta, size_t n, void* mean_out, cudaStream_t st);
 psb_status psb_shard_fold(psb_ctx* c, psb_dtype dt, int P, const uint32_t* sidx, const void* sval,
                           const uint32_t* srow, const uint32_t* range, int seg_shift, psb_order order,
                           const psb_topology* topo, double lr, const double* wscale, int async_mode, void* theta,

@@ -536,6 +536,10 @@ void psb_peer_push_targets(psb_ctx* c, size_t slot_off) {
   c->push_slot_off = slot_off;
 }
 
+void psb_peer_regions(psb_ctx* c, const uint8_t** out) {
+  for (int p = 0; p < c->nranks; ++p) out[p] = reinterpret_cast<const uint8_t*>(c->peer_base[p]) + kHdrBytes;
+}
+
 uint32_t* psb_peer_list_cnt(psb_ctx* c) { return reinterpret_cast<uint32_t*>(c->peer_arena) + kListCnt; }
 
 psb_status psb_peer_signal(psb_ctx* c, cudaStream_t st) {
@@ -598,10 +602,11 @@ psb_status psb_shard_finish(psb_ctx* c, psb_dtype dt, size_t list_off, size_t li
 
 extern "C" psb_status psb_peer_mode(psb_ctx* c, int mode) {
   PSB_REQUIRE(c, c != nullptr, "null ctx");
-  PSB_REQUIRE(c, mode >= 0 && mode <= 3, "psb_peer_mode: mode must be 0, 1, 2 or 3");
+  PSB_REQUIRE(c, mode >= 0 && mode <= 4, "psb_peer_mode: mode must be 0..4");
   c->peer_mode = mode > 0;
   c->shard_mode = mode == 2;
   c->push_mode = mode == 3;
+  c->direct_mode = mode == 4;
   return PSB_OK;
 }
 

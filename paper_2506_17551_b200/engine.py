@@ -151,7 +151,7 @@ class Context:
         """Multi-rank sparse exchange (psb_peer_mode): "pull" (1, default), "push"
         (3: K1 stores its payload into the peers' NVLink arenas), "shard" (2),
         "nccl" (0)."""
-        m = {"pull": 1, "full": 1, "push": 3, "shard": 2, "nccl": 0, True: 1, False: 0}.get(mode, mode)
+        m = {"pull": 1, "full": 1, "push": 3, "shard": 2, "direct": 4, "nccl": 0, True: 1, False: 0}.get(mode, mode)
         self._ck(self.lib.psb_peer_mode(self.h, int(m)), "psb_peer_mode")
 
     @property

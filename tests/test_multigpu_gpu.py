@@ -122,6 +122,7 @@ def test_exchange_paths_match_oracle(comp, order, W):
     ("async", "naive", 1, "shard", 4), ("topk_q8", "ring", 2, "shard", 4),
     ("topk_grow", "ring", 1, "shard", 6), ("topk_grow", "naive", 2, "pull", 6), ("topk", "ring", 1, "pull", 12),
     ("topk", "ring", 1, "push", 4), ("async", "naive", 2, "push", 4), ("topk_grow", "ring", 2, "push", 6),
+    ("topk", "ring", 1, "direct", 4), ("async_q8", "naive", 2, "direct", 4), ("topk", "hierarchical", 2, "direct", 6),
 ])
 def test_payload_exchange_modes(comp, order, W, peer, steps):
     """NCCL all-gather fallback, the NVLink push and sharded modes, arena
