@@ -108,6 +108,7 @@ def ref() -> ctypes.CDLL:
             "ref_wire_encode_onebit": (_SZ, [_P, _SZ, _P]),
             "ref_bpr_batch_gradient": (_I, [_P, _SZ, _SZ, _SZ, _P, _P, _P, _SZ, _P, _P]),
             "ref_evaluate_topk": (_I, [_SZ, _SZ, _SZ, _P, _P, _P, _SZ, _P, _P, _SZ, _P, _P, _SZ, _SZ, _SZ, _U64, _P]),
+            "ref_load_model": (_I, [ctypes.c_char_p, _P, _P, _SZ]),
             "ref_synthetic_split": (_I, [_SZ, _SZ, _SZ, _U64, _P, _P, _P, _P, _P, _P, _P]),
             "ref_train": (_I, [_SZ, _SZ, _SZ, _P, _P, _SZ, _SZ, _I, _SZ, _SZ, _D, _I, _SZ, _I, _U64, _U64, _P, _P, _SZ,
                                _P]),
@@ -407,6 +408,15 @@ def ref_train(users: int, items: int, dim: int, train_u: np.ndarray, train_i: np
                             seed if init_seed is None else init_seed, _p(theta), _p(curve), cap, _p(cn)))
     m = int(cn[0])
     return theta, [(int(curve[2 * j]), float(curve[2 * j + 1])) for j in range(m)]
+
+
+def ref_load_model(path: str, cap: int):
+    """The reference's load_model: ((users, items, dim), flat theta)."""
+    dims = np.zeros(3, dtype=np.uint64)
+    th = np.zeros(cap, dtype=np.float64)
+    _ref_ck(ref().ref_load_model(path.encode(), _p(dims), _p(th), cap))
+    u, i, d = (int(x) for x in dims)
+    return (u, i, d), th[:(u + i) * d]
 
 
 def ref_synthetic_split(users: int, items: int, interactions: int, seed: int):

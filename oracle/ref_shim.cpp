@@ -423,3 +423,19 @@ extern "C" int ref_synthetic_split(size_t users, size_t items, size_t interactio
     return fail_with(e);
   }
 }
+
+// load_model (trainer.hpp:351-378) of a file: dims into dims3, flat theta out.
+extern "C" int ref_load_model(const char* path, size_t* dims3, double* theta_out, size_t cap) {
+  try {
+    const RecModel m = load_model(path);
+    dims3[0] = m.num_users();
+    dims3[1] = m.num_items();
+    dims3[2] = m.embedding_dim();
+    const DenseVector th = flatten_params(m);
+    if (th.size() > cap) return fail_with(std::invalid_argument("ref_load_model: capacity"));
+    std::memcpy(theta_out, th.data(), th.size() * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
+}

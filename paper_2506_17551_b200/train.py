@@ -101,6 +101,69 @@ class TripleSampler:
 class TrainResult:
     theta: torch.Tensor
     loss_curve: List[Tuple[int, float]] = field(default_factory=list)
+    residuals: Optional[torch.Tensor] = None  # [P][n] error-feedback state at the end
+    sampler_state: int = 0                    # TripleSampler SplitMix64 state at the end
+    steps_done: int = 0
+
+
+# ------------------------------------------------------------ checkpoints
+def save_model(path: str, theta: torch.Tensor, users: int, items: int, dim: int) -> None:
+    """save_model (trainer.hpp:332-349): "PSMF" | u64 users, items, dim | flat f64, little-endian
+    (the reference's load_model reads it)."""
+    import struct
+    flat = theta.detach().to("cpu", torch.float64).contiguous()
+    if flat.numel() != (users + items) * dim:
+        raise L.PsbInvalidArgument("save_model: theta size mismatch")
+    with open(path, "wb") as f:
+        f.write(b"PSMF" + struct.pack("<QQQ", users, items, dim))
+        f.write(flat.numpy().astype("<f8").tobytes())
+
+
+def load_model(path: str) -> Tuple[torch.Tensor, int, int, int]:
+    """load_model (trainer.hpp:351-378): (theta f64 CUDA, users, items, dim)."""
+    import struct
+    import numpy as np
+    with open(path, "rb") as f:
+        data = f.read()
+    if len(data) < 4 or data[:4] != b"PSMF":
+        raise RuntimeError(f"load_model: '{path}' is not a model file")
+    if len(data) < 28:
+        raise RuntimeError(f"load_model: corrupt header in '{path}'")
+    users, items, dim = struct.unpack("<QQQ", data[4:28])
+    if users == 0 or items == 0 or dim == 0:
+        raise RuntimeError(f"load_model: corrupt header in '{path}'")
+    n = (users + items) * dim
+    if len(data) < 28 + 8 * n:
+        raise RuntimeError(f"load_model: truncated '{path}'")
+    theta = torch.from_numpy(np.frombuffer(data, dtype="<f8", count=n, offset=28).astype(np.float64)).cuda()
+    return theta, users, items, dim
+
+
+def save_ef_state(path: str, residuals: torch.Tensor, steps_done: int, sampler_state: int) -> None:
+    """Error-feedback checkpoint (absent in the reference, which saves theta
+    only): "PSEF" | u64 P, n, steps_done, sampler state |
+    P x n f64 residuals, little-endian.  With save_model it resumes exactly."""
+    import struct
+    r = residuals.detach().to("cpu", torch.float64).contiguous()
+    P, n = r.shape
+    with open(path, "wb") as f:
+        f.write(b"PSEF" + struct.pack("<QQQQ", P, n, steps_done, sampler_state & ((1 << 64) - 1)))
+        f.write(r.numpy().astype("<f8").tobytes())
+
+
+def load_ef_state(path: str) -> Tuple[torch.Tensor, int, int]:
+    """(residuals [P][n] f64 CUDA, steps_done, sampler_state)."""
+    import struct
+    import numpy as np
+    with open(path, "rb") as f:
+        data = f.read()
+    if len(data) < 36 or data[:4] != b"PSEF":
+        raise RuntimeError(f"load_ef_state: '{path}' is not an error-feedback checkpoint")
+    P, n, steps_done, st = struct.unpack("<QQQQ", data[4:36])
+    if len(data) < 36 + 8 * P * n:
+        raise RuntimeError(f"load_ef_state: truncated '{path}'")
+    r = torch.from_numpy(np.frombuffer(data, dtype="<f8", count=P * n, offset=36).astype(np.float64)).cuda()
+    return r.view(P, n), steps_done, st
 
 
 _COMP = {"none": L.PSB_COMP_NONE, "onebit": L.PSB_COMP_ONEBIT, "topk": L.PSB_COMP_TOPK}
@@ -109,7 +172,8 @@ _COMP = {"none": L.PSB_COMP_NONE, "onebit": L.PSB_COMP_ONEBIT, "topk": L.PSB_COM
 def train(users: int, items: int, dim: int, train_users: Sequence[int], train_items: Sequence[int], P: int,
           steps: int, batch_size: int, lr: float, compressor: str = "none", top_k: int = 0,
           algo: str = "ring", mode: str = "sync", seed: int = 42,
-          ctx: Optional[Context] = None, init_seed: Optional[int] = None) -> TrainResult:
+          ctx: Optional[Context] = None, init_seed: Optional[int] = None,
+          resume: Optional[Tuple[torch.Tensor, torch.Tensor, int, int]] = None) -> TrainResult:
     """parsim train() (trainer.hpp:197-261) with the gradients and updates on the
     device (f64).  init_seed: RecModel::init seed (default: seed, as the tests
     call it; the reference CLI uses seed for init and seed + 1 for training)."""
@@ -120,11 +184,20 @@ def train(users: int, items: int, dim: int, train_users: Sequence[int], train_it
     n = (users + items) * dim
     theta = init_params(users, items, dim, seed if init_seed is None else init_seed)
     sampler = TripleSampler(train_users, train_items, users, items, seed)
+    start = 0
+    if resume is not None:  # (theta, residuals, steps_done, sampler_state) from the checkpoints
+        theta = resume[0].to(torch.float64).clone()
+        start = int(resume[2])
+        sampler.rng.s = int(resume[3])
     own = ctx is None
     if own:
         ctx = Context(n, max(top_k, 1), max(P, 1))
     compressed = compressor != "none"
     res = torch.zeros(P, n, dtype=torch.float64, device="cuda")
+    if resume is not None:
+        res.copy_(resume[1])
+    if mode != "sync" and resume is not None and start:
+        raise L.PsbInvalidArgument("train: resume is supported for sync training (async history is not saved)")
     grads = torch.empty(P, n, dtype=torch.float64, device="cuda")
     history: deque = deque()
     updates = 0
@@ -142,7 +215,7 @@ def train(users: int, items: int, dim: int, train_users: Sequence[int], train_it
         return u, ip, ineg
 
     try:
-        for step in range(steps):
+        for step in range(start, start + steps):
             batch = sampler.next_batch(batch_size)
             if step % 100 == 0:
                 scratch = torch.empty_like(theta)
@@ -183,6 +256,10 @@ def train(users: int, items: int, dim: int, train_users: Sequence[int], train_it
     finally:
         if own:
             ctx.close()
+    out.theta = theta
+    out.residuals = res
+    out.sampler_state = sampler.rng.s
+    out.steps_done = start + steps
     return out
 
 

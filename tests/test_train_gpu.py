@@ -52,3 +52,26 @@ def test_evaluate_topk_matches_reference(items, negatives):
     r = T.evaluate_topk(out.theta, users, items, dim, (tu, ti), (vu, vi), (su, si), 10, negatives, 42)
     assert (r.num_eval_users, r.skipped) == (ne, sk)
     assert r.hr_at_10 == hr and r.ndcg_at_10 == ndcg
+
+
+def test_checkpoint_resume_is_exact(tmp_path):
+    """save_model (reference PSMF format, read back by the reference's
+    load_model) + the error-feedback checkpoint resume a compressed sync run
+    bit-exactly: 60 + 60 steps == 120 steps."""
+    users, items, dim, batch, lr, seed, P, k = 30, 50, 8, 32, 0.05, 7, 2, 30
+    rng = np.random.default_rng(1)
+    tu, ti = rng.integers(0, users, 300), rng.integers(0, items, 300)
+    full = T.train(users, items, dim, tu, ti, P, 120, batch, lr, "topk", k, "ring", "sync", seed)
+    half = T.train(users, items, dim, tu, ti, P, 60, batch, lr, "topk", k, "ring", "sync", seed)
+    mpath, epath = str(tmp_path / "model.bin"), str(tmp_path / "ef.bin")
+    T.save_model(mpath, half.theta, users, items, dim)
+    T.save_ef_state(epath, half.residuals, half.steps_done, half.sampler_state)
+    (u, i, d), th_ref = O.ref_load_model(mpath, (users + items) * dim)
+    assert (u, i, d) == (users, items, dim)
+    assert np.array_equal(th_ref.view(np.uint64), half.theta.cpu().numpy().view(np.uint64))
+    theta, u2, i2, d2 = T.load_model(mpath)
+    res, done, st = T.load_ef_state(epath)
+    rest = T.train(u2, i2, d2, tu, ti, P, 60, batch, lr, "topk", k, "ring", "sync", seed, resume=(theta, res, done, st))
+    assert np.array_equal(rest.theta.cpu().numpy().view(np.uint64), full.theta.cpu().numpy().view(np.uint64))
+    assert np.array_equal(rest.residuals.cpu().numpy().view(np.uint64), full.residuals.cpu().numpy().view(np.uint64))
+    assert rest.loss_curve == [pt for pt in full.loss_curve if pt[0] >= 60]
