@@ -30,6 +30,7 @@ struct PayloadView {
   size_t val_off;    // byte offset of values (or int8 codes) inside a block
   size_t scale_off;  // TOPK_Q8: byte offset of the f32 scales
   int q8;
+  int idx16;  // indices stored as u16 offsets inside their apply segment (wire16 payloads)
   // direct multi-rank mode (wpr > 0): worker q's block lives in rank q / wpr's
   // NVLink-mapped arena at rank_base[q / wpr] + q * block_bytes, its segment
   // offset rows at rank_base[q / wpr] + tab_off + q * (nseg + 1) words
@@ -231,11 +232,17 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
           const int q = worker_of(e, base);
           const uint32_t rq = e - base;
           const uint32_t j = lo[q] + rq;
-          const uint32_t* idx = pl_idx(v, q);
           qq[u] = q;
           r[u] = rq;
-          il[u] = (uint32_t)(idx[j] - seg_base);
-          ilp[u] = rq ? (uint32_t)(idx[j - 1] - seg_base) : 0xffffffffu;
+          if (v.idx16) {  // wire16: the in-segment offset is stored directly
+            const uint16_t* lo16 = reinterpret_cast<const uint16_t*>(pl_block(v, q));
+            il[u] = lo16[j];
+            ilp[u] = rq ? (uint32_t)lo16[j - 1] : 0xffffffffu;
+          } else {
+            const uint32_t* idx = pl_idx(v, q);
+            il[u] = (uint32_t)(idx[j] - seg_base);
+            ilp[u] = rq ? (uint32_t)(idx[j - 1] - seg_base) : 0xffffffffu;
+          }
           if (staged) val[u] = pl_val<T>(v, q, j);
         }
       }
@@ -635,6 +642,62 @@ psb_status psb_sparse_apply_tab(psb_ctx* c, psb_compressor comp, psb_dtype dt, i
                                (double*)mean_out, st, tab);
   return sparse_impl<float>(c, comp, P, payloads, k, order, topo, lr, wscale, async_mode != 0, (float*)theta, n,
                             (float*)mean_out, st, tab);
+}
+
+// wire16 pack: a standard top-k payload block (u32 idx | val) -> (u16 idx &
+// (S-1) | val) -- the apply segment of S = 2^seg_shift <= 2^16 indices an
+// entry falls in is recovered from the per-segment offset rows.
+namespace {
+template <class T>
+__global__ void k_pack16(const uint32_t* __restrict__ idx, const T* __restrict__ val, size_t k, uint32_t mask,
+                         uint16_t* __restrict__ lo16, T* __restrict__ val16) {
+  for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (size_t)gridDim.x * blockDim.x) {
+    lo16[j] = (uint16_t)(idx[j] & mask);
+    val16[j] = val[j];
+  }
+}
+}  // namespace
+
+size_t psb_wire16_bytes(psb_dtype dt, size_t k) {
+  return psb_align16(2 * k) + psb_align16((dt == PSB_F64 ? 8 : 4) * k);
+}
+
+psb_status psb_pack16(psb_ctx* c, psb_dtype dt, const void* payload, size_t k, int seg_shift, void* out,
+                      cudaStream_t st) {
+  const uint8_t* b = reinterpret_cast<const uint8_t*>(payload);
+  uint8_t* o = reinterpret_cast<uint8_t*>(out);
+  const uint32_t mask = (1u << seg_shift) - 1u;
+  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((k + 255) / 256, (size_t)c->num_sms * 8));
+  if (dt == PSB_F64)
+    k_pack16<double><<<grid, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(b),
+                                           reinterpret_cast<const double*>(b + psb_align16(4 * k)), k, mask,
+                                           reinterpret_cast<uint16_t*>(o),
+                                           reinterpret_cast<double*>(o + psb_align16(2 * k)));
+  else
+    k_pack16<float><<<grid, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(b),
+                                          reinterpret_cast<const float*>(b + psb_align16(4 * k)), k, mask,
+                                          reinterpret_cast<uint16_t*>(o),
+                                          reinterpret_cast<float*>(o + psb_align16(2 * k)));
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "wire16 pack");
+  return PSB_OK;
+}
+
+// P wire16 payloads (blocks of psb_wire16_bytes) + their offset rows -> apply.
+psb_status psb_sparse_apply_wire16(psb_ctx* c, psb_dtype dt, int P, const void* payloads, size_t k,
+                                   const uint32_t* tab, psb_order order, const psb_topology* topo, double lr,
+                                   const double* wscale, int async_mode, void* theta, size_t n, void* mean_out,
+                                   cudaStream_t st) {
+  PayloadView v{};
+  v.base = reinterpret_cast<const uint8_t*>(payloads);
+  v.block_bytes = psb_wire16_bytes(dt, k);
+  v.val_off = psb_align16(2 * k);
+  v.idx16 = 1;
+  if (dt == PSB_F64)
+    return sparse_impl<double>(c, PSB_COMP_TOPK, P, payloads, k, order, topo, lr, wscale, async_mode != 0,
+                               (double*)theta, n, (double*)mean_out, st, tab, &v);
+  return sparse_impl<float>(c, PSB_COMP_TOPK, P, payloads, k, order, topo, lr, wscale, async_mode != 0, (float*)theta,
+                            n, (float*)mean_out, st, tab, &v);
 }
 
 // Direct multi-rank apply: the P payloads and their offset rows are read in

@@ -77,6 +77,7 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   if (const char* ns = getenv("PSB_NO_STAGE")) c->no_stage = ns[0] != '0';
   if (const char* np = getenv("PSB_NO_PEER")) c->peer_mode = np[0] == '0';
   if (const char* sh = getenv("PSB_SHARD")) c->shard_mode = sh[0] != '0';
+  if (const char* nw = getenv("PSB_NO_WIRE16")) c->no_wire16 = nw[0] != '0';
   if (const char* pm = getenv("PSB_PEER_MODE")) {  // 0 nccl, 1 pull, 2 shard, 3 push, 4 direct
     const int m = atoi(pm);
     c->peer_mode = m > 0;
@@ -339,6 +340,7 @@ struct ShardPlan {
   bool tab_ready = false;  // full exchange: every worker's offset rows are in the arena
   bool ack_after_apply = false;  // push mode: acknowledge the peers' payloads once applied
   bool direct = false;           // direct mode: apply from the peers' arenas in place
+  bool wire16 = false;           // the arena holds wire16 payloads (u16 in-segment indices)
   int seg_shift = 0;
   uint32_t nseg = 0;
   size_t blk = 0, tab_off = 0, list_off = 0, list_voff = 0, cap = 0;
@@ -358,11 +360,18 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
   const bool push = peer && !shard && c->push_mode && d->compressor == PSB_COMP_TOPK && plan != nullptr;
   // direct: the apply reads every peer's arena in place (no pull copy)
   const bool direct = peer && !shard && !push && c->direct_mode && plan != nullptr && P >= 2;
+  // pull mode, top-k f32/f64: the arena slots carry wire16 payloads (u16
+  // in-segment index | value: 6 instead of 8 bytes per entry on NVLink);
+  // K1 writes the standard payload into local scratch and k_pack16 converts
+  const bool wire16 = peer && !shard && !push && !direct && plan != nullptr && P >= 2 &&
+                      d->compressor == PSB_COMP_TOPK && !c->no_wire16;
+  const size_t pblk = wire16 ? psb_wire16_bytes(d->dtype, d->k) : blk;  // arena slot stride
   psb_status s;
   uint8_t* gb;
+  uint8_t* kb = nullptr;  // this rank's first K1 output slot (arena, or the wire16 scratch)
   if (peer) {
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    size_t region = al(blk * P);
+    size_t region = al(pblk * P);
     if (plan && P >= 2) {
       // per-segment offset rows of every worker's payload, computed by its
       // producer and exchanged with it (the consumer skips k_seg_offsets)
@@ -392,14 +401,21 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
     }
     if (direct) plan->direct = true;
     psb_mark(c, st);
+    kb = gb + (size_t)c->rank * W * blk;
+    if (wire16) {
+      s = ensure(c, &c->d_gather, &c->gather_bytes, blk * W, "wire16 scratch");
+      if (s) return s;
+      kb = reinterpret_cast<uint8_t*>(c->d_gather);
+    }
   } else {
     s = ensure(c, &c->d_gather, &c->gather_bytes, blk * P, "payload gather buffer");
     if (s) return s;
     gb = reinterpret_cast<uint8_t*>(c->d_gather);
+    kb = gb + (size_t)c->rank * W * blk;
   }
   for (int w = 0; w < W; ++w) {
     const int gid = c->rank * W + w;
-    uint8_t* slot = gb + (size_t)gid * blk;
+    uint8_t* slot = kb + (size_t)w * blk;
     const void* g = reinterpret_cast<const uint8_t*>(d->g) + (size_t)w * d->n * es;
     void* r = d->r ? reinterpret_cast<uint8_t*>(d->r) + (size_t)w * d->n * es : nullptr;
     uint32_t* idx = reinterpret_cast<uint32_t*>(slot);
@@ -428,9 +444,17 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
   if (tabs) {
     const ShardPlan& sp = *plan;
     uint32_t* tab = reinterpret_cast<uint32_t*>(gb + sp.tab_off) + (size_t)c->rank * W * (sp.nseg + 1);
-    s = psb_seg_offsets(c, d->compressor, d->dtype, W, gb + (size_t)c->rank * W * blk, d->k, sp.nseg, sp.seg_shift,
+    s = psb_seg_offsets(c, d->compressor, d->dtype, W, kb, d->k, sp.nseg, sp.seg_shift,
                         tab, st);
     if (s) return s;
+    if (wire16) {
+      for (int w = 0; w < W; ++w) {
+        const int gid = c->rank * W + w;
+        s = psb_pack16(c, d->dtype, kb + (size_t)w * blk, d->k, sp.seg_shift, gb + (size_t)gid * pblk, st);
+        if (s) return s;
+      }
+      plan->wire16 = true;
+    }
     psb_mark(c, st);
   }
   if (push) {
@@ -458,7 +482,7 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
     plan->ack_after_apply = true;
     psb_mark(c, st);
   } else if (peer) {
-    s = psb_peer_exchange(c, (size_t)W * blk, tabs ? plan->tab_off : 0,
+    s = psb_peer_exchange(c, (size_t)W * pblk, tabs ? plan->tab_off : 0,
                           tabs ? (size_t)W * (plan->nseg + 1) : 0, st);
     if (s) return s;
     if (tabs) plan->tab_ready = true;
@@ -623,7 +647,10 @@ static psb_status sync_step_core(psb_ctx* c, const psb_step_desc* d, psb_stream_
         psb_peer_regions(c, regions);
         s = psb_sparse_apply_direct(c, d->compressor, d->dtype, P, d->workers, regions, d->k, sp.tab_off, d->order,
                                     &d->topo, d->lr, nullptr, 0, d->theta, d->n, d->mean_out, st);
-      } else if (sp.tab_ready)
+      } else if (sp.wire16)
+        s = psb_sparse_apply_wire16(c, d->dtype, P, pl, d->k, reinterpret_cast<const uint32_t*>(pl + sp.tab_off),
+                                    d->order, &d->topo, d->lr, nullptr, 0, d->theta, d->n, d->mean_out, st);
+      else if (sp.tab_ready)
         s = psb_sparse_apply_tab(c, d->compressor, d->dtype, P, pl, d->k,
                                  reinterpret_cast<const uint32_t*>(pl + sp.tab_off), d->order, &d->topo, d->lr,
                                  nullptr, 0, d->theta, d->n, d->mean_out, st);
@@ -737,6 +764,10 @@ extern "C" psb_status psb_async_round(psb_ctx* c, const psb_step_desc* d, uint32
     s = psb_sparse_apply_direct(c, d->compressor, d->dtype, P, d->workers, regions, d->k, sp.tab_off, PSB_ORDER_NAIVE,
                                 nullptr, 0.0, scale.data(), 1, d->theta, d->n, nullptr, st);
     if (!s) s = psb_peer_ack(c, st);
+  } else if (sp.wire16) {
+    s = psb_sparse_apply_wire16(c, d->dtype, P, pl, d->k, reinterpret_cast<const uint32_t*>(pl + sp.tab_off),
+                                PSB_ORDER_NAIVE, nullptr, 0.0, scale.data(), 1, d->theta, d->n, nullptr, st);
+    if (!s && sp.ack_after_apply) s = psb_peer_ack(c, st);
   } else if (sp.tab_ready) {
     s = psb_sparse_apply_tab(c, d->compressor, d->dtype, P, pl, d->k, reinterpret_cast<const uint32_t*>(pl + sp.tab_off),
                              PSB_ORDER_NAIVE, nullptr, 0.0, scale.data(), 1, d->theta, d->n, nullptr, st);

@@ -104,6 +104,7 @@ struct psb_ctx {
   int shard_mode = 0;           // sharded multi-rank sparse apply (psb_peer_mode 2 / PSB_SHARD=1)
   int push_mode = 0;            // full exchange: K1 pushes its payload to the peers (psb_peer_mode 3)
   int direct_mode = 0;          // the apply reads the peers' arenas in place (psb_peer_mode 4)
+  int no_wire16 = 0;            // PSB_NO_WIRE16=1: 32-bit indices on the NVLink exchange
   // set by the step driver around one worker's K1 call in push mode: the
   // peers' payload-region bases and this worker's slot offset in them
   int push_n = 0;
@@ -151,6 +152,14 @@ psb_status psb_sparse_apply_tab(psb_ctx* c, psb_compressor comp, psb_dtype dt, i
                                 const uint32_t* tab, psb_order order, const psb_topology* topo, double lr,
                                 const double* wscale, int async_mode, void* theta, size_t n, void* mean_out,
                                 cudaStream_t st);
+// wire16 payloads: (u16 in-segment index | val) blocks for the NVLink exchange
+size_t psb_wire16_bytes(psb_dtype dt, size_t k);
+psb_status psb_pack16(psb_ctx* c, psb_dtype dt, const void* payload, size_t k, int seg_shift, void* out,
+                      cudaStream_t st);
+psb_status psb_sparse_apply_wire16(psb_ctx* c, psb_dtype dt, int P, const void* payloads, size_t k,
+                                   const uint32_t* tab, psb_order order, const psb_topology* topo, double lr,
+                                   const double* wscale, int async_mode, void* theta, size_t n, void* mean_out,
+                                   cudaStream_t st);
 psb_status psb_sparse_apply_direct(psb_ctx* c, psb_compressor comp, psb_dtype dt, int P, int W,
                                    const uint8_t* const* rank_region, size_t k, size_t tab_off, psb_order order,
                                    const psb_topology* topo, double lr, const double* wscale, int async_mode,
