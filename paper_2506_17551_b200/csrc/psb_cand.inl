@@ -22,7 +22,11 @@
 //   barrier-free loop does the scattered part (residual fix-up, and the fused
 //   single-worker SGD update theta[idx] += (-lr) * (val * 1)).
 
-constexpr int kCandThreads = 512;
+#ifndef PSB_CAND_THREADS
+#define PSB_CAND_THREADS 512
+#endif
+constexpr int kCandThreads = PSB_CAND_THREADS;
+static_assert(4096 % kCandThreads == 0 && kCandThreads % 32 == 0, "level histograms are split evenly over the CTA");
 constexpr uint32_t kCoarseBins = 4096;
 constexpr int kCoarseShift = 11;  // 2048-ulp coarse bins: 4095 of them span one octave above G
 constexpr uint32_t kLevelHist = 4096;  // words per level histogram buffer
