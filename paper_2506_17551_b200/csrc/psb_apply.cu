@@ -17,6 +17,7 @@
 // theta with separate RN multiply and add (no FMA).  HBM traffic: read the
 // P*k pairs once, read+write theta at the touched indices only.
 #include "psb_fold.cuh"
+#include "psb_debug.h"
 
 namespace {
 

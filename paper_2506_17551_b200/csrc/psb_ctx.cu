@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "psb_internal.cuh"
+#include "psb_debug.h"
 
 psb_status psb_q8_quant_launch(psb_ctx* c, const float* x, float* r, size_t n, uint32_t B,
                                int8_t* codes, float* scales, cudaStream_t st);

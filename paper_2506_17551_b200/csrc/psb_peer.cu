@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "psb_internal.cuh"
+#include "psb_debug.h"
 
 namespace {
 
