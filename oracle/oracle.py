@@ -109,6 +109,7 @@ def ref() -> ctypes.CDLL:
             "ref_bpr_batch_gradient": (_I, [_P, _SZ, _SZ, _SZ, _P, _P, _P, _SZ, _P, _P]),
             "ref_evaluate_topk": (_I, [_SZ, _SZ, _SZ, _P, _P, _P, _SZ, _P, _P, _SZ, _P, _P, _SZ, _SZ, _SZ, _U64, _P]),
             "ref_load_model": (_I, [ctypes.c_char_p, _P, _P, _SZ]),
+            "ref_comm_cost": (_I, [_I, _D, _SZ, _P, _P, _SZ, _P]),
             "ref_synthetic_split": (_I, [_SZ, _SZ, _SZ, _U64, _P, _P, _P, _P, _P, _P, _P]),
             "ref_train": (_I, [_SZ, _SZ, _SZ, _P, _P, _SZ, _SZ, _I, _SZ, _SZ, _D, _I, _SZ, _I, _U64, _U64, _P, _P, _SZ,
                                _P]),
@@ -417,6 +418,16 @@ def ref_load_model(path: str, cap: int):
     _ref_ck(ref().ref_load_model(path.encode(), _p(dims), _p(th), cap))
     u, i, d = (int(x) for x in dims)
     return (u, i, d), th[:(u + i) * d]
+
+
+def ref_comm_cost(algo: int, msg_bytes: float, P: int, counts3, links6, span_devices: int = 0) -> float:
+    """The reference's comm_cost (collectives.hpp:184-215); algo 0..3 = naive, ring, hierarchical, pipelined_ring;
+    links6 = (intra_bw, inter_bw, rack_bw, intra_lat, inter_lat, rack_lat)."""
+    c = np.ascontiguousarray(counts3, dtype=np.uint64)
+    l6 = np.ascontiguousarray(links6, dtype=np.float64)
+    out = np.zeros(1, dtype=np.float64)
+    _ref_ck(ref().ref_comm_cost(algo, float(msg_bytes), P, _p(c), _p(l6), span_devices, _p(out)))
+    return float(out[0])
 
 
 def ref_synthetic_split(users: int, items: int, interactions: int, seed: int):

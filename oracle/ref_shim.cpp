@@ -439,3 +439,22 @@ extern "C" int ref_load_model(const char* path, size_t* dims3, double* theta_out
     return fail_with(e);
   }
 }
+
+// comm_cost (collectives.hpp:184-215) on a topology given as 3 counts + 6
+// link figures {intra_bw, inter_bw, rack_bw, intra_lat, inter_lat, rack_lat}.
+extern "C" int ref_comm_cost(int algo, double msg_bytes, size_t P, const size_t* counts3, const double* links6,
+                             size_t span_devices, double* out) {
+  try {
+    Topology t = make_topo(counts3[0], counts3[1], counts3[2]);
+    t.intra_node_bw = links6[0];
+    t.inter_node_bw = links6[1];
+    t.inter_rack_bw = links6[2];
+    t.intra_node_lat = links6[3];
+    t.inter_node_lat = links6[4];
+    t.inter_rack_lat = links6[5];
+    *out = comm_cost(static_cast<CollectiveAlgorithm>(algo), msg_bytes, P, t, span_devices);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail_with(e);
+  }
+}

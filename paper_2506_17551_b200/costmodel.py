@@ -1,0 +1,208 @@
+"""The reference's alpha-beta communication model, calibrated on this node
+(the measured-topology time model).
+
+The reference prices the data-parallel gradient all-reduce with an analytic
+model over a `Topology` of link classes whose latency/bandwidth come from a
+config file (parsim/collectives.hpp:17-39, 156-215) and folds it into an
+iteration time (parsim/simulator.hpp:119-192).  Here:
+
+- `comm_cost` / `slowest_link_spanning` restate that model in float64 with
+  the reference's operation order, so for equal inputs the result is the
+  reference's double bit for bit (tests/test_costmodel.py pins it against the
+  compiled reference);
+- `calibrate_intra_node` fits the intra-node (NVLink/NVSwitch) link class from
+  measured all-reduce times: the ring model is linear in the message size,
+  t(m) = 2(P-1)*lat + 2(P-1)/P * m/bw, so a least-squares line through
+  (m, t) gives lat and bw;
+- `measure_allreduce` times torch.distributed all-reduces on the device
+  (CUDA events, max over ranks) or, on the gloo backend, with a host clock;
+- `dp_iteration` is the data-parallel slice of simulate_iteration_detail:
+  compute + fixed overhead + (comm - overlap), comm = comm_cost of the
+  compressed message over P devices.
+
+`tools/topology_probe.py` runs the calibration under torchrun and compares
+the model's step time with the measured one (profiles/r01/topology.json).
+This module is host-side planning only: it never runs on the gradient path.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, replace
+from typing import Dict, List, Optional, Sequence, Tuple, Union
+
+from . import _lib as L
+from .parsim import CollectiveAlgorithm, CompressorConfig, Topology, compression_ratio_for
+
+__all__ = ["Link", "validate_topology", "slowest_link_spanning", "comm_cost", "fit_ring", "calibrate_intra_node",
+           "measure_allreduce", "DpIteration", "dp_iteration"]
+
+
+@dataclass
+class Link:
+    latency: float = 0.0
+    bandwidth: float = 1.0
+
+
+def validate_topology(t: Topology) -> None:
+    """Topology::validate (collectives.hpp:30-37)."""
+    if not (t.racks >= 1 and t.nodes_per_rack >= 1 and t.devices_per_node >= 1):
+        raise L.PsbInvalidArgument("Topology: counts must be >= 1")
+    if not (t.intra_node_bw > 0 and t.inter_node_bw > 0 and t.inter_rack_bw > 0):
+        raise L.PsbInvalidArgument("Topology: zero bandwidth")
+    if not (t.intra_node_lat >= 0 and t.inter_node_lat >= 0 and t.inter_rack_lat >= 0):
+        raise L.PsbInvalidArgument("Topology: negative latency")
+
+
+def slowest_link_spanning(t: Topology, span_devices: int) -> Link:
+    """collectives.hpp:163-174: the worst link class a contiguous group of span_devices touches."""
+    link = Link(t.intra_node_lat, t.intra_node_bw)
+    if span_devices > t.devices_per_node:
+        link.latency = max(link.latency, t.inter_node_lat)
+        link.bandwidth = min(link.bandwidth, t.inter_node_bw)
+    if span_devices > t.devices_per_node * t.nodes_per_rack:
+        link.latency = max(link.latency, t.inter_rack_lat)
+        link.bandwidth = min(link.bandwidth, t.inter_rack_bw)
+    return link
+
+
+def _ring_phase(p: int, msg: float, link: Link) -> float:
+    # collectives.hpp:178-183
+    if p <= 1:
+        return 0.0
+    steps = float(p - 1)
+    return 2.0 * steps * link.latency + 2.0 * (steps / float(p)) * msg / link.bandwidth
+
+
+def _algo(a: Union[CollectiveAlgorithm, str]) -> CollectiveAlgorithm:
+    return a if isinstance(a, CollectiveAlgorithm) else CollectiveAlgorithm(a)
+
+
+def comm_cost(algo: Union[CollectiveAlgorithm, str], msg_bytes: float, P: int, topo: Topology,
+              span_devices: int = 0) -> float:
+    """Modeled seconds of one all-reduce of msg_bytes over P participants (collectives.hpp:184-215)."""
+    validate_topology(topo)
+    if msg_bytes < 0.0:
+        raise L.PsbInvalidArgument("comm_cost: negative message size")
+    if P < 1:
+        raise L.PsbInvalidArgument("comm_cost: P must be >= 1")
+    if P == 1:
+        return 0.0
+    a = _algo(algo)
+    link = slowest_link_spanning(topo, P if span_devices == 0 else span_devices)
+    msg = float(msg_bytes)
+    if a == CollectiveAlgorithm.naive:
+        return 2.0 * float(P - 1) * (link.latency + msg / link.bandwidth)
+    if a in (CollectiveAlgorithm.ring, CollectiveAlgorithm.pipelined_ring):
+        return _ring_phase(P, msg, link)
+    # hierarchical: ring per node, per rack, across racks, each on its own link class
+    d = min(P, topo.devices_per_node)
+    nodes_needed = (P + d - 1) // d
+    n = min(nodes_needed, topo.nodes_per_rack)
+    r = (P + d * n - 1) // (d * n)
+    return (_ring_phase(d, msg, Link(topo.intra_node_lat, topo.intra_node_bw)) +
+            _ring_phase(n, msg, Link(topo.inter_node_lat, topo.inter_node_bw)) +
+            _ring_phase(r, msg, Link(topo.inter_rack_lat, topo.inter_rack_bw)))
+
+
+def fit_ring(P: int, sizes: Sequence[float], seconds: Sequence[float]) -> Link:
+    """Least-squares (lat, bw) of the ring model t = 2(P-1)lat + 2(P-1)/P * m/bw.
+
+    A negative intercept (latency below the fit's resolution) clamps to 0."""
+    if P < 2:
+        raise L.PsbInvalidArgument("fit_ring: P must be >= 2")
+    if len(sizes) != len(seconds) or len(sizes) < 2:
+        raise L.PsbInvalidArgument("fit_ring: need >= 2 (size, time) pairs")
+    n = float(len(sizes))
+    mx = sum(sizes) / n
+    my = sum(seconds) / n
+    sxx = sum((x - mx) ** 2 for x in sizes)
+    if sxx <= 0:
+        raise L.PsbInvalidArgument("fit_ring: sizes must differ")
+    slope = sum((x - mx) * (y - my) for x, y in zip(sizes, seconds)) / sxx
+    if slope <= 0:
+        raise L.PsbInvalidArgument("fit_ring: time does not grow with size")
+    icept = my - slope * mx
+    steps = float(P - 1)
+    return Link(latency=max(icept, 0.0) / (2.0 * steps), bandwidth=2.0 * steps / (float(P) * slope))
+
+
+def calibrate_intra_node(P: int, sizes: Sequence[float], seconds: Sequence[float],
+                         base: Optional[Topology] = None) -> Topology:
+    """A Topology whose intra-node class is fitted from measured ring all-reduces on P devices of one node."""
+    link = fit_ring(P, sizes, seconds)
+    t = replace(base) if base is not None else Topology()
+    t.devices_per_node = max(t.devices_per_node, P)
+    t.intra_node_lat = link.latency
+    t.intra_node_bw = link.bandwidth
+    validate_topology(t)
+    return t
+
+
+def measure_allreduce(sizes: Sequence[int], iters: int = 20, warmup: int = 3, group=None) -> List[float]:
+    """Seconds per all-reduce (float32 sum) of each byte size on the current process group, max over ranks.
+
+    On CUDA the timing is CUDA events on the current stream; on gloo a host clock."""
+    import torch
+    import torch.distributed as dist
+
+    cuda = dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if cuda else torch.device("cpu")
+    out: List[float] = []
+    for nbytes in sizes:
+        x = torch.ones(max(1, int(nbytes) // 4), dtype=torch.float32, device=dev)
+        for _ in range(warmup):
+            dist.all_reduce(x, group=group)
+        dist.barrier(group=group)
+        if cuda:
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(iters):
+                dist.all_reduce(x, group=group)
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) * 1e-3 / iters
+        else:
+            t0 = time.perf_counter()
+            for _ in range(iters):
+                dist.all_reduce(x, group=group)
+            t = (time.perf_counter() - t0) / iters
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX, group=group)
+        out.append(float(tt.item()))
+    return out
+
+
+@dataclass
+class DpIteration:
+    compute_time: float
+    comm_time: float
+    overlapped_time: float
+    idle_time: float
+
+    @property
+    def wall_time(self) -> float:
+        # IterationProfile::wall_time (simulator.hpp:57-58)
+        return self.compute_time + self.idle_time + (self.comm_time - self.overlapped_time)
+
+    def as_dict(self) -> Dict[str, float]:
+        return {"compute_time": self.compute_time, "comm_time": self.comm_time,
+                "overlapped_time": self.overlapped_time, "idle_time": self.idle_time, "wall_time": self.wall_time}
+
+
+def dp_iteration(P: int, topo: Topology, gradient_bytes: float, compressor: CompressorConfig,
+                 compute_time: float, collective: Union[CollectiveAlgorithm, str] = CollectiveAlgorithm.ring,
+                 fixed_overhead: float = 0.0, overlap_fraction: float = 0.0) -> DpIteration:
+    """The pure data-parallel case (T = S = 1) of simulate_iteration_detail (simulator.hpp:119-192):
+    the gradient message is gradient_bytes / compression_ratio_for(compressor, gradient_bytes / 8)."""
+    if compute_time < 0 or fixed_overhead < 0 or gradient_bytes < 0:
+        raise L.PsbInvalidArgument("CostParams: negative cost")
+    if not (0.0 <= overlap_fraction <= 1.0):
+        raise L.PsbInvalidArgument("dp_iteration: overlap_fraction must be in [0, 1]")
+    comm = 0.0
+    if P > 1:
+        grad_dim = max(1, int(gradient_bytes / 8.0))
+        msg = gradient_bytes / compression_ratio_for(compressor, grad_dim)
+        comm = comm_cost(collective, msg, P, topo, P)
+    return DpIteration(compute_time=compute_time, comm_time=comm,
+                       overlapped_time=overlap_fraction * min(compute_time, comm), idle_time=fixed_overhead)
