@@ -454,3 +454,15 @@ def compression_ratio_for(cfg: CompressorConfig, dim: int) -> float:
             raise L.PsbInvalidArgument("compression_ratio_for: top_k must be >= 1")
         return 8.0 * dim / (16.0 + 16.0 * k)
     raise L.PsbInvalidArgument("compression_ratio_for: unknown compressor kind")
+
+
+# The reference's alpha-beta model (collectives.hpp:156-215) lives in costmodel.py;
+# forwarded here so `parsim.comm_cost` reads like the reference's namespace.
+def comm_cost(algo, msg_bytes: float, P: int, topo: Topology, span_devices: int = 0) -> float:
+    from .costmodel import comm_cost as f
+    return f(algo, msg_bytes, P, topo, span_devices)
+
+
+def slowest_link_spanning(topo: Topology, span_devices: int):
+    from .costmodel import slowest_link_spanning as f
+    return f(topo, span_devices)
