@@ -342,8 +342,10 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       const double ratio = (double)C / (double)k;
       w->last_ratio = (float)ratio;
       if (pred) {
-        if (ratio > 2.0) f = 1.f - (1.f - f) * 0.8f;         // loose: tighten
-        else if (ratio < 1.08) f = 1.f - (1.f - f) * 1.25f;  // thin: widen
+        const double lo = w->ratio_lo > 0.f ? w->ratio_lo : PSB_RATIO_LO;
+        const double hi = w->ratio_hi > 0.f ? w->ratio_hi : PSB_RATIO_HI;
+        if (ratio > hi) f = 1.f - (1.f - f) * 0.8f;         // loose: tighten
+        else if (ratio < lo) f = 1.f - (1.f - f) * 1.25f;  // thin: widen
       }
       f = fminf(fmaxf(f, 0.5f), 0.999f);
       float rho = w->rho > 0.f ? w->rho : 1.f;

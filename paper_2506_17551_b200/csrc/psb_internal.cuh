@@ -41,6 +41,14 @@ struct TopkScratch {
 
 // Per-worker persistent selection history: the next call's candidate set is
 // {key >= key(T_prev * f)}; f adapts so the set stays a little above k.
+// candidates / k band of the prediction-margin controller (psb_cand.inl)
+#ifndef PSB_RATIO_LO
+#define PSB_RATIO_LO 1.08
+#endif
+#ifndef PSB_RATIO_HI
+#define PSB_RATIO_HI 2.0
+#endif
+
 struct TopkWorker {
   unsigned long long g_key;  // predicted key threshold for the next call (0 = none)
   unsigned long long t_prev; // threshold key T of the previous call
@@ -50,6 +58,7 @@ struct TopkWorker {
   float last_ratio;          // candidates / k of the previous call
   uint32_t pad;
   unsigned long long z_key;  // predicted T without the safety margin (pre-zero boundary)
+  float ratio_lo, ratio_hi;  // margin controller band on candidates / k (0 = defaults)
 };
 
 struct psb_ctx {
