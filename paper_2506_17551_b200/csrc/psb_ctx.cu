@@ -125,12 +125,19 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   c->partials_cap = (size_t)c->num_sms * 4 + 64;
   ALLOC(c->d_partials, sizeof(double) * (c->partials_cap + 1));
 #undef ALLOC
-  if (const char* rl = getenv("PSB_RATIO_BAND")) {  // "lo,hi": the K1 prediction controller's band
-    float lo = 0.f, hi = 0.f;
-    if (sscanf(rl, "%f,%f", &lo, &hi) == 2 && lo > 0.f && hi > lo) {
+  {  // K1 prediction tuning: PSB_RATIO_BAND="lo,hi" (controller band), PSB_SECOND_F (miss second chance)
+    float lo = 0.f, hi = 0.f, f2 = 0.f;
+    const char* rl = getenv("PSB_RATIO_BAND");
+    const char* sf = getenv("PSB_SECOND_F");
+    const bool band = rl && sscanf(rl, "%f,%f", &lo, &hi) == 2 && lo > 0.f && hi > lo;
+    const bool second = sf && sscanf(sf, "%f", &f2) == 1 && f2 < 1.f;
+    if (band || second) {
       std::vector<TopkWorker> tw(max_workers);
       memset(tw.data(), 0, sizeof(TopkWorker) * max_workers);
-      for (auto& w : tw) w.ratio_lo = lo, w.ratio_hi = hi;
+      for (auto& w : tw) {
+        if (band) w.ratio_lo = lo, w.ratio_hi = hi;
+        if (second) w.second_f = f2 > 0.f ? f2 : -1.f;
+      }
       e = cudaMemcpy(c->d_tw, tw.data(), sizeof(TopkWorker) * max_workers, cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return fail(e);
     }

@@ -36,11 +36,10 @@ struct TopkScratch {
   uint32_t start_level;           // first radix level resolved over the candidates
   uint32_t spec_ok;               // predicted mode may pre-zero candidate residuals
   unsigned long long z_key;       // pass A pre-zeroes the residual of keys >= z_key (>= g_key)
+  unsigned long long g_key2;      // second-chance threshold after a miss (< g_key; 0 = none)
   unsigned long long phase_ns[16];  // k_cand phase timestamps (globaltimer, CTA 0)
 };
 
-// Per-worker persistent selection history: the next call's candidate set is
-// {key >= key(T_prev * f)}; f adapts so the set stays a little above k.
 // candidates / k band of the prediction-margin controller (psb_cand.inl)
 #ifndef PSB_RATIO_LO
 #define PSB_RATIO_LO 1.08
@@ -49,6 +48,8 @@ struct TopkScratch {
 #define PSB_RATIO_HI 2.0
 #endif
 
+// Per-worker persistent selection history: the next call's candidate set is
+// {key >= key(T_prev * f)}; f adapts so the set stays a little above k.
 struct TopkWorker {
   unsigned long long g_key;  // predicted key threshold for the next call (0 = none)
   unsigned long long t_prev; // threshold key T of the previous call
@@ -59,6 +60,8 @@ struct TopkWorker {
   uint32_t pad;
   unsigned long long z_key;  // predicted T without the safety margin (pre-zero boundary)
   float ratio_lo, ratio_hi;  // margin controller band on candidates / k (0 = defaults)
+  float second_f;            // second-chance factor after a miss (0 = PSB_SECOND_F, < 0 = off)
+  uint32_t pad2;
 };
 
 struct psb_ctx {

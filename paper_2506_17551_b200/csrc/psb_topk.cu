@@ -65,8 +65,13 @@ __host__ __device__ constexpr int tile_elems() {
   return PSB_SCAN_THREADS * 4 * VecOf<T>::W;  // f32: 4096, f64: 2048
 }
 
-enum { MODE_A = 0, MODE_A2 = 1, MODE_D = 2 };
-enum { DONE_A = 0, DONE_A2 = 1 };
+enum { MODE_A = 0, MODE_A2 = 1, MODE_D = 2, MODE_S = 3 };
+enum { DONE_A = 0, DONE_A2 = 1, DONE_S = 2 };
+// flags written by another CTA of the same (cooperative) grid: bypass L1
+__device__ __forceinline__ uint32_t ld_flag(const uint32_t* p) { return __ldcg(p); }
+#ifndef PSB_SECOND_F
+#define PSB_SECOND_F 0.97f  // second-chance threshold factor after a prediction miss (tools/sweep_second.sh)
+#endif
 
 
 // key <-> magnitude value, for the predicted threshold key(T * f)
@@ -220,6 +225,7 @@ __global__ void k_topk_begin(TopkScratch* s, TopkWorker* w, uint32_t* hist1, uin
     s->start_level = 1;
     s->g_key = predict ? w->g_key : 0ull;
     s->z_key = w->z_key > w->g_key ? w->z_key : w->g_key;
+    s->g_key2 = 0;
     // pre-zeroing the candidates' residual pays off while most candidates are
     // selected (restores C - k < zero-writes k)
     s->spec_ok = w->last_ratio < 2.0f ? 1u : 0u;
@@ -260,12 +266,18 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
   K gk = 0;
   bool compact, hist;
   if (MODE == MODE_D) {
-    if (!a.s->need_compact) return;
+    if (!ld_flag(&a.s->need_compact)) return;
     gk = (K)a.s->b1 << SH1;
     compact = true;
     hist = false;
+  } else if (MODE == MODE_S) {
+    if (!ld_flag(&a.s->need_full_hist)) return;
+    gk = (K)__ldcg(&a.s->g_key2);
+    if (gk == 0) return;
+    compact = true;
+    hist = false;
   } else if (MODE == MODE_A2) {
-    if (!a.s->need_full_hist) return;
+    if (!ld_flag(&a.s->need_full_hist)) return;
     compact = false;
     hist = true;
   } else {
@@ -469,9 +481,29 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
   }
   if (MODE == MODE_D) return;  // k_cand prefix-sums the segment counts itself
 
-  if (!last_block(&a.s->done[MODE == MODE_A ? DONE_A : DONE_A2])) return;
+  if (!last_block(&a.s->done[MODE == MODE_A ? DONE_A : MODE == MODE_S ? DONE_S : DONE_A2])) return;
 
   const unsigned long long k = a.s->k, n = a.s->n;
+  if (MODE == MODE_S) {
+    // second chance valid iff at least k keys >= G2: continue in predicted
+    // mode on G2 (r holds p everywhere now, so no speculative zeros)
+    const unsigned long long C = __ldcg(&a.s->cand_count);
+    if (threadIdx.x == 0) {
+      if (C >= k) {
+        a.s->g_key = a.s->g_key2;
+        a.s->spec_ok = 0;
+        a.s->start_level = 0;
+        a.s->prefix = 0;
+        a.s->need = k;
+        a.s->match = C;
+        __threadfence();
+        a.s->need_full_hist = 0;
+      } else {
+        a.s->cand_count = 0;  // still short: the full histogram pass takes over
+      }
+    }
+    return;
+  }
   if (compact) {
     // predicted mode: valid iff at least k keys >= G (then T >= G)
     const unsigned long long C = __ldcg(&a.s->cand_count);
@@ -483,8 +515,10 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
         a.s->match = C;
       }
     } else if (threadIdx.x == 0) {
-      a.s->need_full_hist = 1;  // miss: restore, rerun level 1 on all of p, then compact
-      a.s->cand_count = 0;
+      a.s->need_full_hist = 1;  // miss: restore, then a second-chance compaction on
+      a.s->cand_count = 0;      // G2 = G * PSB_SECOND_F; the full level-1 pass only if that misses too
+      const float f2 = a.w->second_f != 0.f ? a.w->second_f : PSB_SECOND_F;
+      a.s->g_key2 = f2 > 0.f ? scale_key(gk, f2, T(0)) : 0ull;
       a.w->misses += 1;
       a.w->f = a.w->f > 0.f ? 1.f - (1.f - a.w->f) * 1.5f : 0.97f;  // widen the margin
       if (a.w->f < 0.5f) a.w->f = 0.5f;
@@ -529,7 +563,7 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS, PSB_SCAN_MINB) k_scan(ScanAr
 template <class T>
 __device__ __forceinline__ void restore_body(const ScanArgs<T>& a) {
   constexpr int TILE = tile_elems<T>();
-  if (!a.s->need_full_hist || !a.s->spec_ok || a.r == nullptr) return;
+  if (!ld_flag(&a.s->need_full_hist) || !a.s->spec_ok || a.r == nullptr) return;
   const size_t base = (size_t)blockIdx.x * a.tpc * TILE;
   const uint32_t cnt = a.seg_cnt[blockIdx.x];
   for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) a.r[a.cand_idx[base + j]] = a.cand_val[base + j];
@@ -546,10 +580,12 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_restore(ScanArgs<T> a) {
 template <class T>
 __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_fallback(ScanArgs<T> a) {
   cg::grid_group grid = cg::this_grid();
-  const bool miss = a.s->need_full_hist != 0;
-  if (!miss && !a.s->need_compact) return;  // uniform: flags from the previous kernel
+  const bool miss = ld_flag(&a.s->need_full_hist) != 0;
+  if (!miss && !ld_flag(&a.s->need_compact)) return;  // uniform: flags from the previous kernel
   if (miss) {
     restore_body(a);
+    grid.sync();
+    scan_body<T, MODE_S>(a);   // second chance; its last CTA clears need_full_hist if it holds
     grid.sync();
     scan_body<T, MODE_A2>(a);  // full histogram; its last CTA resolves b1 and sets need_compact
     grid.sync();
@@ -614,9 +650,10 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   if (!fused_fb) {
     (void)cudaGetLastError();
     k_restore<T><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
+    k_scan<T, MODE_S><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
     k_scan<T, MODE_A2><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
     k_scan<T, MODE_D><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
-    c->launches += 2;
+    c->launches += 3;
   }
 
   CandArgs<T> b;

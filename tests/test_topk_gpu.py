@@ -109,6 +109,37 @@ def test_prediction_miss_falls_back_exactly(ctx):
     ctx.check()
 
 
+@pytest.mark.parametrize("ef", [False, True])
+def test_prediction_second_chance_exact(ctx, ef):
+    """The threshold drops a few percent below the predicted margin: pass A
+    misses, the second-chance compaction on G2 = 0.97 G holds (no full
+    histogram pass), and the results stay bit-exact."""
+    n, k = 1_000_003, 10_000
+    scales = [1, 1, 1, 1, 0.93, 1, 1, 1, 0.93, 0.93, 1, 1]
+    second = 0
+    for wi, dt in ((7, np.float32), (8, np.float64)):
+        r_host = np.zeros(n, dtype=dt)
+        r_dev = torch.zeros(n, dtype=torch.float32 if dt == np.float32 else torch.float64, device="cuda")
+        for s, sc in enumerate(scales):
+            g = (O.generate("uniform", 3, 0, s, n) * np.float32(sc)).astype(dt)
+            before = ctx.topk_stats(worker=wi)["misses"]
+            idx, val = ctx.ef_topk(torch.from_numpy(g).cuda(), r_dev if ef else None, k, worker=wi)
+            if ef:
+                oi, ov, _ = O.ef_topk(g, r_host, k)
+            else:
+                oi, ov = O.topk(g, k)
+            assert np.array_equal(tnp(idx).view(np.uint32), oi), (dt, s)
+            assert np.array_equal(tnp(val), ov), (dt, s)
+            if ef:
+                assert np.array_equal(tnp(r_dev), r_host), (dt, s)
+            st = ctx.topk_stats(worker=wi)
+            if st["misses"] > before and st["predicted_valid"]:
+                second += 1
+    ctx.check()
+    if not ef:
+        assert second >= 1  # the second chance was taken and held at least once
+
+
 @pytest.mark.parametrize("n,k", [(1, 1), (2, 2), (3, 1), (4097, 4097), (4097, 1), (12345, 12344)])
 def test_edge_sizes(ctx, n, k):
     g = O.generate("ties", 9, 0, 0, n)
