@@ -297,6 +297,33 @@ def test_momentum_sync_step(ctx, comp, W):
             assert np.array_equal(bits(tnp(res)), bits(res_h)), step
 
 
+def test_momentum_scratch_reuse_across_sizes(ctx):
+    """The momentum pass stores zeros back into the mean scratch instead of a
+    per-step memset: dense (onebit) steps followed by sparse top-k steps at a
+    smaller and then a larger n, on one context, stay bit-exact."""
+    lr, beta = 0.05, 0.9
+    for step, (comp, n, k) in enumerate([("onebit", 120_000, 0), ("topk", 60_000, 600),
+                                          ("none", 90_000, 0), ("topk", 120_000, 300),
+                                          ("topk", 120_000, 50)]):
+        g_h = O.generate("llmrec", 23, 0, step, n)[None, :]
+        theta_h = O.generate("llmrec", 29, 0, step, n)
+        m_h = O.generate("llmrec", 31, 0, step, n)
+        theta = torch.from_numpy(theta_h.copy()).cuda()
+        m = torch.from_numpy(m_h.copy()).cuda()
+        mean = torch.zeros(n, device="cuda")
+        ctx.sync_step(ctx.step_desc(COMPS[comp], torch.from_numpy(g_h).cuda(), None, theta, lr, max(k, 1), "ring",
+                                    256, None, mean, momentum=m, beta=beta))
+        ctx.check()
+        mean_h = O.sync_step(g_h, theta_h.copy(), lr, comp, max(k, 1), "ring", None).astype(np.float32)
+        if comp == "onebit":
+            np.testing.assert_allclose(tnp(mean), mean_h, rtol=1e-5, atol=1e-9)
+            mean_h = tnp(mean).copy()
+        O.momentum_(mean_h, m_h, theta_h, beta, lr)
+        assert np.array_equal(bits(tnp(mean)), bits(mean_h)), step
+        assert np.array_equal(bits(tnp(m)), bits(m_h)), step
+        assert np.array_equal(bits(tnp(theta)), bits(theta_h)), step
+
+
 def test_momentum_rejects_q8_and_async(ctx):
     n = 4096
     g = torch.randn(1, n, device="cuda")
