@@ -613,7 +613,106 @@ __global__ void __launch_bounds__(256) k_momentum(const T* __restrict__ mean, T*
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
 }
 
+// Single-worker top-k momentum step without a dense mean scratch: the mean
+// is the payload itself (P = 1: fold of one buffer, scaled by 1/1), already
+// sorted by index.  k_tile_starts cuts the payload at 4096-element tiles;
+// k_momentum_merge scatters a tile's entries into a zeroed shared-memory tile
+// and makes the dense m / theta pass (16 B/el, f32) reading the mean from it.
+constexpr int kMomTile = 4096;
+
+__global__ void k_tile_starts(const uint32_t* __restrict__ idx, size_t k, uint32_t* __restrict__ starts,
+                              long long ntiles) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j <= k; j += stride) {
+    const long long cur = j < k ? (long long)(idx[j] / kMomTile) : ntiles;
+    const long long prev = j > 0 ? (long long)(idx[j - 1] / kMomTile) : -1;
+    for (long long t = prev + 1; t <= cur; ++t) starts[t] = (uint32_t)j;
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_momentum_merge(const uint32_t* __restrict__ idx, const T* __restrict__ val,
+                                                        const uint32_t* __restrict__ starts, T* __restrict__ m,
+                                                        T* __restrict__ theta, T* __restrict__ mean_out, T beta,
+                                                        T coef, size_t n, uint32_t* flags) {
+  __shared__ __align__(16) T gt[kMomTile];
+  for (int e = threadIdx.x; e < kMomTile; e += blockDim.x) gt[e] = T(0);
+  bool bad = false;
+  const size_t ntiles = (n + kMomTile - 1) / kMomTile;
+  const bool vec = sizeof(T) == 4 && ((((uintptr_t)m) | ((uintptr_t)theta) | ((uintptr_t)mean_out)) & 15) == 0;
+  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const size_t lo = t * kMomTile;
+    const uint32_t a = starts[t], b = starts[t + 1];
+    __syncthreads();  // zeroed tile (first pass / previous un-scatter) visible
+    for (uint32_t j = a + threadIdx.x; j < b; j += blockDim.x) gt[idx[j] - lo] = val[j];
+    __syncthreads();
+    if (vec && lo + kMomTile <= n) {
+      constexpr int V = kMomTile / 4 / 256;
+      float4 m4[V], t4[V];
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        const size_t v = lo / 4 + threadIdx.x + (size_t)u * 256;
+        m4[u] = __ldcs(reinterpret_cast<const float4*>(m) + v);
+        t4[u] = __ldcs(reinterpret_cast<const float4*>(theta) + v);
+      }
+      const float bb = (float)beta, cf = (float)coef;
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        const int e4 = threadIdx.x + u * 256;
+        const float4 g4 = reinterpret_cast<const float4*>(gt)[e4];
+        float4 a4 = m4[u], th = t4[u];
+        a4.x = __fadd_rn(__fmul_rn(bb, a4.x), g4.x);
+        a4.y = __fadd_rn(__fmul_rn(bb, a4.y), g4.y);
+        a4.z = __fadd_rn(__fmul_rn(bb, a4.z), g4.z);
+        a4.w = __fadd_rn(__fmul_rn(bb, a4.w), g4.w);
+        th.x = __fadd_rn(__fmul_rn(cf, a4.x), th.x);
+        th.y = __fadd_rn(__fmul_rn(cf, a4.y), th.y);
+        th.z = __fadd_rn(__fmul_rn(cf, a4.z), th.z);
+        th.w = __fadd_rn(__fmul_rn(cf, a4.w), th.w);
+        const size_t v = lo / 4 + e4;
+        __stcs(reinterpret_cast<float4*>(m) + v, a4);
+        __stcs(reinterpret_cast<float4*>(theta) + v, th);
+        if (mean_out) reinterpret_cast<float4*>(mean_out)[v] = g4;
+        bad |= !is_finite(th.x) || !is_finite(th.y) || !is_finite(th.z) || !is_finite(th.w);
+      }
+    } else {
+      for (int e = threadIdx.x; e < kMomTile && lo + e < n; e += blockDim.x) {
+        const size_t i = lo + e;
+        const T mi = add_rn(mul_rn(beta, m[i]), gt[e]);
+        m[i] = mi;
+        const T th = add_rn(mul_rn(coef, mi), theta[i]);
+        theta[i] = th;
+        if (mean_out) mean_out[i] = gt[e];
+        bad |= !is_finite(th);
+      }
+    }
+    __syncthreads();  // every thread done reading the tile
+    for (uint32_t j = a + threadIdx.x; j < b; j += blockDim.x) gt[idx[j] - lo] = T(0);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
+}
+
 }  // namespace
+
+psb_status psb_momentum_topk1(psb_ctx* c, psb_dtype dt, const uint8_t* payload, size_t k, void* m, void* theta,
+                              void* mean_out, double beta, double lr, size_t n, uint32_t* starts_buf,
+                              cudaStream_t st) {
+  const long long ntiles = (long long)((n + kMomTile - 1) / kMomTile);
+  const uint32_t* idx = reinterpret_cast<const uint32_t*>(payload);
+  const void* val = payload + psb_align16(k * 4);
+  const unsigned g0 = (unsigned)std::max<size_t>(1, std::min<size_t>((k + 1 + 255) / 256, (size_t)c->num_sms * 8));
+  k_tile_starts<<<g0, 256, 0, st>>>(idx, k, starts_buf, ntiles);
+  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(ntiles, (long long)c->num_sms * 8));
+  if (dt == PSB_F32)
+    k_momentum_merge<float><<<grid, 256, 0, st>>>(idx, (const float*)val, starts_buf, (float*)m, (float*)theta,
+                                                   (float*)mean_out, (float)beta, (float)(-lr), n, c->d_flags);
+  else
+    k_momentum_merge<double><<<grid, 256, 0, st>>>(idx, (const double*)val, starts_buf, (double*)m, (double*)theta,
+                                                    (double*)mean_out, beta, -lr, n, c->d_flags);
+  c->launches += 2;
+  PSB_LAUNCH_CHECK(c, "psb_momentum_topk1");
+  return PSB_OK;
+}
 
 extern "C" psb_status psb_momentum_sgd(psb_ctx* c, psb_dtype dt, const void* mean, void* m, void* theta, double beta,
                                        double lr, size_t n, psb_stream_t stream) {

@@ -738,6 +738,19 @@ extern "C" psb_status psb_sync_step(psb_ctx* c, const psb_step_desc* d, psb_stre
   PSB_REQUIRE(c, d->compressor != PSB_COMP_Q8, "momentum: not supported with the dense q8 compressor");
   cudaStream_t st = (cudaStream_t)stream;
   const size_t es = d->dtype == PSB_F64 ? 8 : 4;
+  static const bool no_merge = getenv("PSB_MOM_NO_MERGE") && atoi(getenv("PSB_MOM_NO_MERGE"));
+  if (!no_merge && c->nranks == 1 && d->workers == 1 && d->compressor == PSB_COMP_TOPK) {
+    // one payload: its sorted (index, value) list is the mean; no dense scratch
+    s = ensure(c, &c->d_mom_mean, &c->mom_bytes, sizeof(uint32_t) * (d->n / 4096 + 2), "momentum tile table");
+    if (s) return s;
+    uint8_t* pl = nullptr;
+    s = compress_and_gather(c, d, st, &pl, false, nullptr);
+    if (s) return s;
+    s = psb_momentum_topk1(c, d->dtype, pl, d->k, d->m, d->theta, d->mean_out, d->beta, d->lr, d->n,
+                           reinterpret_cast<uint32_t*>(c->d_mom_mean), st);
+    psb_mark(c, st);
+    return s;
+  }
   s = ensure(c, &c->d_mom_mean, &c->mom_bytes, es * d->n, "momentum mean buffer");
   if (s) return s;
   CUDA_TRY(c, cudaMemsetAsync(c->d_mom_mean, 0, es * d->n, st), "momentum");

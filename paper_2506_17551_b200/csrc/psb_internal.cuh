@@ -137,6 +137,10 @@ struct psb_ctx {
 void psb_mark(psb_ctx* c, cudaStream_t st);
 
 // NVLink peer exchange (psb_peer.cu)
+// single-worker top-k momentum step straight from the payload; psb_apply.cu
+psb_status psb_momentum_topk1(psb_ctx* c, psb_dtype dt, const uint8_t* payload, size_t k, void* m, void* theta,
+                              void* mean_out, double beta, double lr, size_t n, uint32_t* starts_buf,
+                              cudaStream_t st);
 psb_status psb_peer_ensure(psb_ctx* c, size_t payload_bytes, cudaStream_t st);
 uint8_t* psb_peer_payload(psb_ctx* c);
 psb_status psb_peer_wait_ack(psb_ctx* c, cudaStream_t st);

@@ -324,6 +324,33 @@ def test_momentum_scratch_reuse_across_sizes(ctx):
         assert np.array_equal(bits(tnp(theta)), bits(theta_h)), step
 
 
+@pytest.mark.parametrize("n,k,off", [(3 * 4096, 40, 0), (50_001, 500, 1), (4096 * 7 + 5, 4096 * 7 + 5, 0)])
+def test_momentum_topk_single_worker_f64_and_views(ctx, n, k, off):
+    """Single-worker top-k momentum takes the payload-merge pass (no dense
+    mean scratch): f64, a misaligned f32 view, and k = n (every entry
+    selected), 4 steps with EF, bit-exact vs the oracle composite."""
+    lr, beta = 0.05, 0.9
+    for dt in (np.float64, np.float32):
+        tdt = torch.float64 if dt == np.float64 else torch.float32
+        theta_h = np.zeros(n, dtype=dt)
+        m_h = np.zeros(n, dtype=dt)
+        res_h = np.zeros((1, n), dtype=dt)
+        base = torch.zeros(3, n + off, dtype=tdt, device="cuda")
+        theta, m, mean = base[0, off:], base[1, off:], base[2, off:]
+        res = torch.zeros(1, n, dtype=tdt, device="cuda")
+        for step in range(4):
+            g_h = O.generate("llmrec", 37, 0, step, n).astype(dt)[None, :]
+            ctx.sync_step(ctx.step_desc(L.PSB_COMP_TOPK, torch.from_numpy(g_h).cuda(), res, theta, lr, k, "ring",
+                                        256, None, mean, momentum=m, beta=beta))
+            ctx.check()
+            mean_h = O.sync_step(g_h, theta_h.copy(), lr, "topk", k, "ring", res_h).astype(dt)
+            O.momentum_(mean_h, m_h, theta_h, beta, lr)
+            assert np.array_equal(bits(tnp(mean)), bits(mean_h)), (dt, step)
+            assert np.array_equal(bits(tnp(m)), bits(m_h)), (dt, step)
+            assert np.array_equal(bits(tnp(theta)), bits(theta_h)), (dt, step)
+            assert np.array_equal(bits(tnp(res)), bits(res_h)), (dt, step)
+
+
 def test_momentum_rejects_q8_and_async(ctx):
     n = 4096
     g = torch.randn(1, n, device="cuda")
