@@ -32,6 +32,11 @@ PSB_API psb_status psb_debug_exchange(psb_ctx* ctx, size_t bytes_per_rank, int i
  * sums of the sparse apply. */
 PSB_API void psb_debug_apply_trace(unsigned long long* out8, int reset);
 
+/* Only in a build with EXTRA_NVFLAGS=-DPSB_SCAN_TRACE: globaltimer (ns) at
+ * entry and exit of every CTA of the last K1 streaming pass, as pairs; returns
+ * the number of CTAs copied (0 in a normal build). */
+PSB_API int psb_debug_scan_trace(unsigned long long* out, int max_ctas);
+
 #ifdef __cplusplus
 }
 #endif

@@ -12,7 +12,9 @@ import os
 import torch  # noqa: F401  (loads the NCCL/cudart the library links against first)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpsb.so")
+# PSB_LIB: an alternative build of the same library (diagnostics builds such
+# as libpsb_trace.so from tools/); the product path is libpsb.so
+LIB_PATH = os.path.join(_HERE, os.environ.get("PSB_LIB") or "libpsb.so")
 
 # psb_status
 PSB_OK, PSB_EINVAL, PSB_ENONFINITE, PSB_ECUDA, PSB_ENCCL, PSB_ENOMEM, PSB_ESTATE = range(7)

@@ -160,6 +160,10 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
 #ifdef PSB_APPLY_TRACE
   unsigned long long t_prev = gtimer();
 #endif
+  // a peer timed out in the exchange (flag 8, psb_peer.cu): its payload slot
+  // may hold the previous step's data, so theta is left untouched and the
+  // step reports PSB_ESTATE at the caller's psb_check
+  if (flags != nullptr && (__ldcg(flags) & 8u)) return;
   if (range) {  // segment range decided on the device (sharded multi-rank apply)
     seg_lo = range[0];
     nseg = range[1] - range[0];

@@ -37,11 +37,14 @@ struct CandArgs {
   TopkScratch* s;
   TopkWorker* w;
   uint32_t* hlev;  // kNumLevelHists x kLevelHist global histograms (zero between calls)
-  const uint32_t* cand_idx;
-  const T* cand_val;
-  const uint32_t* seg_cnt;  // candidates per k_scan CTA segment (nseg)
-  uint32_t nseg;
-  size_t seg_cap;           // segment stride (= elements streamed by one k_scan CTA)
+  const uint32_t* seg_idx;   // k_scan's tile-segmented candidates (tile t at t*TILE, tile_cnt[t] entries)
+  const T* seg_val;
+  const uint32_t* tile_cnt;
+  uint32_t* sb;              // [3][sb_stride] superblock sums of tile_cnt (cleared here for the next call)
+  uint32_t sb_stride;
+  uint32_t ntiles;
+  uint32_t* cand_idx;        // the same candidates as one contiguous index-ordered list [0, C)
+  T* cand_val;
   uint32_t stage_cap;       // entries of the shared-memory staging area
   unsigned long long* cta;  // per-CTA (gt | eq << 32) totals
   uint32_t* idx_out;
@@ -58,28 +61,6 @@ struct CandArgs {
   T* push_val[PSB_MAX_P];
 };
 
-// Flat view of the segmented candidate list: logical entry e (index order)
-// lies in segment s with pre[s] <= e < pre[s+1], physically at
-// s*cap + (e - pre[s]).
-struct FlatMap {
-  const uint32_t* pre;  // shared-memory copy
-  uint32_t nseg;
-  size_t cap;
-  __device__ __forceinline__ uint32_t seg_of(uint32_t e) const {
-    uint32_t lo = 0, hi = nseg;  // pre[lo] <= e < pre[hi]
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (pre[mid] <= e) lo = mid;
-      else hi = mid;
-    }
-    return lo;
-  }
-  __device__ __forceinline__ size_t phys(uint32_t e, uint32_t* sg) const {
-    while (pre[*sg + 1] <= e) ++*sg;
-    return (size_t)*sg * cap + (e - pre[*sg]);
-  }
-};
-
 template <class T>
 __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   typedef KeyOf<T> KO;
@@ -91,7 +72,6 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   T* st_val = reinterpret_cast<T*>(dsm + kCoarseBins * 4);                 // stage_cap values
   uint32_t* st_idx = reinterpret_cast<uint32_t*>(st_val + a.stage_cap);    // stage_cap indices
   uint32_t* st_slot = st_idx + a.stage_cap;                                // stage_cap output slots
-  __shared__ uint32_t sh_pre[PSB_FINAL_TPC_MAX + 1];
   __shared__ unsigned long long sh_warp[32];
   __shared__ LevelResult sh_res;
   __shared__ uint32_t sh_bad;
@@ -110,51 +90,156 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   };
   phase();
 
-  // ---- this CTA's slice [lo, hi) of the logical list (multiple of 4 entries)
-  // exclusive prefix of the k_scan segment counts, computed by every CTA
-  // (no serial last-block pass at the end of k_scan)
+  // ---- this CTA's slice of the index-ordered list, located without a grid
+  // barrier.  Slices are whole k_scan tiles [tb, te), balanced on the cost
+  // entries + alpha * tiles (alpha >= 8): a slice covering a sparse stretch
+  // of the index space is bounded in tiles, so its tile prefix fits one
+  // shared-memory window.  Every CTA scans the superblock sums (64 tiles
+  // each), finds the superblocks holding its two boundaries, refines them to
+  // tiles with one warp each, then scans its tiles' counts in windows of up to
+  // 4095 tiles and copies its entries out of k_scan's tile segments -- into
+  // shared memory when the slice fits the stage, else into the contiguous
+  // global list at [lo, hi).
+  constexpr int TILE = tile_elems<T>();
+  constexpr uint32_t kWin = kCoarseBins - 1;  // tiles per prefix window (sh_h)
+  constexpr uint32_t kSb = 1u << PSB_SB_SHIFT;
+  __shared__ uint32_t sh_bsb[2];                 // superblock holding each boundary
+  __shared__ unsigned long long sh_bpre[2];      // entries before that superblock
+  __shared__ uint32_t sh_bt[2], sh_be[2];        // boundary tile and entries before it
+  if (threadIdx.x == 0) sh_bad = 0;
+  const uint32_t pass = __ldcg(&s->list_pass);
+  const uint32_t* sbc = a.sb + (size_t)pass * a.sb_stride;
+  const uint32_t nsb = (a.ntiles + kSb - 1) >> PSB_SB_SHIFT;
+  uint32_t C;
+  unsigned long long alpha, total_cost, tgt0, tgt1;
   {
-    const uint32_t q = (a.nseg + blockDim.x - 1) / blockDim.x;
-    const uint32_t b0 = min(a.nseg, threadIdx.x * q), b1 = min(a.nseg, b0 + q);
+    const uint32_t per = (nsb + blockDim.x - 1) / blockDim.x;
+    const uint32_t b0 = min(nsb, threadIdx.x * per), b1 = min(nsb, b0 + per);
     unsigned long long loc = 0;
-    for (uint32_t b = b0; b < b1; ++b) loc += __ldcg(a.seg_cnt + b);
+    for (uint32_t b = b0; b < b1; ++b) loc += __ldcg(sbc + b);
     unsigned long long tot;
-    unsigned long long run0 = block_exscan_u64(loc, sh_warp, &tot);
-    for (uint32_t b = b0; b < b1; ++b) {
-      sh_pre[b] = (uint32_t)run0;
-      run0 += __ldcg(a.seg_cnt + b);
+    const unsigned long long ex = block_exscan_u64(loc, sh_warp, &tot);
+    C = (uint32_t)tot;
+    alpha = max(8ull, (tot + 2048ull * gridDim.x - 1) / (2048ull * gridDim.x));
+    total_cost = tot + alpha * a.ntiles;
+    const unsigned long long q = (total_cost + gridDim.x - 1) / gridDim.x;
+    tgt0 = (unsigned long long)blockIdx.x * q;
+    tgt1 = tgt0 + q;
+    if (threadIdx.x < 2) {
+      sh_bsb[threadIdx.x] = nsb;  // boundary at or past the end: the last tile
+      sh_bpre[threadIdx.x] = tot;
     }
-    if (threadIdx.x == 0) {
-      sh_pre[a.nseg] = (uint32_t)tot;
-      sh_bad = 0;
+    __syncthreads();
+    unsigned long long e = ex;
+    for (uint32_t b = b0; b < b1; ++b) {
+      const uint32_t cb = __ldcg(sbc + b);
+      const unsigned long long c_lo = e + alpha * ((unsigned long long)b << PSB_SB_SHIFT);
+      const unsigned long long c_hi = e + cb + alpha * min((unsigned long long)a.ntiles,
+                                                           (unsigned long long)(b + 1) << PSB_SB_SHIFT);
+      if (c_lo <= tgt0 && tgt0 < c_hi) {
+        sh_bsb[0] = b;
+        sh_bpre[0] = e;
+      }
+      if (c_lo <= tgt1 && tgt1 < c_hi) {
+        sh_bsb[1] = b;
+        sh_bpre[1] = e;
+      }
+      e += cb;
     }
   }
   __syncthreads();
-  FlatMap m;
-  m.pre = sh_pre;
-  m.nseg = a.nseg;
-  m.cap = a.seg_cap;
-  const uint32_t C = sh_pre[a.nseg];
-  uint32_t chunk = (C + gridDim.x - 1) / gridDim.x;
-  chunk = (chunk + 3u) & ~3u;
-  const uint32_t lo = min(C, blockIdx.x * chunk), hi = min(C, lo + chunk);
+  if (threadIdx.x < 64) {  // warp q2 refines boundary q2 to a tile
+    const int q2 = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned long long target = q2 ? tgt1 : tgt0;
+    const uint32_t b = sh_bsb[q2];
+    if (b >= nsb) {
+      if (lane == 0) {
+        sh_bt[q2] = a.ntiles;
+        sh_be[q2] = C;
+      }
+    } else {
+      const uint32_t T0 = b << PSB_SB_SHIFT, nt = min(kSb, a.ntiles - T0);
+      const uint32_t i0 = 2 * lane, i1 = 2 * lane + 1;
+      const uint32_t c0 = i0 < nt ? __ldcg(a.tile_cnt + T0 + i0) : 0u;
+      const uint32_t c1 = i1 < nt ? __ldcg(a.tile_cnt + T0 + i1) : 0u;
+      uint32_t incl = c0 + c1;  // entries of this lane's two tiles, scanned over the warp
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const unsigned long long e0 = sh_bpre[q2] + (incl - c0 - c1);  // entries before tile i0
+      const unsigned long long t_cost0 = e0 + alpha * (T0 + i0);
+      const unsigned long long t_cost1 = e0 + c0 + alpha * (T0 + i1);
+      // boundary = first tile whose start cost reaches the target
+      const bool below0 = i0 < nt && t_cost0 < target;
+      const bool below1 = i1 < nt && t_cost1 < target;
+      const uint32_t nbelow = __popc(__ballot_sync(0xffffffffu, below0)) + __popc(__ballot_sync(0xffffffffu, below1));
+      // entries of the tiles before the boundary
+      const uint32_t part = (below0 ? c0 : 0u) + (below1 ? c1 : 0u);
+      uint32_t sum = part;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) {
+        sh_bt[q2] = T0 + nbelow;
+        sh_be[q2] = (uint32_t)(sh_bpre[q2] + sum);
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t lo = sh_be[0], hi = sh_be[1];
+  const uint32_t tb = sh_bt[0], te = sh_bt[1];
   const uint32_t cnt = hi - lo;
   const bool staged = cnt <= a.stage_cap;
-  if (staged && cnt) {
-    // copy the slice with cp.async (LDGSTS), all copies in flight at once.
-    // Thread t takes entries t, t + blockDim, ... and walks the k_scan
-    // segments forward as it goes (one binary search per thread), so a slice
-    // spanning hundreds of sparse segments costs no per-segment round trip.
-    uint32_t sg = m.seg_of(min(lo + threadIdx.x, hi > 0 ? hi - 1 : 0));
-    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
-      const uint32_t e = lo + j;
-      while (sh_pre[sg + 1] <= e) ++sg;
-      const size_t src = (size_t)sg * m.cap + (e - sh_pre[sg]);
-      __pipeline_memcpy_async(st_val + j, a.cand_val + src, sizeof(T));
-      __pipeline_memcpy_async(st_idx + j, a.cand_idx + src, 4);
+  if (cnt) {
+    uint32_t* win = sh_h;  // logical prefix of the window's tiles (kWin + 1 entries)
+    unsigned long long pre = lo;
+    for (uint32_t ws = tb; ws < te; ws += kWin) {
+      const uint32_t nwin = min(kWin, te - ws);
+      {
+        const uint32_t per = (nwin + blockDim.x - 1) / blockDim.x;
+        const uint32_t i0 = min(nwin, threadIdx.x * per), i1 = min(nwin, i0 + per);
+        unsigned long long loc = 0;
+        for (uint32_t i = i0; i < i1; ++i) loc += __ldcg(a.tile_cnt + ws + i);
+        unsigned long long tot;
+        unsigned long long r0 = pre + block_exscan_u64(loc, sh_warp, &tot);
+        for (uint32_t i = i0; i < i1; ++i) {
+          win[i] = (uint32_t)r0;
+          r0 += __ldcg(a.tile_cnt + ws + i);
+        }
+        if (threadIdx.x == 0) win[nwin] = (uint32_t)(pre + tot);
+        pre += tot;
+      }
+      __syncthreads();
+      const uint32_t e_lo = max(lo, win[0]), e_hi = min(hi, win[nwin]);
+      if (e_lo < e_hi) {
+        // thread-strided entries (coalesced inside a tile); each entry finds
+        // its tile by binary search (a forward walk would cross thousands of
+        // near-empty tiles per step in sparse stretches of the index space)
+        for (uint32_t e = e_lo + threadIdx.x; e < e_hi; e += blockDim.x) {
+          uint32_t l = 0, h = nwin;  // win[l] <= e < win[h]
+          while (h - l > 1) {
+            const uint32_t m = (l + h) >> 1;
+            if (win[m] <= e) l = m;
+            else h = m;
+          }
+          const size_t src = (size_t)(ws + l) * TILE + (e - win[l]);
+          const uint32_t j = e - lo;
+          if (staged) {
+            __pipeline_memcpy_async(st_idx + j, a.seg_idx + src, 4);
+            __pipeline_memcpy_async(st_val + j, a.seg_val + src, sizeof(T));
+          } else {
+            a.cand_idx[e] = a.seg_idx[src];
+            a.cand_val[e] = a.seg_val[src];
+          }
+        }
+      }
+      __syncthreads();  // the window is rewritten next
     }
-    __pipeline_commit();
-    __pipeline_wait_prior(0);
+    if (staged) {
+      __pipeline_commit();
+      __pipeline_wait_prior(0);
+    }
   }
   __syncthreads();
   phase();
@@ -168,13 +253,11 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
         if (want_idx) id[c] = j0 + c < cnt ? st_idx[j0 + c] : 0u;
       }
     } else {
-      uint32_t sg = j0 < cnt ? m.seg_of(lo + j0) : 0;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         if (j0 + c < cnt) {
-          const size_t p = m.phys(lo + j0 + c, &sg);
-          v[c] = a.cand_val[p];
-          if (want_idx) id[c] = a.cand_idx[p];
+          v[c] = a.cand_val[lo + j0 + c];
+          if (want_idx) id[c] = a.cand_idx[lo + j0 + c];
         } else {
           v[c] = T(0);
           if (want_idx) id[c] = 0u;
@@ -325,10 +408,13 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
     block_exscan_u64(part, sh_warp, &total);
     if (threadIdx.x == 0) sh_base = total;
   }
-  // every CTA has read the level histograms: clear them for the next call
+  // every CTA has read the level histograms and the superblock sums: clear
+  // them for the next call
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < kNumLevelHists * kLevelHist;
        b += gridDim.x * blockDim.x)
     a.hlev[b] = 0;
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < 3 * a.sb_stride; b += gridDim.x * blockDim.x)
+    a.sb[b] = 0;
   if (blockIdx.x == 0) {
     if (threadIdx.x == 0) {
       s->prefix = T_key;  // diagnostics (psb_topk_stats)

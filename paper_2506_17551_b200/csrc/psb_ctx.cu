@@ -87,7 +87,6 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
     c->direct_mode = m == 4;
   }
   if (const char* sm = getenv("PSB_STEP_MARKS")) c->marks_on = sm[0] != '0';
-  if (const char* sn = getenv("PSB_SCAN_TMA")) c->scan_tma = sn[0] != '0';
   if (const char* qt = getenv("PSB_Q8_NO_TMA")) c->q8_no_tma = qt[0] != '0';
   if (const char* qu = getenv("PSB_Q8_UNFUSED")) c->q8_unfused = qu[0] != '0';
   if (const char* vc = getenv("PSB_APPLY_VCAP")) c->apply_vcap = (uint32_t)std::min(16384l, std::max(0l, atol(vc))) & ~1u;
@@ -114,11 +113,15 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   ALLOC(c->d_hist1, sizeof(uint32_t) * PSB_HIST_BINS);
   ALLOC(c->d_histr, sizeof(uint32_t) * PSB_HIST_BINS * 10);  // k_cand level histograms
   ALLOC(c->d_histd, sizeof(uint32_t) * 16384);
-  ALLOC(c->d_seg_cnt, sizeof(uint32_t) * PSB_FINAL_TPC_MAX);
-  ALLOC(c->d_cta, sizeof(unsigned long long) * PSB_FINAL_TPC_MAX);
+  ALLOC(c->d_tile_cnt, sizeof(uint32_t) * ntiles);
+  c->sb_stride = (uint32_t)((ntiles >> PSB_SB_SHIFT) + 1);
+  ALLOC(c->d_sb, sizeof(uint32_t) * 3 * c->sb_stride);
+  ALLOC(c->d_cta, sizeof(unsigned long long) * 2 * PSB_MAX_CTAS);  // (gt, eq) totals | tile-chunk sums
   ALLOC(c->d_stage_idx, sizeof(uint32_t) * stage_cap);
   c->stage_val_bytes = sizeof(double) * stage_cap;
   ALLOC(c->d_stage_val, c->stage_val_bytes);
+  ALLOC(c->d_list_idx, sizeof(uint32_t) * stage_cap);
+  ALLOC(c->d_list_val, c->stage_val_bytes);
   // segment table: smallest segment is 64 entries (P*S*8 + 4S <= 96 KB, P <= 32)
   c->seg_cap = (size_t)max_workers * (max_n / 64 + 2);
   ALLOC(c->d_seg_off, sizeof(uint32_t) * c->seg_cap);
@@ -152,7 +155,7 @@ extern "C" void psb_ctx_destroy(psb_ctx* c) {
   cudaDeviceSynchronize();
   psb_peer_destroy(c);
   void* ptrs[] = {c->d_flags,    c->d_tk,        c->d_tw,        c->d_hist1,   c->d_histr,
-                  c->d_seg_cnt,  c->d_cta,       c->d_histd,       c->d_stage_idx, c->d_stage_val,
+                  c->d_tile_cnt, c->d_sb, c->d_cta, c->d_list_idx, c->d_list_val,       c->d_histd,       c->d_stage_idx, c->d_stage_val,
                   c->d_seg_off,  c->d_partials,  c->d_gather,    c->d_work,    c->d_qmean,   c->d_mom_mean};
   for (void* p : ptrs)
     if (p) cudaFree(p);

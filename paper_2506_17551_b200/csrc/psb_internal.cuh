@@ -16,7 +16,7 @@
 #define PSB_HIST_BINS 4096    // widest radix digit (12 bits)
 #define PSB_SCAN_THREADS 256  // K1 scan CTA size
 #define PSB_ITEMS 16          // elements per thread per K1 tile (f32)
-#define PSB_FINAL_TPC_MAX 2048  // max tiles per CTA and CTAs of k_final_count
+#define PSB_MAX_CTAS 2048  // max CTAs of the cooperative candidate phase
 
 // ------------------------------------------------------------------ K1 state
 // Per-call scratch of the top-k selection (reset by k_topk_begin every call).
@@ -38,7 +38,13 @@ struct TopkScratch {
   unsigned long long z_key;       // pass A pre-zeroes the residual of keys >= z_key (>= g_key)
   unsigned long long g_key2;      // second-chance threshold after a miss (< g_key; 0 = none)
   unsigned long long phase_ns[16];  // k_cand phase timestamps (globaltimer, CTA 0)
+  uint32_t tile_ctr[4];             // dynamic tile counters of the scan passes (A, S, D, A2)
+  uint32_t list_pass;               // scan pass whose tile segments hold the final list (0 A, 1 S, 2 D)
 };
+
+// K1 tiles per superblock: k_scan sums the tile counts per superblock so the
+// candidate phase can locate its slice of the list without a grid barrier.
+#define PSB_SB_SHIFT 6
 
 // candidates / k band of the prediction-margin controller (psb_cand.inl)
 #ifndef PSB_RATIO_LO
@@ -82,9 +88,13 @@ struct psb_ctx {
   uint32_t* d_hist1 = nullptr;   // level-1 histogram
   uint32_t* d_histr = nullptr;   // refine-level histogram
   uint32_t* d_histd = nullptr;   // (key - G) histogram of the predicted mode
-  uint32_t* d_seg_cnt = nullptr;          // candidates per k_scan CTA segment
+  uint32_t* d_tile_cnt = nullptr;          // candidates per K1 tile (segment) of the scan passes
+  uint32_t* d_sb = nullptr;                // [3][sb_stride] superblock sums of the tile counts (passes A, S, D)
+  uint32_t sb_stride = 0;
   unsigned long long* d_cta = nullptr;    // per-CTA totals / prefixes
-  uint32_t* d_stage_idx = nullptr;  // candidate staging, tile-segmented, capacity max_n
+  uint32_t* d_stage_idx = nullptr;  // tile-segmented candidates written by k_scan, capacity max_n
+  uint32_t* d_list_idx = nullptr;   // the same, contiguous (k_cand's prologue), capacity max_n
+  void* d_list_val = nullptr;
   void* d_stage_val = nullptr;      // f64 capacity
   size_t stage_val_bytes = 0;
   // apply scratch
@@ -105,7 +115,6 @@ struct psb_ctx {
   int prof = 0;
   int predict = 1;  // K1 threshold prediction (PSB_NO_PREDICT=1 disables)
   uint32_t apply_vcap = 2048;  // PSB_APPLY_VCAP: staged entries per apply segment
-  int scan_tma = 0;  // PSB_SCAN_TMA=1: K1 streaming pass through a TMA stage ring (measured slower)
   int q8_no_tma = 0;   // PSB_Q8_NO_TMA=1: register double-buffer kernel for the one-worker q8 step
   int q8_unfused = 0;  // PSB_Q8_UNFUSED=1: single-rank q8 step as quant + reduce (diagnostics)
   // NVLink peer exchange (psb_peer.cu)

@@ -44,6 +44,7 @@
 #include <cuda_pipeline.h>
 
 #include "psb_internal.cuh"
+#include "psb_debug.h"
 
 namespace cg = cooperative_groups;
 
@@ -99,9 +100,10 @@ struct ScanArgs {
   TopkScratch* s;
   TopkWorker* w;
   uint32_t* hist1;
-  uint32_t tpc;       // tiles per CTA: CTA b streams tiles [b*tpc, (b+1)*tpc)
-  uint32_t* seg_cnt;  // candidates written by CTA b (segment b of the list)
-  uint32_t* cand_idx;
+  uint32_t* tile_cnt;      // candidates of tile t (segment t of the list)
+  uint32_t* sb;            // [3][sb_stride] superblock sums of tile_cnt (passes A, S, D)
+  uint32_t sb_stride;
+  uint32_t* cand_idx;      // tile-segmented candidates: tile t's at [t*TILE, t*TILE + tile_cnt[t])
   T* cand_val;
   uint32_t* flags;
 };
@@ -212,6 +214,7 @@ __global__ void k_topk_begin(TopkScratch* s, TopkWorker* w, uint32_t* hist1, uin
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < 8; ++i) s->done[i] = 0;
+    for (int i = 0; i < 4; ++i) s->tile_ctr[i] = 0;
     s->b1 = 0;
     s->need_full_hist = 0;
     s->need_compact = 0;
@@ -233,34 +236,34 @@ __global__ void k_topk_begin(TopkScratch* s, TopkWorker* w, uint32_t* hist1, uin
 }
 
 // ------------------------------------------------------------------ scan
-// TMA=true (opt-in, PSB_SCAN_TMA=1; MODE_A with EF, 16-byte aligned): one
-// elected thread streams the CTA's full tiles of g and r into a ring of
-// kScanStages shared-memory stages with 1-D bulk copies (mbarrier
-// complete_tx).  Measured slower than the register path at 125M (285 vs
-// 276 us): the ring halves the resident CTAs and this pass is bound by its
-// per-tile compaction, not by bytes in flight.  Everything else is identical.
-constexpr int kScanStages = 2;
+// Work distribution: tiles are handed out dynamically (one atomic per tile,
+// taken one tile ahead so its latency and the next tile's L2 prefetch overlap
+// the current tile).  A static contiguous range per CTA left the pass
+// tail-bound: with 4 CTAs per SM sharing issue slots unevenly, CTAs with
+// equal work ended between 204 and 271 us at 125M (tools/probe_scan_trace.py).
+// Each tile compacts its candidates, in index order, into its own segment of
+// the list (t*TILE, capacity TILE) and records the count; k_cand turns the
+// segments into one contiguous list (grid-wide prefix over the tile counts).
+// (A decoupled look-back writing the contiguous list directly from here was
+// measured 3x slower: with ~600 tiles in flight every tile waits for its
+// predecessors' counts.)
 #ifndef PSB_PF
-#define PSB_PF 1  // L2 prefetch distance of the streaming pass, in tiles
+#define PSB_PF 1  // L2 prefetch of the next tile (tools: PSB_PF=0 disables)
 #endif
 
-template <class T, int MODE, bool TMA = false>
+template <class T, int MODE>
 __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
   typedef KeyOf<T> KO;
   typedef typename KO::K K;
   constexpr int VW = VecOf<T>::W;
   constexpr int TILE = tile_elems<T>();
   constexpr int SH1 = KO::shift(0);
-  constexpr uint32_t kTileBytes = TILE * sizeof(T);
-  extern __shared__ __align__(128) unsigned char scan_smem[];
-  T* st_g = reinterpret_cast<T*>(scan_smem);   // [kScanStages][TILE]
-  T* st_r = st_g + (size_t)kScanStages * TILE;  // [kScanStages][TILE]
-  __shared__ __align__(8) uint64_t sh_full[TMA ? kScanStages : 1];
 
   __shared__ uint32_t sh_hist[PSB_HIST_BINS];
   __shared__ unsigned long long sh_warp[32];
   __shared__ uint32_t sh_nonfinite;
   __shared__ LevelResult sh_res;
+  __shared__ uint32_t sh_tile[2];
 
   // compact: keep key >= gk.  hist: level-1 histogram of every element.
   K gk = 0;
@@ -289,88 +292,39 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
   // >= z (the predicted T without margin; predicted mode, EF pass only)
   const bool spec = MODE == MODE_A && compact && a.s->spec_ok;
   const K zk = (K)a.s->z_key;
+  constexpr int slot = MODE == MODE_A ? 0 : (MODE == MODE_S ? 1 : (MODE == MODE_D ? 2 : 3));
+  uint32_t* ctr = &a.s->tile_ctr[slot];
+  uint32_t* sbp = a.sb + (size_t)(slot < 3 ? slot : 0) * a.sb_stride;
 
   if (hist)
     for (int b = threadIdx.x; b < PSB_HIST_BINS; b += blockDim.x) sh_hist[b] = 0;
-  if (threadIdx.x == 0) sh_nonfinite = 0;
+  if (threadIdx.x == 0) {
+    sh_nonfinite = 0;
+    sh_tile[0] = atomicAdd(ctr, 1u);
+  }
   __syncthreads();
 
   uint32_t nonfinite = 0;
   const T* __restrict__ src = (MODE == MODE_A) ? a.g : a.p;
   T* __restrict__ rr = a.r;
-
-  // CTA b streams a contiguous tile range in index order and appends its
-  // candidates to its own segment (capacity = its element count).
-  const uint32_t t_lo = blockIdx.x * a.tpc;
-  const uint32_t t_hi = min(a.ntiles, t_lo + a.tpc);
-  const size_t seg_base = (size_t)t_lo * TILE;
-  // TMA ring: tiles [t_lo, t_full) are full and streamed through shared memory
-  const uint32_t t_full = TMA ? min(t_hi, (uint32_t)(a.n / TILE)) : t_lo;
-  auto issue = [&](uint32_t tile) {
-    const int sidx = (int)((tile - t_lo) % kScanStages);
-    const size_t base = (size_t)tile * TILE;
-    mbar_expect_tx(&sh_full[sidx], 2 * kTileBytes);
-    tma_load_1d(st_g + (size_t)sidx * TILE, src + base, kTileBytes, &sh_full[sidx]);
-    tma_load_1d(st_r + (size_t)sidx * TILE, rr + base, kTileBytes, &sh_full[sidx]);
-  };
-  if (TMA) {
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < kScanStages; ++i) mbar_init(&sh_full[i], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  auto prefetch_tile = [&](uint32_t t2) {
+    if (PSB_PF && MODE == MODE_A && a.vec_ok && t2 < a.ntiles && (size_t)(t2 + 1) * TILE <= a.n) {
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + (size_t)t2 * TILE),
+                   "r"((uint32_t)(TILE * sizeof(T))) : "memory");
+      if (rr != nullptr)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rr + (size_t)t2 * TILE),
+                     "r"((uint32_t)(TILE * sizeof(T))) : "memory");
     }
-    __syncthreads();
-    if (threadIdx.x == 0)
-      for (uint32_t t = t_lo; t < t_full && t < t_lo + kScanStages; ++t) issue(t);
-  }
-  uint32_t run = 0;  // candidates appended so far (uniform across the CTA)
-  for (uint32_t tile = t_lo; tile < t_hi; ++tile) {
+  };
+  if (threadIdx.x == 0) prefetch_tile(sh_tile[0]);
+  unsigned long long run = 0;  // candidates written by this CTA
+  int cur = 0;
+  for (uint32_t tile = sh_tile[0]; tile < a.ntiles; tile = sh_tile[cur]) {
     const size_t base = (size_t)tile * TILE;
     const bool full = a.vec_ok && (base + TILE <= a.n);
     T x[4][VW];
     uint32_t valid = 0;
-    if (TMA && tile < t_full) {
-      // p = r + g from the staged tile; residual out (speculative +0) to global
-      const uint32_t li = tile - t_lo;
-      const int sidx = (int)(li % kScanStages);
-      mbar_wait(&sh_full[sidx], (li / kScanStages) & 1u);
-      const T* sg = st_g + (size_t)sidx * TILE;
-      const T* sr = st_r + (size_t)sidx * TILE;
-      valid = 0xffffu;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int o = (j * PSB_SCAN_THREADS + threadIdx.x) * VW;
-        T gv[VW], rv[VW], out[VW];
-        ld_vec(sg + o, gv);
-        ld_vec(sr + o, rv);
-#pragma unroll
-        for (int c = 0; c < VW; ++c) {
-          x[j][c] = add_rn(rv[c], gv[c]);
-          out[c] = (spec && KO::key(x[j][c]) >= zk) ? T(0) : x[j][c];
-        }
-        st_vec_stream(rr + base + o, out);
-      }
-      __syncthreads();  // every thread has read stage sidx: refill it
-      if (threadIdx.x == 0 && tile + kScanStages < t_full) issue(tile + kScanStages);
-    } else if (!TMA && MODE == MODE_A && threadIdx.x == 0 && a.vec_ok) {
-      // TMA bulk prefetch into L2, PSB_PF tiles ahead (the first tile also
-      // primes the ones before): those loads then hit L2 while this tile's
-      // scan and stores run
-      auto pf = [&](uint32_t t2) {
-        if (t2 < t_hi && (size_t)(t2 + 1) * TILE <= a.n) {
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + (size_t)t2 * TILE),
-                       "r"((uint32_t)(TILE * sizeof(T))) : "memory");
-          if (rr != nullptr)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rr + (size_t)t2 * TILE),
-                         "r"((uint32_t)(TILE * sizeof(T))) : "memory");
-        }
-      };
-      if (tile == t_lo)
-        for (uint32_t d = 1; d < PSB_PF; ++d) pf(tile + d);
-      pf(tile + PSB_PF);
-    }
-    if (TMA && tile < t_full) {
-      // staged above
-    } else if (full) {
+    if (full) {
       valid = 0xffffu;
       if (MODE == MODE_A && rr != nullptr) {
         T gv[4][VW], rv[4][VW];
@@ -379,6 +333,11 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
           const size_t e = base + (size_t)(j * PSB_SCAN_THREADS + threadIdx.x) * VW;
           ld_vec_stream(src + e, gv[j]);
           ld_vec_stream(rr + e, rv[j]);  // evict-first: keep L2 for the candidate list
+        }
+        if (threadIdx.x == 0) {  // next tile: its grab and L2 prefetch overlap this tile
+          const uint32_t nt = atomicAdd(ctr, 1u);
+          sh_tile[cur ^ 1] = nt;
+          prefetch_tile(nt);
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -397,8 +356,14 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
           const size_t e = base + (size_t)(j * PSB_SCAN_THREADS + threadIdx.x) * VW;
           ld_vec(src + e, x[j]);
         }
+        if (threadIdx.x == 0) {
+          const uint32_t nt = atomicAdd(ctr, 1u);
+          sh_tile[cur ^ 1] = nt;
+          prefetch_tile(nt);
+        }
       }
     } else {
+      if (threadIdx.x == 0) sh_tile[cur ^ 1] = atomicAdd(ctr, 1u);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
 #pragma unroll
@@ -445,7 +410,7 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
         packed |= (unsigned long long)__popc((fl >> (j * VW)) & ((1u << VW) - 1u)) << (16 * j);
       unsigned long long tot;
       const unsigned long long ex = block_exscan_u64(packed, sh_warp, &tot);
-      uint32_t acc = run;
+      uint32_t acc = 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         uint32_t pos = acc + (uint32_t)((ex >> (16 * j)) & 0xffffu);
@@ -454,24 +419,28 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
         for (int c = 0; c < VW; ++c) {
           if ((fl >> (j * VW + c)) & 1u) {
             const size_t e = base + (size_t)(j * PSB_SCAN_THREADS + threadIdx.x) * VW + c;
-            a.cand_idx[seg_base + pos] = (uint32_t)e;
-            a.cand_val[seg_base + pos] = x[j][c];
+            a.cand_idx[base + pos] = (uint32_t)e;
+            a.cand_val[base + pos] = x[j][c];
             ++pos;
           }
         }
       }
-      run = acc;
+      if (threadIdx.x == 0) {
+        a.tile_cnt[tile] = acc;
+        if (acc) atomicAdd(sbp + (tile >> PSB_SB_SHIFT), acc);
+      }
+      run += acc;
+    } else {
+      __syncthreads();  // sh_tile[cur ^ 1] visible
     }
+    cur ^= 1;
   }
 
   if (nonfinite) sh_nonfinite = 1;
   __syncthreads();
   if (threadIdx.x == 0) {
     if (sh_nonfinite) atomicOr(a.flags, 1u);
-    if (compact) {
-      a.seg_cnt[blockIdx.x] = run;
-      if (run) atomicAdd(&a.s->cand_count, (unsigned long long)run);
-    }
+    if (compact && run) atomicAdd(&a.s->cand_count, run);
   }
   if (hist) {
     for (int b = threadIdx.x; b < PSB_HIST_BINS; b += blockDim.x) {
@@ -479,7 +448,7 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
       if (h) atomicAdd(&a.hist1[b], h);
     }
   }
-  if (MODE == MODE_D) return;  // k_cand prefix-sums the segment counts itself
+  if (MODE == MODE_D) return;  // k_cand reads cand_count after the kernel boundary
 
   if (!last_block(&a.s->done[MODE == MODE_A ? DONE_A : MODE == MODE_S ? DONE_S : DONE_A2])) return;
 
@@ -490,6 +459,7 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
     const unsigned long long C = __ldcg(&a.s->cand_count);
     if (threadIdx.x == 0) {
       if (C >= k) {
+        a.s->list_pass = 1;
         a.s->g_key = a.s->g_key2;
         a.s->spec_ok = 0;
         a.s->start_level = 0;
@@ -509,6 +479,7 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
     const unsigned long long C = __ldcg(&a.s->cand_count);
     if (C >= k) {
       if (threadIdx.x == 0) {
+        a.s->list_pass = 0;
         a.s->start_level = 0;
         a.s->prefix = 0;
         a.s->need = k;
@@ -543,30 +514,50 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
       a.s->match = n - R.total;
     }
     a.s->start_level = 1;
+    a.s->list_pass = 2;
     a.s->need_compact = 1;
     a.s->cand_count = 0;
     if (MODE == MODE_A) a.w->calls += 1;
   }
 }
 
-template <class T, int MODE, bool TMA = false>
+#ifdef PSB_SCAN_TRACE
+// diagnostics build only: globaltimer at entry / exit of every k_scan<MODE_A> CTA
+__device__ unsigned long long g_scan_trace[2 * 4096];
+#endif
+
 #ifndef PSB_SCAN_MINB
 #define PSB_SCAN_MINB 4
 #endif
+template <class T, int MODE>
 __global__ void __launch_bounds__(PSB_SCAN_THREADS, PSB_SCAN_MINB) k_scan(ScanArgs<T> a) {
-  scan_body<T, MODE, TMA>(a);
+#ifdef PSB_SCAN_TRACE
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
+  scan_body<T, MODE>(a);
+#ifdef PSB_SCAN_TRACE
+  if (MODE == MODE_A && threadIdx.x == 0 && blockIdx.x < 4096) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    g_scan_trace[2 * blockIdx.x] = t0;
+    g_scan_trace[2 * blockIdx.x + 1] = t1;
+  }
+#endif
 }
 
 // Prediction missed: pass A speculatively stored +0 for its candidates; put p
-// back (segment b holds exactly those written by k_scan CTA b) before the
-// cold path re-reads p from r.
+// back (tile t's segment holds exactly those of tile t) before the second
+// chance re-reads p from r.
 template <class T>
 __device__ __forceinline__ void restore_body(const ScanArgs<T>& a) {
   constexpr int TILE = tile_elems<T>();
   if (!ld_flag(&a.s->need_full_hist) || !a.s->spec_ok || a.r == nullptr) return;
-  const size_t base = (size_t)blockIdx.x * a.tpc * TILE;
-  const uint32_t cnt = a.seg_cnt[blockIdx.x];
-  for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) a.r[a.cand_idx[base + j]] = a.cand_val[base + j];
+  for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    const uint32_t cnt = __ldcg(a.tile_cnt + t);
+    const size_t base = (size_t)t * TILE;
+    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) a.r[a.cand_idx[base + j]] = a.cand_val[base + j];
+  }
 }
 
 template <class T>
@@ -574,9 +565,9 @@ __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_restore(ScanArgs<T> a) {
   restore_body(a);
 }
 
-// The miss / cold fallback (restore, full level-1 histogram, compaction) as
-// ONE cooperative launch on the k_scan grid (co-resident): in steady state it
-// is a single node that exits at once instead of three.
+// The miss / cold fallback (restore, second chance, full level-1 histogram,
+// compaction) as ONE cooperative launch on the k_scan grid (co-resident): in
+// steady state it is a single node that exits at once instead of four.
 template <class T>
 __global__ void __launch_bounds__(PSB_SCAN_THREADS) k_fallback(ScanArgs<T> a) {
   cg::grid_group grid = cg::this_grid();
@@ -617,26 +608,16 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   a.s = s;
   a.w = w;
   a.hist1 = c->d_hist1;
-  // TMA streaming (EF, aligned): as many CTAs per SM as the stage ring allows
-  const bool tma = r != nullptr && vec_ok && c->scan_tma && (size_t)ntiles >= (size_t)c->num_sms;
-  const size_t tma_smem = (size_t)2 * kScanStages * TILE * sizeof(T);
-  int per_sm = PSB_SCAN_MINB;
-  if (tma) {
-    cudaFuncSetAttribute(k_scan<T, MODE_A, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem);
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_scan<T, MODE_A, true>, PSB_SCAN_THREADS, tma_smem);
-    per_sm = std::max(1, occ);
-  }
-  const uint32_t scan_grid0 = (uint32_t)std::min<size_t>(ntiles, (size_t)c->num_sms * per_sm);
-  a.tpc = (ntiles + scan_grid0 - 1) / scan_grid0;
-  const uint32_t scan_grid = (ntiles + a.tpc - 1) / a.tpc;
-  a.seg_cnt = c->d_seg_cnt;
+  a.tile_cnt = c->d_tile_cnt;
+  a.sb = c->d_sb;
+  a.sb_stride = c->sb_stride;
+  // persistent-style grid: PSB_SCAN_MINB CTAs per SM pull tiles dynamically
+  const uint32_t scan_grid = (uint32_t)std::min<size_t>(ntiles, (size_t)c->num_sms * PSB_SCAN_MINB);
   a.cand_idx = c->d_stage_idx;
   a.cand_val = reinterpret_cast<T*>(c->d_stage_val);
   a.flags = c->d_flags;
   if (c->prof) cudaEventRecord(psb_prof_event(c), st);
-  if (tma) k_scan<T, MODE_A, true><<<scan_grid, PSB_SCAN_THREADS, tma_smem, st>>>(a);
-  else k_scan<T, MODE_A><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
+  k_scan<T, MODE_A><<<scan_grid, PSB_SCAN_THREADS, 0, st>>>(a);
   if (c->prof) cudaEventRecord(psb_prof_event(c), st);
   // fallback: one cooperative node when the k_scan grid is co-resident
   int fb_occ = 0;
@@ -660,11 +641,14 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   b.s = s;
   b.w = w;
   b.hlev = c->d_histr;
-  b.cand_idx = c->d_stage_idx;
-  b.cand_val = reinterpret_cast<const T*>(c->d_stage_val);
-  b.seg_cnt = c->d_seg_cnt;
-  b.nseg = scan_grid;
-  b.seg_cap = (size_t)a.tpc * TILE;
+  b.seg_idx = c->d_stage_idx;
+  b.seg_val = reinterpret_cast<const T*>(c->d_stage_val);
+  b.tile_cnt = c->d_tile_cnt;
+  b.sb = c->d_sb;
+  b.sb_stride = c->sb_stride;
+  b.ntiles = ntiles;
+  b.cand_idx = c->d_list_idx;
+  b.cand_val = reinterpret_cast<T*>(c->d_list_val);
   b.cta = c->d_cta;
   b.idx_out = idx_out;
   b.val_out = val_out;
@@ -806,4 +790,17 @@ extern "C" psb_status psb_topk_stats(psb_ctx* c, int worker, uint64_t* out8) {
   out8[6] = ((uint64_t)w.misses << 32) | w.calls;
   out8[7] = fbits;          // margin factor f for the next call
   return PSB_OK;
+}
+
+// diagnostics (psb_debug.h): per-CTA entry/exit timestamps of the last
+// k_scan<MODE_A> launch in a -DPSB_SCAN_TRACE build; returns 0 otherwise
+extern "C" PSB_API int psb_debug_scan_trace(unsigned long long* out, int max_ctas) {
+#ifdef PSB_SCAN_TRACE
+  const int m = max_ctas < 4096 ? max_ctas : 4096;
+  return cudaMemcpyFromSymbol(out, g_scan_trace, sizeof(unsigned long long) * 2 * m) == cudaSuccess ? m : -1;
+#else
+  (void)out;
+  (void)max_ctas;
+  return 0;
+#endif
 }

@@ -124,17 +124,26 @@ extern "C" psb_status psb_wire_decode_topk(psb_ctx* c, psb_dtype dt, const void*
   unsigned long long* hdr = reinterpret_cast<unsigned long long*>(c->d_flags + 8);  // 2 x u64 scratch
   const uint8_t* i8 = reinterpret_cast<const uint8_t*>(in);
   const size_t work = nbytes >= 16 ? (nbytes - 16) / 16 : 1;
+  // the decoder reports through its own flag word (d_flags[4]), so the
+  // sticky step flags (d_flags[0]: non-finite, peer timeout) stay untouched
+  // for the caller's next psb_check
+  uint32_t* dflag = c->d_flags + 4;
+  CUDA_TRY(c, cudaMemsetAsync(dflag, 0, sizeof(uint32_t), st), "psb_wire_decode_topk");
   if (dt == PSB_F32)
-    k_wire_decode_topk<float><<<grid_for(c, work), 256, 0, st>>>(i8, nbytes, k_cap, idx, (float*)val, hdr, c->d_flags);
+    k_wire_decode_topk<float><<<grid_for(c, work), 256, 0, st>>>(i8, nbytes, k_cap, idx, (float*)val, hdr, dflag);
   else
     k_wire_decode_topk<double><<<grid_for(c, work), 256, 0, st>>>(i8, nbytes, k_cap, idx, (double*)val, hdr,
-                                                                   c->d_flags);
+                                                                   dflag);
   c->launches += 1;
   PSB_LAUNCH_CHECK(c, "psb_wire_decode_topk");
   unsigned long long h[2] = {0, 0};
+  uint32_t f = 0;
   CUDA_TRY(c, cudaMemcpyAsync(h, hdr, sizeof(h), cudaMemcpyDeviceToHost, st), "psb_wire_decode_topk");
-  psb_status s = psb_check(c, stream);  // reports truncation / capacity / range errors
-  if (s) return s;
+  CUDA_TRY(c, cudaMemcpyAsync(&f, dflag, sizeof(f), cudaMemcpyDeviceToHost, st), "psb_wire_decode_topk");
+  CUDA_TRY(c, cudaStreamSynchronize(st), "psb_wire_decode_topk");
+  if (f & 16u) return psb_set_err(c, PSB_EINVAL, "wire_decode: truncated input");
+  if (f & 32u) return psb_set_err(c, PSB_EINVAL, "wire_decode: message exceeds the output capacity");
+  if (f & 64u) return psb_set_err(c, PSB_EINVAL, "wire_decode: index exceeds the 32-bit range");
   *dim_out = h[0];
   *count_out = (size_t)h[1];
   return PSB_OK;

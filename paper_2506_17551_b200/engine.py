@@ -334,6 +334,18 @@ class Context:
         _need_cuda(g, r, theta, mean_out, momentum)
         W = g.shape[0] if g.dim() == 2 else 1
         n = g.shape[-1]
+        # the C ABI sees bare pointers: every buffer must have g's dtype and
+        # the shape the step writes through (theta/mean/m: [n], r: [W][n])
+        for name, t, numel in (("theta", theta, n), ("mean_out", mean_out, n), ("momentum", momentum, n),
+                               ("r", r, W * n)):
+            if t is None:
+                continue
+            if t.dtype != g.dtype:
+                raise L.PsbInvalidArgument(f"step_desc: {name} dtype {t.dtype} != gradient dtype {g.dtype}")
+            if t.numel() != numel:
+                raise L.PsbInvalidArgument(f"step_desc: {name} has {t.numel()} elements, expected {numel}")
+        if r is not None and r.dim() == 2 and tuple(r.shape) != (W, n):
+            raise L.PsbInvalidArgument(f"step_desc: r shape {tuple(r.shape)} != ({W}, {n})")
         d = L.StepDesc()
         d.compressor = compressor
         d.dtype = _dtype_code(g)

@@ -181,14 +181,17 @@ def train(users: int, items: int, dim: int, train_users: Sequence[int], train_it
         raise L.PsbInvalidArgument("HyperParams: learning_rate must be > 0")
     if batch_size < P:
         raise L.PsbInvalidArgument("train: batch_size must be >= data_degree")
+    if mode != "sync" and resume is not None and int(resume[2]):
+        raise L.PsbInvalidArgument("train: resume is supported for sync training (async history is not saved)")
     n = (users + items) * dim
-    theta = init_params(users, items, dim, seed if init_seed is None else init_seed)
     sampler = TripleSampler(train_users, train_items, users, items, seed)
     start = 0
     if resume is not None:  # (theta, residuals, steps_done, sampler_state) from the checkpoints
         theta = resume[0].to(torch.float64).clone()
         start = int(resume[2])
         sampler.rng.s = int(resume[3])
+    else:
+        theta = init_params(users, items, dim, seed if init_seed is None else init_seed)
     own = ctx is None
     if own:
         ctx = Context(n, max(top_k, 1), max(P, 1))
@@ -196,8 +199,6 @@ def train(users: int, items: int, dim: int, train_users: Sequence[int], train_it
     res = torch.zeros(P, n, dtype=torch.float64, device="cuda")
     if resume is not None:
         res.copy_(resume[1])
-    if mode != "sync" and resume is not None and start:
-        raise L.PsbInvalidArgument("train: resume is supported for sync training (async history is not saved)")
     grads = torch.empty(P, n, dtype=torch.float64, device="cuda")
     history: deque = deque()
     updates = 0

@@ -131,3 +131,74 @@ def test_payload_exchange_modes(comp, order, W, peer, steps):
     nr = min(torch.cuda.device_count(), 4)
     res = _run(nr, W, comp, order, steps=steps, peer=peer)
     assert all(v == "ok" for v in res.values()), res
+
+
+def _worker_full_size(rank, nranks, uid, comp, q):
+    """Bench size (cfg2: 125M, top-k 1% + EF, pull/wire16 exchange; cfg3:
+    125M dense q8, NCCL all-to-all + all-gather): the multi-rank step must
+    equal, bit for bit, the same P workers run as virtual workers on one GPU
+    -- a path the oracle pins at small sizes (test_apply_gpu.py)."""
+    sys.path.insert(0, ROOT)
+    try:
+        import torch as th
+
+        from paper_2506_17551_b200 import _lib as L
+        from paper_2506_17551_b200.engine import Context, generate
+
+        th.cuda.set_device(rank)
+        n, lr = 125_000_000, 0.05
+        code, k, order = ((L.PSB_COMP_TOPK, n // 100, "ring") if comp == "topk" else (L.PSB_COMP_Q8, 0, "naive"))
+        P = nranks
+        c = Context(n, max(k, 1), P, device=rank)
+        c.comm_init(rank, nranks, uid)
+        g = th.empty(1, n, device="cuda")
+        res = th.zeros(1, n, device="cuda")
+        theta = th.zeros(n, device="cuda")
+        steps = 3
+        for s in range(steps):
+            generate("llmrec", 42, rank, s, n, g[0])
+            c.sync_step(c.step_desc(code, g, res, theta, lr, k, order, 256))
+        c.check()
+        if comp == "topk" and not c.peer_active:
+            q.put((rank, "NVLink peer exchange not active"))
+            return
+        c2 = Context(n, max(k, 1), P, device=rank)
+        g2 = th.empty(P, n, device="cuda")
+        res2 = th.zeros(P, n, device="cuda")
+        theta2 = th.zeros(n, device="cuda")
+        for s in range(steps):
+            for p in range(P):
+                generate("llmrec", 42, p, s, n, g2[p])
+            c2.sync_step(c2.step_desc(code, g2, res2, theta2, lr, k, order, 256))
+        c2.check()
+        if not th.equal(theta.view(th.int32), theta2.view(th.int32)):
+            q.put((rank, "theta differs from the virtual-worker run"))
+            return
+        if not th.equal(res[0].view(th.int32), res2[rank].view(th.int32)):
+            q.put((rank, "residual differs from the virtual-worker run"))
+            return
+        q.put((rank, "ok"))
+        c.close()
+        c2.close()
+    except Exception as e:
+        q.put((rank, f"error: {type(e).__name__}: {e}"))
+
+
+@needs2
+@pytest.mark.parametrize("comp", ["topk", "q8"])
+def test_full_size_multi_rank_equals_virtual_workers(comp):
+    from paper_2506_17551_b200.engine import Context
+    nr = min(torch.cuda.device_count(), 4)
+    uid = Context.unique_id()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_full_size, args=(r, nr, uid, comp, q)) for r in range(nr)]
+    for p in procs:
+        p.start()
+    results = {}
+    for _ in range(nr):
+        r, msg = q.get(timeout=600)
+        results[r] = msg
+    for p in procs:
+        p.join(timeout=60)
+    assert all(v == "ok" for v in results.values()), results
