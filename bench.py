@@ -205,7 +205,9 @@ def ours(args, cfg, world, rank, local_rank):
         from paper_2506_17551_b200.dist import init_comm
         init_comm(ctx)  # NCCL unique id from rank 0 over the process group
 
-    NB = 3  # rotated gradient buffers (each > L2): inputs larger than L2
+    # rotated gradient buffers (each > L2: inputs larger than L2); 8 rather than
+    # 3 so the sequence the threshold predictor sees is not period-3
+    NB = 8
     with torch.cuda.stream(stream):
         grads = [torch.empty(W, n, device=dev) for _ in range(NB)]
         for b in range(NB):

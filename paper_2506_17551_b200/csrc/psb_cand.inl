@@ -27,8 +27,8 @@
 #endif
 constexpr int kCandThreads = PSB_CAND_THREADS;
 static_assert(4096 % kCandThreads == 0 && kCandThreads % 32 == 0, "level histograms are split evenly over the CTA");
-constexpr uint32_t kCoarseBins = 4096;
-constexpr int kCoarseShift = 11;  // 2048-ulp coarse bins: 4095 of them span one octave above G
+constexpr uint32_t kCoarseBins = PSB_COARSE_BINS;
+constexpr int kCoarseShift = PSB_COARSE_SHIFT;  // 2048-ulp coarse bins: 4095 of them span one octave above G
 constexpr uint32_t kLevelHist = 4096;  // words per level histogram buffer
 constexpr int kHistCoarse = 8, kHistFine = 9, kNumLevelHists = 10;  // radix levels use 0..7
 
@@ -37,6 +37,7 @@ struct CandArgs {
   TopkScratch* s;
   TopkWorker* w;
   uint32_t* hlev;  // kNumLevelHists x kLevelHist global histograms (zero between calls)
+  uint32_t* histd; // coarse (key - G) histogram of pass A's candidates, built by k_scan (f32; zero between calls)
   const uint32_t* seg_idx;   // k_scan's tile-segmented candidates (tile t at t*TILE, tile_cnt[t] entries)
   const T* seg_val;
   const uint32_t* tile_cnt;
@@ -86,9 +87,21 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       s->phase_ns[nphase] = t;
     }
+#ifdef PSB_SCAN_TRACE
+    if (threadIdx.x == 0 && blockIdx.x < 1024 && nphase < 15) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_cand_trace[blockIdx.x * 16 + nphase] = t;
+    }
+#endif
     ++nphase;
   };
   phase();
+#ifdef PSB_SCAN_TRACE
+#define TPHASE() phase()
+#else
+#define TPHASE()
+#endif
 
   // ---- this CTA's slice of the index-ordered list, located without a grid
   // barrier.  Slices are whole k_scan tiles [tb, te), balanced on the cost
@@ -148,6 +161,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
     }
   }
   __syncthreads();
+  TPHASE();
   if (threadIdx.x < 64) {  // warp q2 refines boundary q2 to a tile
     const int q2 = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned long long target = q2 ? tgt1 : tgt0;
@@ -187,10 +201,14 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
     }
   }
   __syncthreads();
+  TPHASE();
   const uint32_t lo = sh_be[0], hi = sh_be[1];
   const uint32_t tb = sh_bt[0], te = sh_bt[1];
   const uint32_t cnt = hi - lo;
   const bool staged = cnt <= a.stage_cap;
+#ifdef PSB_SCAN_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cand_trace[blockIdx.x * 16 + 15] = ((unsigned long long)(te - tb) << 32) | cnt;
+#endif
   if (cnt) {
     uint32_t* win = sh_h;  // logical prefix of the window's tiles (kWin + 1 entries)
     unsigned long long pre = lo;
@@ -211,12 +229,14 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
         pre += tot;
       }
       __syncthreads();
-      const uint32_t e_lo = max(lo, win[0]), e_hi = min(hi, win[nwin]);
-      if (e_lo < e_hi) {
-        // thread-strided entries (coalesced inside a tile); each entry finds
-        // its tile by binary search (a forward walk would cross thousands of
-        // near-empty tiles per step in sparse stretches of the index space)
-        for (uint32_t e = e_lo + threadIdx.x; e < e_hi; e += blockDim.x) {
+      // dense windows (>= 32 entries per tile): one warp per tile, lanes copy
+      // the tile's segment; sparse windows: one thread per entry, its tile
+      // found by binary search (a warp per near-empty tile idles its lanes).
+      // 4-byte cp.async into the stage, plain copies into the global list.
+      const uint32_t lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+      const uint32_t w_lo = win[0], w_n = win[nwin] - w_lo;
+      if (w_n < 32u * nwin) {
+        for (uint32_t e = w_lo + threadIdx.x; e < w_lo + w_n; e += blockDim.x) {
           uint32_t l = 0, h = nwin;  // win[l] <= e < win[h]
           while (h - l > 1) {
             const uint32_t m = (l + h) >> 1;
@@ -224,13 +244,27 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
             else h = m;
           }
           const size_t src = (size_t)(ws + l) * TILE + (e - win[l]);
-          const uint32_t j = e - lo;
           if (staged) {
-            __pipeline_memcpy_async(st_idx + j, a.seg_idx + src, 4);
-            __pipeline_memcpy_async(st_val + j, a.seg_val + src, sizeof(T));
+            __pipeline_memcpy_async(st_idx + (e - lo), a.seg_idx + src, 4);
+            __pipeline_memcpy_async(st_val + (e - lo), a.seg_val + src, sizeof(T));
           } else {
             a.cand_idx[e] = a.seg_idx[src];
             a.cand_val[e] = a.seg_val[src];
+          }
+        }
+      } else
+      for (uint32_t i = threadIdx.x >> 5; i < nwin; i += nw) {
+        const uint32_t e0 = win[i], ct = win[i + 1] - e0;
+        const size_t src = (size_t)(ws + i) * TILE;
+        if (staged) {
+          for (uint32_t j = lane; j < ct; j += 32) {
+            __pipeline_memcpy_async(st_idx + (e0 - lo) + j, a.seg_idx + src + j, 4);
+            __pipeline_memcpy_async(st_val + (e0 - lo) + j, a.seg_val + src + j, sizeof(T));
+          }
+        } else {
+          for (uint32_t j = lane; j < ct; j += 32) {
+            a.cand_idx[e0 + j] = a.seg_idx[src + j];
+            a.cand_val[e0 + j] = a.seg_val[src + j];
           }
         }
       }
@@ -238,10 +272,21 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
     }
     if (staged) {
       __pipeline_commit();
+      TPHASE();
       __pipeline_wait_prior(0);
     }
   }
   __syncthreads();
+  if (a.theta != nullptr && staged) {
+    // the fused SGD updates theta at the selected indices: start pulling
+    // those sectors into L2 now, while the threshold is being resolved --
+    // only for the candidates at or above the predicted T (the margin band
+    // below it is mostly not selected; cold mode: all)
+    const bool pz = s->g_key != 0 && !s->need_full_hist && s->spec_ok;
+    const K zk0 = pz ? (K)s->z_key : (K)0;
+    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x)
+      if (KO::key(st_val[j]) >= zk0) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.theta + st_idx[j]));
+  }
   phase();
 
   // Four consecutive entries j0..j0+3 of the slice (j0 local, multiple of 4).
@@ -268,7 +313,6 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   // One histogram pass over the slice (digit(key) for matching keys), flushed
   // into global histogram `g`; then the grid barrier; then every CTA resolves
   // the level from `g`: bin holding the need-th largest (bin 0 implicit).
-  bool pf_theta = a.theta != nullptr && staged;  // first level pass only
   auto level_pass = [&](uint32_t* g, uint32_t nbins, unsigned long long need, unsigned long long match,
                         auto digit_of, uint32_t* bin, unsigned long long* above,
                         unsigned long long* bcnt) {
@@ -278,14 +322,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       const uint32_t j0 = base + 4 * threadIdx.x;
       T v[4];
       uint32_t id[4];
-      load4(j0, v, id, pf_theta);
-      if (pf_theta) {
-        // the fused SGD at the end updates theta at the selected indices:
-        // pull those sectors into L2 while this pass (sync/atomic-bound) runs
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (j0 + c < cnt) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.theta + id[c]));
-      }
+      load4(j0, v, id, false);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t d = 0;
@@ -298,7 +335,6 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       const uint32_t h = sh_h[b];
       if (h) atomicAdd(&g[b], h);
     }
-    pf_theta = false;
     grid.sync();
     phase();
     resolve_level(g, nbins, 1, need, sh_warp, &sh_res, sh_h);
@@ -323,13 +359,22 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
     unsigned long long above, bcnt;
     // coarse digit min((key - G) >> kCoarseShift, 4095): the top bin collects
     // every key an octave or more above G; digit 0 is implicit (C - others).
-    level_pass(a.hlev + kHistCoarse * kLevelHist, kCoarseBins, k, C,
-               [&](K key, uint32_t* d) {
-                 const K dl = (key - G) >> kCoarseShift;
-                 *d = dl < (K)(kCoarseBins - 1) ? (uint32_t)dl : kCoarseBins - 1;
-                 return *d != 0;
-               },
-               &cb, &above, &bcnt);
+    // When the list is pass A's, k_scan already built this histogram while
+    // compacting (no pass, no grid barrier here).
+    if (pass == 0 && a.histd != nullptr) {
+      resolve_level(a.histd, kCoarseBins, 1, k, sh_warp, &sh_res, sh_h);
+      cb = sh_res.found ? sh_res.bin : 0u;
+      above = sh_res.found ? sh_res.above : sh_res.total;
+      bcnt = sh_res.found ? sh_res.cnt : C - sh_res.total;
+    } else {
+      level_pass(a.hlev + kHistCoarse * kLevelHist, kCoarseBins, k, C,
+                 [&](K key, uint32_t* d) {
+                   const K dl = (key - G) >> kCoarseShift;
+                   *d = dl < (K)(kCoarseBins - 1) ? (uint32_t)dl : kCoarseBins - 1;
+                   return *d != 0;
+                 },
+                 &cb, &above, &bcnt);
+    }
     if (cb < kCoarseBins - 1) {
       uint32_t fb;
       unsigned long long fabove, fcnt;
@@ -365,6 +410,87 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   }
   const K T_key = prefix;
   const unsigned long long need_eq = need;
+
+  bool bad = false;
+  auto scatter = [&](uint32_t id, T v, bool sel) {
+    if (sel) {
+      if (a.r && !zeroed(v)) a.r[id] = T(0);  // pass A stored p
+      if (a.theta) {
+        const T mean = mul_rn(v, T(1));  // P = 1: mean = v * (1/1)
+        const T t2 = add_rn(mul_rn(a.coef, mean), a.theta[id]);
+        a.theta[id] = t2;
+        if (a.mean_out) a.mean_out[id] = mean;
+        bad |= !is_finite(t2);
+      }
+    } else if (a.r && zeroed(v)) {
+      a.r[id] = v;  // unselected candidate: undo the speculative +0
+    }
+  };
+  if (staged) {
+    // ---- early scatter: every entry whose key differs from T is decided
+    // (key > T selected, key < T not); only ties at T wait for their
+    // cross-CTA rank.  The theta read-modify-write and the residual fix-ups
+    // -- the random-access part of the phase -- run before the count barrier
+    // and the ordered write.  Batches of U entries per thread issue all their
+    // theta loads before any store (the indices are distinct).
+    constexpr int U = 8;
+    for (uint32_t j0 = threadIdx.x; j0 < cnt; j0 += U * blockDim.x) {
+      uint32_t id[U];
+      T v[U], th[U];
+      uint32_t selm = 0, actm = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t j = j0 + u * blockDim.x;
+        if (j < cnt) {
+          v[u] = st_val[j];
+          const K key = KO::key(v[u]);
+          if (key != T_key) {
+            actm |= 1u << u;
+            id[u] = st_idx[j];
+            if (key > T_key) selm |= 1u << u;
+          }
+        }
+      }
+#ifdef PSB_DIAG_NO_THETA
+      T* const theta_d = nullptr;  // diagnostics build: time the scatter without the theta RMW
+#else
+      T* const theta_d = a.theta;
+#endif
+      if (theta_d) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#ifdef PSB_DIAG_THETA_NOLOAD
+          th[u] = T(0);
+#else
+          if ((selm >> u) & 1u) th[u] = a.theta[id[u]];
+#endif
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!((actm >> u) & 1u)) continue;
+        if ((selm >> u) & 1u) {
+#ifndef PSB_DIAG_NO_RFIX
+          if (a.r && !zeroed(v[u])) a.r[id[u]] = T(0);
+#endif
+          if (theta_d) {
+            const T mean = mul_rn(v[u], T(1));  // P = 1: mean = v * (1/1)
+            const T t2 = add_rn(mul_rn(a.coef, mean), th[u]);
+            
+#ifndef PSB_DIAG_THETA_NOSTORE
+            a.theta[id[u]] = t2;
+#endif
+
+            if (a.mean_out) a.mean_out[id[u]] = mean;
+            bad |= !is_finite(t2);
+          }
+        } else if (a.r && zeroed(v[u])) {
+#ifndef PSB_DIAG_NO_RFIX
+          a.r[id[u]] = v[u];  // unselected candidate: undo the speculative +0
+#endif
+        }
+      }
+    }
+  }
 
   // ---- (gt, eq) counts per CTA; every CTA sums the totals of the CTAs before it.
   // Staged slices: thread t owns the contiguous run [r0, r1) of the slice, so
@@ -415,6 +541,9 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
     a.hlev[b] = 0;
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < 3 * a.sb_stride; b += gridDim.x * blockDim.x)
     a.sb[b] = 0;
+  if (a.histd != nullptr)
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < kCoarseBins; b += gridDim.x * blockDim.x)
+      a.histd[b] = 0;
   if (blockIdx.x == 0) {
     if (threadIdx.x == 0) {
       s->prefix = T_key;  // diagnostics (psb_topk_stats)
@@ -448,26 +577,14 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
   }
   __syncthreads();
 
-  // ---- ordered write.  Loop 1: slots (block scans) and the sequential payload
-  // writes; loop 2 (staged slices): the scattered updates without barriers.
+  // ---- ordered write.  Staged slices: each thread walks its run in index
+  // order (slot = gt_before + min(eq_before, need_eq)), records the slot
+  // relative to the CTA's first one in shared memory and settles its ties;
+  // then the CTA writes its contiguous payload range with coalesced stores.
+  // Unstaged slices: 4 entries per thread per block scan, side effects inline.
   unsigned long long run = sh_base;  // (gt | eq << 32) before this slice
-  bool bad = false;
-  auto scatter = [&](uint32_t id, T v, bool sel) {
-    if (sel) {
-      if (a.r && !zeroed(v)) a.r[id] = T(0);  // pass A stored p
-      if (a.theta) {
-        const T mean = mul_rn(v, T(1));  // P = 1: mean = v * (1/1)
-        const T t2 = add_rn(mul_rn(a.coef, mean), a.theta[id]);
-        a.theta[id] = t2;
-        if (a.mean_out) a.mean_out[id] = mean;
-        bad |= !is_finite(t2);
-      }
-    } else if (a.r && zeroed(v)) {
-      a.r[id] = v;  // unselected candidate: undo the speculative +0
-    }
-  };
   if (staged) {
-    // the thread's run, in index order: slot = gt_before + min(eq_before, need_eq)
+    const unsigned long long s_lo = (run & 0xffffffffull) + min(run >> 32, need_eq);
     unsigned long long before = run + my_ex;
     for (uint32_t j = r0; j < r1; ++j) {
       const T v = st_val[j];
@@ -475,15 +592,19 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       const bool gt = key > T_key, eq = key == T_key;
       const unsigned long long gt_b = before & 0xffffffffull, eq_b = before >> 32;
       const bool sel = gt || (eq && eq_b < need_eq);
-      if (sel) {
-        const unsigned long long slot = gt_b + (eq_b < need_eq ? eq_b : need_eq);
-        a.idx_out[slot] = st_idx[j];
-        a.val_out[slot] = v;
-      }
-      st_slot[j] = sel ? 1u : kNoSlot;
+      st_slot[j] = sel ? (uint32_t)(gt_b + (eq_b < need_eq ? eq_b : need_eq) - s_lo) : kNoSlot;
+      if (eq) scatter(st_idx[j], v, sel);
       before += (unsigned long long)gt | ((unsigned long long)eq << 32);
     }
     run += cta_total;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
+      const uint32_t sl = st_slot[j];
+      if (sl != kNoSlot) {
+        a.idx_out[s_lo + sl] = st_idx[j];
+        a.val_out[s_lo + sl] = st_val[j];
+      }
+    }
   }
   for (uint32_t base = 0; base < (staged ? 0u : cnt); base += 4 * kCandThreads) {
     const uint32_t j0 = base + 4 * threadIdx.x;
@@ -512,10 +633,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
         a.idx_out[slot] = id[c];
         a.val_out[slot] = v[c];
       }
-      if (j0 + c < cnt) {
-        if (staged) st_slot[j0 + c] = sel ? 1u : kNoSlot;
-        else scatter(id[c], v[c], sel);
-      }
+      if (j0 + c < cnt) scatter(id[c], v[c], sel);
       before += (unsigned long long)gt | ((unsigned long long)eq << 32);
     }
     run += tot;
@@ -535,49 +653,6 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       for (int q = 0; q < a.npush; ++q) {
         a.push_idx[q][j] = id;
         a.push_val[q][j] = v;
-      }
-    }
-  }
-  if (staged) {
-    __syncthreads();
-    // batches of U entries per thread: all theta loads of a batch are issued
-    // before any store (the indices are distinct), so U loads per thread are
-    // in flight instead of one dependent round trip per entry
-    constexpr int U = 8;
-    for (uint32_t j0 = threadIdx.x; j0 < cnt; j0 += U * blockDim.x) {
-      uint32_t id[U];
-      T v[U], th[U];
-      uint32_t selm = 0, actm = 0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t j = j0 + u * blockDim.x;
-        if (j < cnt) {
-          actm |= 1u << u;
-          id[u] = st_idx[j];
-          v[u] = st_val[j];
-          if (st_slot[j] != kNoSlot) selm |= 1u << u;
-        }
-      }
-      if (a.theta) {
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if ((selm >> u) & 1u) th[u] = a.theta[id[u]];
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (!((actm >> u) & 1u)) continue;
-        if ((selm >> u) & 1u) {
-          if (a.r && !zeroed(v[u])) a.r[id[u]] = T(0);
-          if (a.theta) {
-            const T mean = mul_rn(v[u], T(1));  // P = 1: mean = v * (1/1)
-            const T t2 = add_rn(mul_rn(a.coef, mean), th[u]);
-            a.theta[id[u]] = t2;
-            if (a.mean_out) a.mean_out[id[u]] = mean;
-            bad |= !is_finite(t2);
-          }
-        } else if (a.r && zeroed(v[u])) {
-          a.r[id[u]] = v[u];  // unselected candidate: undo the speculative +0
-        }
       }
     }
   }

@@ -45,6 +45,10 @@ struct TopkScratch {
 // K1 tiles per superblock: k_scan sums the tile counts per superblock so the
 // candidate phase can locate its slice of the list without a grid barrier.
 #define PSB_SB_SHIFT 6
+// Coarse histogram of (key - G) >> PSB_COARSE_SHIFT over the predicted
+// candidates (2048-ulp bins, the top one collecting an octave and more).
+#define PSB_COARSE_BINS 4096
+#define PSB_COARSE_SHIFT 11
 
 // candidates / k band of the prediction-margin controller (psb_cand.inl)
 #ifndef PSB_RATIO_LO

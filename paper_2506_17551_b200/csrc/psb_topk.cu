@@ -103,6 +103,7 @@ struct ScanArgs {
   uint32_t* tile_cnt;      // candidates of tile t (segment t of the list)
   uint32_t* sb;            // [3][sb_stride] superblock sums of tile_cnt (passes A, S, D)
   uint32_t sb_stride;
+  uint32_t* histd;         // pass A (f32): coarse (key - G) histogram of the candidates, for k_cand
   uint32_t* cand_idx;      // tile-segmented candidates: tile t's at [t*TILE, t*TILE + tile_cnt[t])
   T* cand_val;
   uint32_t* flags;
@@ -292,11 +293,15 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
   // >= z (the predicted T without margin; predicted mode, EF pass only)
   const bool spec = MODE == MODE_A && compact && a.s->spec_ok;
   const K zk = (K)a.s->z_key;
+  // pass A in predicted mode (f32) also histograms its candidates' coarse
+  // digit (key - G) >> PSB_COARSE_SHIFT, so k_cand resolves that level
+  // without a pass of its own
+  const bool chist = MODE == MODE_A && compact && sizeof(T) == 4 && a.histd != nullptr;
   constexpr int slot = MODE == MODE_A ? 0 : (MODE == MODE_S ? 1 : (MODE == MODE_D ? 2 : 3));
   uint32_t* ctr = &a.s->tile_ctr[slot];
   uint32_t* sbp = a.sb + (size_t)(slot < 3 ? slot : 0) * a.sb_stride;
 
-  if (hist)
+  if (hist || chist)
     for (int b = threadIdx.x; b < PSB_HIST_BINS; b += blockDim.x) sh_hist[b] = 0;
   if (threadIdx.x == 0) {
     sh_nonfinite = 0;
@@ -422,6 +427,10 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
             a.cand_idx[base + pos] = (uint32_t)e;
             a.cand_val[base + pos] = x[j][c];
             ++pos;
+            if (chist) {
+              const K dl = (KO::key(x[j][c]) - gk) >> PSB_COARSE_SHIFT;
+              atomicAdd(&sh_hist[dl < (K)(PSB_COARSE_BINS - 1) ? (uint32_t)dl : PSB_COARSE_BINS - 1], 1u);
+            }
           }
         }
       }
@@ -442,10 +451,11 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
     if (sh_nonfinite) atomicOr(a.flags, 1u);
     if (compact && run) atomicAdd(&a.s->cand_count, run);
   }
-  if (hist) {
-    for (int b = threadIdx.x; b < PSB_HIST_BINS; b += blockDim.x) {
+  if (hist || chist) {
+    uint32_t* gh = hist ? a.hist1 : a.histd;
+    for (int b = threadIdx.x + (chist ? 1 : 0); b < PSB_HIST_BINS; b += blockDim.x) {  // coarse digit 0 is implicit
       const uint32_t h = sh_hist[b];
-      if (h) atomicAdd(&a.hist1[b], h);
+      if (h) atomicAdd(&gh[b], h);
     }
   }
   if (MODE == MODE_D) return;  // k_cand reads cand_count after the kernel boundary
@@ -524,6 +534,8 @@ __device__ __forceinline__ void scan_body(const ScanArgs<T>& a) {
 #ifdef PSB_SCAN_TRACE
 // diagnostics build only: globaltimer at entry / exit of every k_scan<MODE_A> CTA
 __device__ unsigned long long g_scan_trace[2 * 4096];
+// k_cand: per CTA 15 phase timestamps + (tiles << 32 | entries) of its slice
+__device__ unsigned long long g_cand_trace[16 * 1024];
 #endif
 
 #ifndef PSB_SCAN_MINB
@@ -611,6 +623,7 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   a.tile_cnt = c->d_tile_cnt;
   a.sb = c->d_sb;
   a.sb_stride = c->sb_stride;
+  a.histd = sizeof(T) == 4 ? c->d_histd : nullptr;
   // persistent-style grid: PSB_SCAN_MINB CTAs per SM pull tiles dynamically
   const uint32_t scan_grid = (uint32_t)std::min<size_t>(ntiles, (size_t)c->num_sms * PSB_SCAN_MINB);
   a.cand_idx = c->d_stage_idx;
@@ -646,6 +659,7 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   b.tile_cnt = c->d_tile_cnt;
   b.sb = c->d_sb;
   b.sb_stride = c->sb_stride;
+  b.histd = sizeof(T) == 4 ? c->d_histd : nullptr;
   b.ntiles = ntiles;
   b.cand_idx = c->d_list_idx;
   b.cand_val = reinterpret_cast<T*>(c->d_list_val);
@@ -798,6 +812,17 @@ extern "C" PSB_API int psb_debug_scan_trace(unsigned long long* out, int max_cta
 #ifdef PSB_SCAN_TRACE
   const int m = max_ctas < 4096 ? max_ctas : 4096;
   return cudaMemcpyFromSymbol(out, g_scan_trace, sizeof(unsigned long long) * 2 * m) == cudaSuccess ? m : -1;
+#else
+  (void)out;
+  (void)max_ctas;
+  return 0;
+#endif
+}
+
+extern "C" PSB_API int psb_debug_cand_trace(unsigned long long* out, int max_ctas) {
+#ifdef PSB_SCAN_TRACE
+  const int m = max_ctas < 1024 ? max_ctas : 1024;
+  return cudaMemcpyFromSymbol(out, g_cand_trace, sizeof(unsigned long long) * 16 * m) == cudaSuccess ? m : -1;
 #else
   (void)out;
   (void)max_ctas;
