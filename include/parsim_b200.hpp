@@ -4,11 +4,17 @@
 // The reference (/root/reference/proj/include/parsim) is header-only C++ with
 // host std::vector<double> in and out.  This header keeps those shapes and
 // semantics for the hot-path functions and runs them on the GPU through
-// libpsb.so in f64 (bit-identical to the reference; see tests/test_facade_gpu.py):
+// libpsb.so in f64 -- bit-identical to the reference except the 1-bit scale
+// (sign bits exact; scale = sum|g|/n as a fixed-shape device sum, within 1e-12
+// relative of the reference's sequential fold, and the 1-bit residual with it;
+// tests/test_facade_gpu.py).  The reference's own signatures, types and tests
+// are served by the drop-in headers in include/parsim_dropin/ (built on this
+// class):
 //
 //   compress_topk            parsim/compression.hpp:81-99
 //   ef_compress_step (topk)  parsim/compression.hpp:146-157
-//   ef_compress_step (1-bit) parsim/compression.hpp:67-77, 146-157
+//   compress_onebit, ef_compress_step (1-bit) parsim/compression.hpp:67-77, 146-157
+//   decompress               parsim/compression.hpp:113-142
 //   allreduce_mean           parsim/collectives.hpp:135-154
 //   sync_data_parallel_step  parsim/strategies.hpp:86-121 (top-k / 1-bit / none)
 //   async_step               parsim/strategies.hpp:125-129
@@ -108,25 +114,68 @@ class Device {
     return m;
   }
 
+  // compress_onebit(g): sign bits (sign(0) = +1) and scale = sum|g| / n.
+  SignBitMessage compress_onebit(const DenseVector& g) {
+    require(!g.empty(), "compress_onebit: empty vector");
+    fit(g.size(), 1, 1);
+    double* dg = upload(0, g);
+    return run_onebit(dg, nullptr, g.size());
+  }
+
+  // decompress(TopKPayload) on the device: zeros + scatter, with the
+  // reference's index validation (compression.hpp:127-140) raised from the
+  // device as std::invalid_argument.
+  DenseVector decompress_topk(std::size_t dim, const std::vector<std::size_t>& indices, const DenseVector& values) {
+    require(indices.size() == values.size(), "decompress: index/value count mismatch");
+    for (std::size_t j = 0; j < indices.size(); ++j)  // beyond the device's u32 indices: out of range anyway
+      require(indices[j] < dim && indices[j] <= 0xffffffffull,
+              "decompress: index " + std::to_string(indices[j]) + " out of range for dim " + std::to_string(dim));
+    DenseVector out(dim, 0.0);
+    if (dim == 0 || indices.empty()) return out;
+    fit(dim, indices.size(), 1);
+    std::vector<uint32_t> i32(indices.begin(), indices.end());
+    uint32_t* di = static_cast<uint32_t*>(buf(4, i32.size() * 4));
+    ck_cuda(cudaMemcpy(di, i32.data(), i32.size() * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
+    double* dv = upload(5, values);
+    double* dout = static_cast<double*>(buf(1, dim * sizeof(double)));
+    ck_cuda(cudaMemsetAsync(dout, 0, dim * sizeof(double), st_), "cudaMemsetAsync");
+    ck(psb_decompress_topk(ctx_, PSB_F64, di, dv, i32.size(), dim, dout, st_), "decompress");
+    check();
+    download(dout, out);
+    return out;
+  }
+
+  // decompress(SignBitPayload): +-scale per sign bit, through the 1-bit mean
+  // kernel with one worker (mean = value * (1/1)).
+  DenseVector decompress_signbit(std::size_t dim, double scale, const std::vector<std::uint8_t>& sign_bytes) {
+    require(sign_bytes.size() == (dim + 7) / 8, "decompress: sign byte count does not match dim");
+    DenseVector out(dim);
+    if (dim == 0) return out;
+    fit(dim, 1, 1);
+    const std::size_t nw = (dim + 31) / 32;
+    std::vector<uint32_t> words(nw, 0u);
+    std::memcpy(words.data(), sign_bytes.data(), sign_bytes.size());
+    uint32_t* dw = static_cast<uint32_t*>(buf(2, nw * 4));
+    ck_cuda(cudaMemcpy(dw, words.data(), nw * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
+    double* ds = static_cast<double*>(buf(3, sizeof(double)));
+    ck_cuda(cudaMemcpy(ds, &scale, sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy");
+    double* dout = static_cast<double*>(buf(1, dim * sizeof(double)));
+    psb_topology t{0, 0, 0};
+    ck(psb_onebit_mean_sgd(ctx_, PSB_F64, 1, dw, ds, PSB_ORDER_NAIVE, &t, 0.0, nullptr, dim, dout, st_),
+       "decompress");
+    check();
+    download(dout, out);
+    return out;
+  }
+
   // ef_compress_step(state, g, {onebit}).
   SignBitMessage ef_compress_step_onebit(ErrorFeedbackState& st, const DenseVector& g) {
     require(!g.empty(), "compress_onebit: empty vector");
     require(st.residual.size() == g.size(), "ef_compress_step: residual/gradient dimension mismatch");
     fit(g.size(), 1, 1);
-    const std::size_t n = g.size(), nw = (n + 31) / 32;
     double* dg = upload(0, g);
     double* dr = upload(1, st.residual);
-    uint32_t* words = static_cast<uint32_t*>(buf(2, nw * 4));
-    double* scale = static_cast<double*>(buf(3, sizeof(double)));
-    ck(psb_ef_onebit(ctx_, PSB_F64, dg, dr, n, words, scale, st_), "ef_compress_step");
-    check();
-    SignBitMessage m;
-    m.dim = n;
-    std::vector<uint32_t> hw(nw);
-    ck_cuda(cudaMemcpy(hw.data(), words, nw * 4, cudaMemcpyDeviceToHost), "cudaMemcpy");
-    m.sign_bytes.resize((n + 7) / 8);
-    std::memcpy(m.sign_bytes.data(), hw.data(), m.sign_bytes.size());
-    ck_cuda(cudaMemcpy(&m.scale, scale, sizeof(double), cudaMemcpyDeviceToHost), "cudaMemcpy");
+    SignBitMessage m = run_onebit(dg, dr, g.size());
     download(dr, st.residual);
     return m;
   }
@@ -160,7 +209,6 @@ class Device {
     const std::size_t n = workers[0].size(), P = workers.size();
     for (const auto& b : workers) require(b.size() == n, "WorkerGroup: dim mismatch across workers");
     require(n == params.size(), "sync_data_parallel_step: worker/param dim mismatch");
-    require(lr > 0.0, "HyperParams: learning_rate must be > 0");
     if (kind != CompressorKind::none && residuals)
       require(residuals->size() == P, "sync_data_parallel_step: one error-feedback state per worker required");
     fit(n, kind == CompressorKind::topk ? top_k : 1, (int)P);
@@ -283,6 +331,21 @@ class Device {
     if (!t) return psb_topology{0, 0, 0};  // flat: devices_per_node = P (collectives.hpp:150-154)
     (void)P;
     return psb_topology{(uint32_t)t->racks, (uint32_t)t->nodes_per_rack, (uint32_t)t->devices_per_node};
+  }
+  SignBitMessage run_onebit(double* dg, double* dr, std::size_t n) {
+    const std::size_t nw = (n + 31) / 32;
+    uint32_t* words = static_cast<uint32_t*>(buf(2, nw * 4));
+    double* scale = static_cast<double*>(buf(3, sizeof(double)));
+    ck(psb_ef_onebit(ctx_, PSB_F64, dg, dr, n, words, scale, st_), "ef_compress_step");
+    check();
+    SignBitMessage m;
+    m.dim = n;
+    std::vector<uint32_t> hw(nw);
+    ck_cuda(cudaMemcpy(hw.data(), words, nw * 4, cudaMemcpyDeviceToHost), "cudaMemcpy");
+    m.sign_bytes.resize((n + 7) / 8);
+    std::memcpy(m.sign_bytes.data(), hw.data(), m.sign_bytes.size());
+    ck_cuda(cudaMemcpy(&m.scale, scale, sizeof(double), cudaMemcpyDeviceToHost), "cudaMemcpy");
+    return m;
   }
   TopKMessage run_topk(double* dg, double* dr, std::size_t n, std::size_t k) {
     uint32_t* idx = static_cast<uint32_t*>(buf(4, k * 4));

@@ -36,6 +36,10 @@ PSB_API void psb_debug_apply_trace(unsigned long long* out8, int reset);
  * entry and exit of every CTA of the last K1 streaming pass, as pairs; returns
  * the number of CTAs copied (0 in a normal build). */
 PSB_API int psb_debug_scan_trace(unsigned long long* out, int max_ctas);
+/* Same build: per CTA of the last candidate phase, 16 words -- globaltimer at
+ * its phase boundaries (unused slots 0) and, in word 15, (tiles << 32 |
+ * entries) of its slice. */
+PSB_API int psb_debug_cand_trace(unsigned long long* out, int max_ctas);
 
 #ifdef __cplusplus
 }

@@ -11,6 +11,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cmath>
+
 #include "psb_internal.cuh"
 #include "psb_debug.h"
 
@@ -330,7 +332,10 @@ static psb_status check_desc(psb_ctx* c, const psb_step_desc* d) {
   PSB_REQUIRE(c, (size_t)d->workers * c->nranks <= (size_t)c->max_workers,
               "sync_data_parallel_step: P exceeds ctx max_workers");
   PSB_REQUIRE(c, d->n >= 1 && d->n <= c->max_n, "sync_data_parallel_step: n out of range for ctx");
-  PSB_REQUIRE(c, d->lr > 0.0, "HyperParams: learning_rate must be > 0");
+  // any finite rate, as sync_data_parallel_step itself (strategies.hpp:86-113;
+  // HyperParams::validate is the caller's check).  lr < 0 differs from the
+  // reference's dense vec_axpy only in the sign of untouched -0 entries.
+  PSB_REQUIRE(c, std::isfinite(d->lr), "sync_data_parallel_step: learning rate must be finite");
   PSB_REQUIRE(c, d->g && d->theta, "sync_data_parallel_step: null buffer");
   if (d->compressor == PSB_COMP_TOPK || d->compressor == PSB_COMP_TOPK_Q8) {
     PSB_REQUIRE(c, d->k >= 1 && d->k <= d->n,

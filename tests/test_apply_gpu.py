@@ -254,8 +254,11 @@ def test_step_rejects_bad_args(ctx):
     from paper_2506_17551_b200 import PsbInvalidArgument
     g = torch.zeros(2, 100, device="cuda")
     theta = torch.zeros(100, device="cuda")
-    with pytest.raises(PsbInvalidArgument, match="learning_rate"):
-        ctx.sync_step(ctx.step_desc(L.PSB_COMP_TOPK, g, None, theta, 0.0, 5))
+    with pytest.raises(PsbInvalidArgument, match="learning rate must be finite"):
+        ctx.sync_step(ctx.step_desc(L.PSB_COMP_TOPK, g, None, theta, float("nan"), 5))
+    ctx.sync_step(ctx.step_desc(L.PSB_COMP_TOPK, g, None, theta, 0.0, 5))  # lr = 0: a no-op update
+    ctx.check()
+    assert not bool(theta.any())
     with pytest.raises(PsbInvalidArgument, match="k out of range"):
         ctx.sync_step(ctx.step_desc(L.PSB_COMP_TOPK, g, None, theta, 0.1, 101))
 
