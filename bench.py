@@ -221,6 +221,14 @@ def ours(args, cfg, world, rank, local_rank):
                  for b in range(NB)]
     stream.synchronize()
     gu = [0]
+    if mode == "async":
+        # bounded-staleness pipeline: round r's exchange + apply on the ctx's
+        # apply stream overlap round r+1's compression (psb_async_pipeline)
+        ctx.async_pipeline(True)
+
+    def drain():  # join the apply stream back (before timing ends / capture closes)
+        if mode == "async":
+            ctx.async_sync()
 
     def step(i):
         d = descs[i % NB]
@@ -236,6 +244,7 @@ def ours(args, cfg, world, rank, local_rank):
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
             step(i)
+        drain()
         ctx.check()
         # ---- timed region: K steps, device-timed with events on our stream.
         # The K steps are captured once into a CUDA graph and replayed (the
@@ -252,6 +261,7 @@ def ours(args, cfg, world, rank, local_rank):
             with torch.cuda.graph(graph, stream=stream):
                 for i in range(args.steps):
                     step(args.warmup + i)
+                drain()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         torch.cuda.synchronize(dev)
@@ -262,6 +272,7 @@ def ours(args, cfg, world, rank, local_rank):
             else:
                 for i in range(args.steps):
                     step(args.warmup + i)
+                drain()
             e1.record(stream)
             torch.cuda.synchronize(dev)
         barrier()
@@ -273,6 +284,7 @@ def ours(args, cfg, world, rank, local_rank):
             ctx.profile_enable(True)
             for i in range(args.steps):
                 step(args.warmup + args.steps + i)
+            drain()
             torch.cuda.synchronize(dev)
         ctx.profile_enable(False)
         k1_ms, k1_count = ctx.profile_read()
@@ -316,6 +328,7 @@ def ours(args, cfg, world, rank, local_rank):
             stream.wait_event(in_done[b])
             if mode == "async":
                 gu[0] = ctx.async_round(d_e2e[b], extra.get("staleness", 2), gu[0])
+                drain()  # the theta snapshot below reads this round's result
             else:
                 ctx.sync_step(d_e2e[b])
             if i >= 2:

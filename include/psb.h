@@ -327,6 +327,20 @@ PSB_API psb_status psb_sync_step(psb_ctx* ctx, const psb_step_desc* d, psb_strea
 PSB_API psb_status psb_async_round(psb_ctx* ctx, const psb_step_desc* d, uint32_t staleness_bound,
                            uint64_t* global_updates, psb_stream_t stream);
 
+/* Bounded-staleness pipeline of psb_async_round (the async branch's overlap,
+ * driven by CUDA streams and events instead of host threads): with enable =
+ * 1, round r's exchange + apply run on a ctx-owned stream, gated by an event
+ * recorded after round r's compression on `stream`, so round r+1's
+ * compression overlaps round r's apply; payload slots are double-buffered
+ * (round r+2 waits for round r's apply).  theta is then up to one round
+ * behind `stream`: psb_async_sync makes `stream` wait for every pending
+ * apply (call it before reading theta, and before ending a CUDA-graph capture
+ * of rounds).  Results are bitwise those of serial rounds (same kernels, same
+ * per-buffer order).  Pull (mode 1) and NCCL (mode 0) exchanges pipeline;
+ * the other peer modes run serially.  psb_check drains the apply stream. */
+PSB_API psb_status psb_async_pipeline(psb_ctx* ctx, int enable);
+PSB_API psb_status psb_async_sync(psb_ctx* ctx, psb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

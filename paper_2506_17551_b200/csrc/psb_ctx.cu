@@ -156,6 +156,12 @@ extern "C" void psb_ctx_destroy(psb_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   psb_peer_destroy(c);
+  for (int i = 0; i < 2; ++i) {
+    if (c->comp_ev[i]) cudaEventDestroy(c->comp_ev[i]);
+    if (c->apply_ev[i]) cudaEventDestroy(c->apply_ev[i]);
+    if (c->pipe_pl[i]) cudaFree(c->pipe_pl[i]);
+  }
+  if (c->apply_st) cudaStreamDestroy(c->apply_st);
   void* ptrs[] = {c->d_flags,    c->d_tk,        c->d_tw,        c->d_hist1,   c->d_histr,
                   c->d_tile_cnt, c->d_sb, c->d_cta, c->d_list_idx, c->d_list_val,       c->d_histd,       c->d_stage_idx, c->d_stage_val,
                   c->d_seg_off,  c->d_partials,  c->d_gather,    c->d_work,    c->d_qmean,   c->d_mom_mean};
@@ -224,6 +230,7 @@ extern "C" uint64_t psb_launch_count(const psb_ctx* c) { return c ? c->launches 
 extern "C" psb_status psb_check(psb_ctx* c, psb_stream_t stream) {
   if (!c) return PSB_EINVAL;
   CUDA_TRY(c, cudaStreamSynchronize((cudaStream_t)stream), "psb_check");
+  if (c->apply_st) CUDA_TRY(c, cudaStreamSynchronize(c->apply_st), "psb_check (async apply stream)");
   uint32_t flags = 0;
   CUDA_TRY(c, cudaMemcpy(&flags, c->d_flags, sizeof(uint32_t), cudaMemcpyDeviceToHost), "psb_check");
   if (c->comm) {
@@ -775,6 +782,140 @@ extern "C" psb_status psb_sync_step(psb_ctx* c, const psb_step_desc* d, psb_stre
   return PSB_OK;
 }
 
+extern "C" psb_status psb_async_pipeline(psb_ctx* c, int enable) {
+  PSB_REQUIRE(c, c != nullptr, "null ctx");
+  if (enable && !c->apply_st) {
+    CUDA_TRY(c, cudaSetDevice(c->device), "psb_async_pipeline");
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->apply_st, cudaStreamNonBlocking), "psb_async_pipeline");
+    for (int i = 0; i < 2; ++i) {
+      CUDA_TRY(c, cudaEventCreateWithFlags(&c->comp_ev[i], cudaEventDisableTiming), "psb_async_pipeline");
+      CUDA_TRY(c, cudaEventCreateWithFlags(&c->apply_ev[i], cudaEventDisableTiming), "psb_async_pipeline");
+    }
+  }
+  c->async_pipe = enable ? 1 : 0;
+  return PSB_OK;
+}
+
+extern "C" psb_status psb_async_sync(psb_ctx* c, psb_stream_t stream) {
+  PSB_REQUIRE(c, c != nullptr, "null ctx");
+  for (int i = 0; i < 2; ++i)
+    if (c->apply_pending[i]) {
+      CUDA_TRY(c, cudaStreamWaitEvent((cudaStream_t)stream, c->apply_ev[i], 0), "psb_async_sync");
+      c->apply_pending[i] = false;
+    }
+  return PSB_OK;
+}
+
+// One pipelined round (psb_async_pipeline on): compress on `st` into the
+// round's payload slot, then exchange + apply on the ctx's apply stream.
+// Every stage is bitwise the serial round's (the same kernels in the same
+// order per buffer): only the cross-round overlap differs.
+static psb_status async_round_pipelined(psb_ctx* c, const psb_step_desc* d, const double* scale,
+                                        cudaStream_t st) {
+  const int W = d->workers, R = c->nranks, P = W * R;
+  const size_t blk = psb_payload_bytes(d->compressor, d->dtype, d->k);
+  const int slot = (int)(c->pipe_round & 1);
+  const size_t need = blk * (size_t)W;
+  if (c->pipe_bytes < need) {
+    // grow: nothing may still read the old slots
+    CUDA_TRY(c, cudaStreamSynchronize(st), "async pipeline");
+    CUDA_TRY(c, cudaStreamSynchronize(c->apply_st), "async pipeline");
+    for (int i = 0; i < 2; ++i) {
+      if (c->pipe_pl[i]) cudaFree(c->pipe_pl[i]);
+      c->pipe_pl[i] = nullptr;
+      c->apply_pending[i] = false;
+    }
+    for (int i = 0; i < 2; ++i)
+      if (cudaMalloc(&c->pipe_pl[i], need) != cudaSuccess)
+        return psb_set_err(c, PSB_ENOMEM, "async pipeline: out of device memory");
+    c->pipe_bytes = need;
+  }
+  // ---- compress (caller's stream): this slot's previous apply must be done
+  if (c->apply_pending[slot]) {
+    CUDA_TRY(c, cudaStreamWaitEvent(st, c->apply_ev[slot], 0), "async pipeline");
+    c->apply_pending[slot] = false;
+  }
+  uint8_t* kb = reinterpret_cast<uint8_t*>(c->pipe_pl[slot]);
+  const size_t es = d->dtype == PSB_F64 ? 8 : 4;
+  psb_status s;
+  for (int w = 0; w < W; ++w) {
+    uint8_t* pslot = kb + (size_t)w * blk;
+    const void* g = reinterpret_cast<const uint8_t*>(d->g) + (size_t)w * d->n * es;
+    void* r = d->r ? reinterpret_cast<uint8_t*>(d->r) + (size_t)w * d->n * es : nullptr;
+    uint32_t* idx = reinterpret_cast<uint32_t*>(pslot);
+    if (d->compressor == PSB_COMP_TOPK) {
+      s = psb_topk_run(c, d->dtype, w, g, r, d->n, d->k, idx, pslot + psb_align16(d->k * 4), st);
+    } else {
+      int8_t* codes = reinterpret_cast<int8_t*>(pslot + psb_align16(d->k * 4));
+      float* scales = reinterpret_cast<float*>(pslot + psb_align16(d->k * 4) + psb_align16(d->k));
+      s = psb_ef_topk_q8(c, w, (const float*)g, (float*)r, d->n, d->k, idx, codes, scales, (psb_stream_t)st);
+    }
+    if (s) return s;
+  }
+  CUDA_TRY(c, cudaEventRecord(c->comp_ev[slot], st), "async pipeline");
+  // ---- exchange + apply (apply stream, in round order)
+  cudaStream_t as = c->apply_st;
+  CUDA_TRY(c, cudaStreamWaitEvent(as, c->comp_ev[slot], 0), "async pipeline");
+  const uint8_t* pl = kb;
+  if (R > 1 && c->peer_mode && P >= 2) {
+    // NVLink pull: this rank's payloads (wire16 for f32/f64 top-k) and their
+    // per-segment offset rows into its arena, signal, pull the peers', apply
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const bool wire16 = d->compressor == PSB_COMP_TOPK && !c->no_wire16;
+    const size_t pblk = wire16 ? psb_wire16_bytes(d->dtype, d->k) : blk;
+    const int seg_shift = psb_apply_seg_shift(P);
+    const uint32_t nseg = (uint32_t)((d->n + ((size_t)1 << seg_shift) - 1) >> seg_shift);
+    const size_t tab_off = al(pblk * P);
+    const size_t region = tab_off + al(sizeof(uint32_t) * P * (nseg + 1));
+    s = psb_peer_ensure(c, region, as);
+    if (s) return s;
+    uint8_t* gb = psb_peer_payload(c);
+    s = psb_peer_wait_ack(c, as);
+    if (s) return s;
+    uint32_t* tab = reinterpret_cast<uint32_t*>(gb + tab_off) + (size_t)c->rank * W * (nseg + 1);
+    s = psb_seg_offsets(c, d->compressor, d->dtype, W, kb, d->k, nseg, seg_shift, tab, as);
+    if (s) return s;
+    for (int w = 0; w < W; ++w) {
+      const int gid = c->rank * W + w;
+      if (wire16) s = psb_pack16(c, d->dtype, kb + (size_t)w * blk, d->k, seg_shift, gb + (size_t)gid * pblk, as);
+      else
+        s = cudaMemcpyAsync(gb + (size_t)gid * pblk, kb + (size_t)w * blk, blk, cudaMemcpyDeviceToDevice, as) ==
+                    cudaSuccess
+                ? PSB_OK
+                : psb_set_err(c, PSB_ECUDA, "async pipeline: payload copy");
+      if (s) return s;
+    }
+    s = psb_peer_exchange(c, (size_t)W * pblk, tab_off, (size_t)W * (nseg + 1), as);
+    if (s) return s;
+    const uint32_t* tabs = reinterpret_cast<const uint32_t*>(gb + tab_off);
+    if (wire16)
+      s = psb_sparse_apply_wire16(c, d->dtype, P, gb, d->k, tabs, PSB_ORDER_NAIVE, nullptr, 0.0, scale, 1, d->theta,
+                                  d->n, nullptr, as);
+    else
+      s = psb_sparse_apply_tab(c, d->compressor, d->dtype, P, gb, d->k, tabs, PSB_ORDER_NAIVE, nullptr, 0.0, scale,
+                               1, d->theta, d->n, nullptr, as);
+  } else {
+    if (R > 1) {
+      // NCCL all-gather of the payloads (psb_peer_mode 0)
+      s = ensure(c, &c->d_gather, &c->gather_bytes, blk * P, "payload gather buffer");
+      if (s) return s;
+      uint8_t* gb = reinterpret_cast<uint8_t*>(c->d_gather);
+      CUDA_TRY(c, cudaMemcpyAsync(gb + (size_t)c->rank * W * blk, kb, blk * W, cudaMemcpyDeviceToDevice, as),
+               "async pipeline");
+      if (!c->comm) return psb_set_err(c, PSB_ESTATE, "async round: communicator not initialised");
+      NCCL_TRY(c, ncclAllGather(gb + (size_t)c->rank * W * blk, gb, (size_t)W * blk, ncclUint8, c->comm, as),
+               "ncclAllGather(payloads)");
+      pl = gb;
+    }
+    s = psb_sparse_async_apply(c, d->compressor, d->dtype, P, pl, d->k, scale, d->theta, d->n, (psb_stream_t)as);
+  }
+  if (s) return s;
+  CUDA_TRY(c, cudaEventRecord(c->apply_ev[slot], as), "async pipeline");
+  c->apply_pending[slot] = true;
+  c->pipe_round += 1;
+  return PSB_OK;
+}
+
 extern "C" psb_status psb_async_round(psb_ctx* c, const psb_step_desc* d, uint32_t staleness_bound,
                                       uint64_t* global_updates, psb_stream_t stream) {
   psb_status s = check_desc(c, d);
@@ -785,10 +926,6 @@ extern "C" psb_status psb_async_round(psb_ctx* c, const psb_step_desc* d, uint32
               "psb_async_round: sparse compressors only");
   cudaStream_t st = (cudaStream_t)stream;
   const int P = d->workers * c->nranks;
-  uint8_t* pl = nullptr;
-  ShardPlan sp;
-  s = compress_and_gather(c, d, st, &pl, false, &sp);
-  if (s) return s;
   std::vector<double> scale(P);
   const uint64_t g0 = *global_updates;
   for (int p = 0; p < P; ++p) {
@@ -796,6 +933,20 @@ extern "C" psb_status psb_async_round(psb_ctx* c, const psb_step_desc* d, uint32
     const uint64_t tau = std::min<uint64_t>(g0 + (uint64_t)p, (uint64_t)p % bound);
     scale[p] = d->lr / (1.0 + (double)tau);  // strategies.hpp:127
   }
+  // pipelined rounds (pull or NCCL exchange; the push / sharded / direct
+  // modes run serially)
+  if (c->async_pipe && (c->nranks == 1 || c->peer_mode <= 1)) {
+    s = async_round_pipelined(c, d, scale.data(), st);
+    if (s) return s;
+    *global_updates = g0 + (uint64_t)P;
+    return PSB_OK;
+  }
+  s = psb_async_sync(c, stream);  // a serial round after pipelined ones
+  if (s) return s;
+  uint8_t* pl = nullptr;
+  ShardPlan sp;
+  s = compress_and_gather(c, d, st, &pl, false, &sp);
+  if (s) return s;
   if (sp.on) s = shard_apply(c, d, sp, scale.data(), true, st);
   else if (sp.direct) {
     const uint8_t* regions[PSB_MAX_P];

@@ -138,6 +138,17 @@ struct psb_ctx {
   int push_wait = 0;            // K1 waits for the peers' acknowledgement before its write phase
   int no_stage = 0; // PSB_NO_STAGE=1: k_cand reads the list from global memory (diagnostics)
   int cand_smem[2] = {0, 0};  // dynamic shared memory of the cooperative k_cand (f32, f64)
+  // bounded-staleness pipeline of psb_async_round (psb_async_pipeline): the
+  // exchange + apply of round r runs on apply_st, gated by comp_ev[r % 2],
+  // while round r+1 compresses on the caller's stream into the other payload
+  // slot (pipe_pl[(r+1) % 2], reused once apply_ev of round r-1 fired)
+  int async_pipe = 0;
+  cudaStream_t apply_st = nullptr;
+  cudaEvent_t comp_ev[2] = {nullptr, nullptr}, apply_ev[2] = {nullptr, nullptr};
+  bool apply_pending[2] = {false, false};
+  uint64_t pipe_round = 0;
+  void* pipe_pl[2] = {nullptr, nullptr};
+  size_t pipe_bytes = 0;
   std::vector<cudaEvent_t> prof_ev;  // pairs (start, stop)
   size_t prof_used = 0;
   // step milestones (PSB_STEP_MARKS=1, eager diagnostics: psb_debug_marks)

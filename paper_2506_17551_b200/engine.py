@@ -363,6 +363,16 @@ class Context:
         self._ck(self.lib.psb_sync_step(self.h, ctypes.byref(desc), self.stream()),
                  "sync_data_parallel_step")
 
+    def async_pipeline(self, enable: bool = True) -> None:
+        """psb_async_pipeline: round r's exchange + apply on a ctx stream,
+        overlapping round r+1's compression; theta trails the current stream
+        by up to one round until async_sync()."""
+        self._ck(self.lib.psb_async_pipeline(self.h, 1 if enable else 0), "psb_async_pipeline")
+
+    def async_sync(self) -> None:
+        """Make the current stream wait for every pending pipelined apply."""
+        self._ck(self.lib.psb_async_sync(self.h, self.stream()), "psb_async_sync")
+
     def async_round(self, desc: L.StepDesc, staleness_bound: int, global_updates: int) -> int:
         gu = ctypes.c_uint64(global_updates)
         self._ck(self.lib.psb_async_round(self.h, ctypes.byref(desc), staleness_bound,

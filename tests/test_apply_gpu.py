@@ -365,3 +365,78 @@ def test_momentum_rejects_q8_and_async(ctx):
                       momentum=torch.zeros(n, device="cuda"), beta=0.9)
     with pytest.raises(L.PsbInvalidArgument, match="momentum"):
         ctx.async_round(d, 2, 0)
+
+
+@pytest.mark.parametrize("q8,W", [(False, 1), (False, 4), (True, 2)])
+def test_async_pipeline_bitwise(cuda, q8, W):
+    """The stream/event pipeline of psb_async_round (round r's apply on the
+    ctx's apply stream overlapping round r+1's compression, double-buffered
+    payloads): 7 rounds issued back to back with no host sync, then
+    async_sync -- bitwise the trainer's async loop (oracle), s = 2 and 3."""
+    from paper_2506_17551_b200.engine import Context
+    n, k, lr = 80_000, 400, 0.1
+    for s in (2, 3):
+        c = Context(n, k, W)
+        c.async_pipeline(True)
+        theta_h = np.zeros(n, dtype=np.float32)
+        res_h = np.zeros((W, n), dtype=np.float32)
+        theta = torch.zeros(n, device="cuda")
+        res = torch.zeros(W, n, device="cuda")
+        comp = L.PSB_COMP_TOPK_Q8 if q8 else L.PSB_COMP_TOPK
+        gs = [np.stack([O.generate("llmrec", 6, w, step, n) for w in range(W)]) for step in range(7)]
+        gd = [torch.from_numpy(g).cuda() for g in gs]
+        gu = gu_h = 0
+        for step in range(7):
+            gu = c.async_round(c.step_desc(comp, gd[step], res, theta, lr, k), s, gu)
+            gu_h = O.async_round(gs[step], theta_h, lr, k, res_h, s, gu_h, q8=q8)
+        c.async_sync()
+        c.check()
+        assert gu == gu_h
+        assert np.array_equal(bits(tnp(theta)), bits(theta_h)), s
+        assert np.array_equal(bits(tnp(res)), bits(res_h)), s
+        c.close()
+
+
+def test_async_pipeline_graph_capture(cuda):
+    """Pipelined rounds captured into a CUDA graph (the apply stream joins
+    the capture through the events; async_sync joins it back) and replayed:
+    same bits as the same rounds run eagerly."""
+    from paper_2506_17551_b200.engine import Context
+    n, k, lr, W, R = 120_000, 600, 0.05, 2, 4
+    gs = [torch.empty(W, n, device="cuda") for _ in range(R)]
+    from paper_2506_17551_b200.engine import generate
+    for b in range(R):
+        for w in range(W):
+            generate("llmrec", 8, w, b, n, gs[b][w])
+    out = []
+    for graph in (False, True):
+        c = Context(n, k, W)
+        c.async_pipeline(True)
+        theta = torch.zeros(n, device="cuda")
+        res = torch.zeros(W, n, device="cuda")
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            descs = [c.step_desc(L.PSB_COMP_TOPK, gs[b], res, theta, lr, k) for b in range(R)]
+            gu = 0
+            for i in range(3):  # warm-up (eager), then drained
+                gu = c.async_round(descs[i % R], 2, gu)
+            c.async_sync()
+            c.check()
+            if graph:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    for i in range(R):
+                        gu = c.async_round(descs[i], 2, gu)
+                    c.async_sync()
+                g.replay()
+                g.replay()
+            else:
+                for _ in range(2):
+                    for i in range(R):
+                        gu = c.async_round(descs[i], 2, gu)
+                c.async_sync()
+            c.check()
+        out.append((theta.clone(), res.clone()))
+        c.close()
+    assert torch.equal(out[0][0].view(torch.int32), out[1][0].view(torch.int32))
+    assert torch.equal(out[0][1].view(torch.int32), out[1][1].view(torch.int32))

@@ -34,6 +34,10 @@ def _worker(rank, nranks, uid, W, comp, order, steps, q, peer="full"):
         c = Context(n, 2 * k, P, device=rank)
         c.comm_init(rank, nranks, uid)
         c.peer_mode(peer)
+        pipe = comp.endswith("_pipe")  # stream/event pipeline of the async rounds
+        comp = comp[:-5] if pipe else comp
+        if pipe:
+            c.async_pipeline(True)
         grow = comp == "topk_grow"  # k doubles mid-run: the peer arenas are re-created
         comp = "topk" if grow else comp
         code = {"topk": L.PSB_COMP_TOPK, "topk_q8": L.PSB_COMP_TOPK_Q8, "onebit": L.PSB_COMP_ONEBIT,
@@ -55,6 +59,8 @@ def _worker(rank, nranks, uid, W, comp, order, steps, q, peer="full"):
             d = c.step_desc(code, g, res, theta, lr, k, order, 256, topo)
             if comp.startswith("async"):
                 gu = c.async_round(d, 2, gu)
+                if pipe:
+                    c.async_sync()
                 gu_h = O.async_round(g_all, theta_h, lr, k, res_h, 2, gu_h, q8=comp == "async_q8")
             else:
                 c.sync_step(d)
@@ -108,6 +114,7 @@ needs2 = pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GP
     ("topk", "ring", 1), ("topk", "naive", 2), ("topk", "hierarchical", 2),
     ("topk_q8", "naive", 1), ("onebit", "ring", 1), ("none", "naive", 2),
     ("q8", "naive", 1), ("q8", "ring", 2), ("async", "naive", 2), ("async_q8", "naive", 1),
+    ("async_pipe", "naive", 1), ("async_pipe", "naive", 2), ("async_q8_pipe", "naive", 1),
 ])
 def test_exchange_paths_match_oracle(comp, order, W):
     nr = min(torch.cuda.device_count(), 4)
