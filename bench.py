@@ -288,12 +288,15 @@ def ours(args, cfg, world, rank, local_rank):
             torch.cuda.synchronize(dev)
         ctx.profile_enable(False)
         k1_ms, k1_count = ctx.profile_read()
+        ex_ms, _ = ctx.profile_read_phase(1)  # exchange (signal + pull / NCCL), per profiled step
+        ap_ms, _ = ctx.profile_read_phase(2)  # P-payload apply
         ctx.check()
         ms_local = e0.elapsed_time(e1) / args.steps
-        t = torch.tensor([ms_local, k1_ms / max(k1_count, 1)], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms_local, k1_ms / max(k1_count, 1), ex_ms / args.steps, ap_ms / args.steps],
+                         device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step, k1_avg_ms = float(t[0]), float(t[1])
+        ms_step, k1_avg_ms, ex_step_ms, ap_step_ms = (float(x) for x in t)
 
         # ---- e2e through the public API: pinned host gradient in, theta out
         host_g = [torch.empty(W, n, pin_memory=True) for _ in range(2)]
@@ -399,6 +402,48 @@ def ours(args, cfg, world, rank, local_rank):
                         "step, theta snapshot D2H to pinned host (copies double-buffered on side streams)"},
         "gpu_launches": launches,
     }
+    if world > 1:
+        # NVLink exchange: bytes this rank receives per step and their rate;
+        # for an all-gather that ingress rate is the NCCL-convention busBW
+        # ((P-1)/P x algBW).  The exchange window includes waiting for the
+        # slowest peer.  Peak: 900 GB/s per direction (NVLink 5 spec; no
+        # measured NVLink figure in MEASURED_PEAKS.json).
+        a16 = lambda b: (b + 15) // 16 * 16  # noqa: E731
+        if comp == "q8":
+            B = extra.get("q8_block", 256)
+            nb = (n + B - 1) // B
+            nbs = (nb + world - 1) // world
+            shard = nbs * B + 4 * nbs
+            bytes_in = (world - 1) * W * shard + (world - 1) * shard  # all-to-all + all-gather
+            if os.environ.get("PSB_NO_PEER") or os.environ.get("PSB_PEER_MODE", "1") == "0":
+                how = "NCCL grouped send/recv all-to-all of int8 block shards + all-gather of the requantized shards"
+            else:
+                how = ("NVLink pulls: every remote worker's int8 codes of this rank's block shard, then every "
+                       "rank's requantized shard (window: two flag rounds, both pulls and the shard reduce)")
+        elif comp in ("topk", "topk_q8"):
+            if comp == "topk" and not os.environ.get("PSB_NO_WIRE16") and os.environ.get("PSB_PEER_MODE", "1") == "1" \
+                    and not os.environ.get("PSB_NO_PEER"):
+                seg_shift = 15
+                while seg_shift > 10 and (P * 8) << (seg_shift - 5) > 16 * 1024:
+                    seg_shift -= 1
+                nseg = (n + (1 << seg_shift) - 1) >> seg_shift
+                blk = a16(2 * k) + a16(4 * k) + 4 * (nseg + 1)  # wire16 payload + offset rows
+                how = "NVLink pull of wire16 payloads (u16 in-segment index | f32) + per-segment offset rows"
+            else:
+                from paper_2506_17551_b200.engine import payload_bytes
+                blk = payload_bytes(comp_code, torch.float32, k)
+                how = ("NCCL all-gather of the payloads" if os.environ.get("PSB_NO_PEER") or
+                       os.environ.get("PSB_PEER_MODE", "1") == "0" else "NVLink pull of the payloads")
+            bytes_in = (P - W) * blk
+        else:
+            bytes_in, how = None, comp
+        if bytes_in and ex_step_ms > 0:
+            bw = bytes_in / (ex_step_ms * 1e-3) / 1e9
+            line["exchange"] = {"bytes_in_per_rank": bytes_in, "ms_per_step": ex_step_ms, "busbw_gbs": bw,
+                                "peak_gbs": 900.0, "peak_source": "NVLink 5 spec, per direction",
+                                "frac": bw / 900.0, "what": how}
+        if ap_step_ms > 0:
+            line["apply_ms_per_step"] = ap_step_ms
     if comp.startswith("topk"):
         st = ctx.topk_stats(0)
         line["config"]["k1_last_call"] = {kk: st[kk] for kk in ("candidates", "predicted_valid", "first_radix_level",

@@ -106,6 +106,11 @@ PSB_API uint64_t psb_launch_count(const psb_ctx* ctx);
  * count since the last read, and clears them. */
 PSB_API psb_status psb_profile_enable(psb_ctx* ctx, int enable);
 PSB_API psb_status psb_profile_read(psb_ctx* ctx, double* total_ms, uint64_t* launches);
+/* Same for a phase of the multi-rank steps: 0 = the K1 streaming pass (as
+ * psb_profile_read), 1 = the exchange (NVLink signal + pull, or the NCCL
+ * collectives; wait for the slowest peer included), 2 = the P-payload apply.
+ * Returns the summed ms and the number of event pairs since the last read. */
+PSB_API psb_status psb_profile_read_phase(psb_ctx* ctx, int phase, double* total_ms, uint64_t* pairs);
 
 /* Diagnostics of the last K1 call and of `worker`'s threshold prediction:
  * out[0] candidates, [1] k, [2] threshold key T, [3] ties taken at T,

@@ -121,6 +121,7 @@ _SIGS = {
                                  _vp, _vp]),
     "psb_sync_step": (_i, [_vp, ctypes.POINTER(StepDesc), _vp]),
     "psb_async_round": (_i, [_vp, ctypes.POINTER(StepDesc), _u32, ctypes.POINTER(_u64), _vp]),
+    "psb_profile_read_phase": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)]),
     "psb_async_pipeline": (_i, [_vp, _i]),
     "psb_async_sync": (_i, [_vp, _vp]),
 }

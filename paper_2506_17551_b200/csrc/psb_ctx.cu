@@ -18,17 +18,15 @@
 
 psb_status psb_q8_quant_launch(psb_ctx* c, const float* x, float* r, size_t n, uint32_t B,
                                int8_t* codes, float* scales, cudaStream_t st);
-psb_status psb_q8_reduce_launch(psb_ctx* c, const int8_t* wcodes, size_t wstride,
-                                const float* wscales, size_t sstride, int P, size_t blk_lo,
+psb_status psb_q8_reduce_launch(psb_ctx* c, const Q8Workers& wv, int P, size_t blk_lo,
                                 size_t blk_hi, size_t n, uint32_t B, psb_order order, uint32_t dpn,
                                 uint32_t npr, int8_t* mcodes, float* mscales, double lr,
                                 float* theta, float* mean_out, cudaStream_t st);
 psb_status psb_q8_step1_launch(psb_ctx* c, const float* g, size_t gstride, float* r, size_t rstride,
                                int P, size_t n, uint32_t B, psb_order order, uint32_t dpn, uint32_t npr,
                                double lr, float* theta, float* mean_out, cudaStream_t st);
-psb_status psb_q8_apply_launch(psb_ctx* c, const int8_t* mcodes, const float* mscales, size_t n,
-                               uint32_t B, double lr, float* theta, float* mean_out,
-                               cudaStream_t st);
+psb_status psb_q8_apply_launch(psb_ctx* c, const Q8Shards& ms, int R, size_t n, uint32_t B, double lr,
+                               float* theta, float* mean_out, cudaStream_t st);
 
 psb_status psb_set_err(psb_ctx* c, psb_status s, const std::string& msg) {
   if (c) c->err = msg;
@@ -169,6 +167,8 @@ extern "C" void psb_ctx_destroy(psb_ctx* c) {
     if (p) cudaFree(p);
   if (c->comm) ncclCommDestroy(c->comm);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+  for (auto& v : c->prof_ph_ev)
+    for (cudaEvent_t e : v) cudaEventDestroy(e);
   delete c;
 }
 
@@ -199,6 +199,37 @@ cudaEvent_t psb_prof_event(psb_ctx* c) {
     c->prof_ev.push_back(e);
   }
   return c->prof_ev[c->prof_used++];
+}
+
+void psb_prof_mark(psb_ctx* c, int phase, cudaStream_t st) {
+  if (!c->prof || phase < 1 || phase > 2) return;
+  auto& v = c->prof_ph_ev[phase];
+  size_t& used = c->prof_ph_used[phase];
+  if (used == v.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    v.push_back(e);
+  }
+  cudaEventRecord(v[used++], st);
+}
+
+extern "C" psb_status psb_profile_read_phase(psb_ctx* c, int phase, double* total_ms, uint64_t* pairs_out) {
+  PSB_REQUIRE(c, c != nullptr && total_ms && pairs_out, "psb_profile_read_phase: null argument");
+  PSB_REQUIRE(c, phase >= 0 && phase <= 2, "psb_profile_read_phase: phase must be 0, 1 or 2");
+  if (phase == 0) return psb_profile_read(c, total_ms, pairs_out);
+  auto& v = c->prof_ph_ev[phase];
+  const size_t pairs = c->prof_ph_used[phase] / 2;
+  double t = 0.0;
+  for (size_t i = 0; i < pairs; ++i) {
+    CUDA_TRY(c, cudaEventSynchronize(v[2 * i + 1]), "psb_profile_read_phase");
+    float ms = 0.f;
+    CUDA_TRY(c, cudaEventElapsedTime(&ms, v[2 * i], v[2 * i + 1]), "psb_profile_read_phase");
+    t += ms;
+  }
+  *total_ms = t;
+  *pairs_out = pairs;
+  c->prof_ph_used[phase] = 0;
+  return PSB_OK;
 }
 
 extern "C" psb_status psb_profile_enable(psb_ctx* c, int enable) {
@@ -515,15 +546,19 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
     plan->ack_after_apply = true;
     psb_mark(c, st);
   } else if (peer) {
+    psb_prof_mark(c, 1, st);
     s = psb_peer_exchange(c, (size_t)W * pblk, tabs ? plan->tab_off : 0,
                           tabs ? (size_t)W * (plan->nseg + 1) : 0, st);
+    psb_prof_mark(c, 1, st);
     if (s) return s;
     if (tabs) plan->tab_ready = true;
     psb_mark(c, st);
   } else if (c->nranks > 1) {
     if (!c->comm) return psb_set_err(c, PSB_ESTATE, "sync step: communicator not initialised");
+    psb_prof_mark(c, 1, st);
     NCCL_TRY(c, ncclAllGather(gb + (size_t)c->rank * W * blk, gb, (size_t)W * blk, ncclUint8, c->comm, st),
              "ncclAllGather(payloads)");
+    psb_prof_mark(c, 1, st);
   }
   *payloads_out = gb;
   return PSB_OK;
@@ -563,6 +598,113 @@ static psb_status shard_apply(psb_ctx* c, const psb_step_desc* d, const ShardPla
   if (s) return s;
   psb_mark(c, st);
   s = psb_shard_finish(c, d->dtype, sp.list_off, sp.list_voff, d->theta, sp.cap, st);
+  psb_mark(c, st);
+  return s;
+}
+
+// Dense q8 all-reduce across ranks over NVLink peer memory (the default for
+// nranks > 1; psb_peer_mode 0 keeps the NCCL all-to-all + all-gather).  Each
+// rank quantizes its W workers straight into its arena; after one flag round
+// every rank reduces its block shard reading all P workers' codes and scales
+// in place from the peers' arenas (the reduce-scatter is the reduce kernel's
+// own NVLink loads), requantizes the mean into its arena; after a second flag
+// round it applies SGD reading each block's mean from the rank that reduced it
+// (the all-gather is the apply's own NVLink loads).  No staging copies; the
+// fold order, requantization and update are those of the NCCL path.
+static psb_status q8_step_nvlink(psb_ctx* c, const psb_step_desc* d, cudaStream_t st, size_t n_pad, size_t nbs,
+                                 uint32_t dpn, uint32_t npr) {
+  const int W = d->workers, R = c->nranks, P = W * R;
+  const uint32_t B = d->q8_block ? d->q8_block : 256;
+  const size_t n = d->n, nb = (n + B - 1) / B;
+  const size_t shard = nbs * B;
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  // arena: local codes [W][n_pad] | local scales [W][R*nbs] | mean codes [n_pad]
+  //        | mean scales [R*nbs] | pulled codes [P][shard] | pulled scales [P][nbs]
+  const size_t o_lc = 0;
+  const size_t o_ls = o_lc + al((size_t)W * n_pad);
+  const size_t o_mc = o_ls + al(sizeof(float) * W * R * nbs);
+  const size_t o_ms = o_mc + al(n_pad);
+  const size_t o_xc = o_ms + al(sizeof(float) * R * nbs);
+  const size_t o_xs = o_xc + al((size_t)P * shard);
+  const size_t total = o_xs + al(sizeof(float) * P * nbs);
+  psb_status s = psb_peer_ensure(c, total, st);
+  if (s) return s;
+  uint8_t* own = psb_peer_payload(c);
+  psb_mark(c, st);
+  s = psb_peer_wait_ack(c, st);  // peers done reading our previous codes / mean
+  if (s) return s;
+  psb_mark(c, st);
+  if (c->prof) cudaEventRecord(psb_prof_event(c), st);
+  for (int w = 0; w < W; ++w) {
+    const float* g = reinterpret_cast<const float*>(d->g) + (size_t)w * n;
+    float* r = d->r ? reinterpret_cast<float*>(d->r) + (size_t)w * n : nullptr;
+    s = psb_q8_quant_launch(c, g, r, n, B, reinterpret_cast<int8_t*>(own + o_lc) + (size_t)w * n_pad,
+                            reinterpret_cast<float*>(own + o_ls) + (size_t)w * R * nbs, st);
+    if (s) return s;
+  }
+  if (c->prof) cudaEventRecord(psb_prof_event(c), st);
+  psb_mark(c, st);
+  auto lo_of = [&](int q) { return std::min(nb, (size_t)q * nbs); };
+  auto hi_of = [&](int q) { return std::min(nb, (size_t)(q + 1) * nbs); };
+  const size_t blk_lo = lo_of(c->rank), blk_hi = hi_of(c->rank);
+  // ---- reduce-scatter: pull every remote worker's codes and scales of our
+  // shard over NVLink, fold all P workers in order, requantize our shard
+  psb_prof_mark(c, 1, st);
+  s = psb_peer_signal(c, st);
+  if (!s) s = psb_peer_wait_ready(c, st);
+  if (s) return s;
+  psb_mark(c, st);
+  PeerSegs sg{};
+  for (int q = 0; q < P; ++q) {
+    if (q / W == c->rank || blk_hi <= blk_lo) continue;
+    const int w = q % W;
+    sg.s[sg.n++] = {q / W, o_lc + (size_t)w * n_pad + blk_lo * B, o_xc + (size_t)q * shard, (blk_hi - blk_lo) * B};
+    sg.s[sg.n++] = {q / W, o_ls + sizeof(float) * ((size_t)w * R * nbs + blk_lo), o_xs + sizeof(float) * q * nbs,
+                    sizeof(float) * (blk_hi - blk_lo)};
+  }
+  s = psb_peer_gather(c, sg, st);
+  if (s) return s;
+  psb_mark(c, st);
+  Q8Workers wv{};
+  for (int q = 0; q < P; ++q) {
+    if (q / W == c->rank) {
+      wv.codes[q] = reinterpret_cast<const int8_t*>(own + o_lc) + (size_t)(q % W) * n_pad + blk_lo * B;
+      wv.scales[q] = reinterpret_cast<const float*>(own + o_ls) + (size_t)(q % W) * R * nbs + blk_lo;
+    } else {
+      wv.codes[q] = reinterpret_cast<const int8_t*>(own + o_xc) + (size_t)q * shard;
+      wv.scales[q] = reinterpret_cast<const float*>(own + o_xs) + (size_t)q * nbs;
+    }
+  }
+  s = psb_q8_reduce_launch(c, wv, P, blk_lo, blk_hi, n, B, d->order, dpn, npr,
+                           reinterpret_cast<int8_t*>(own + o_mc), reinterpret_cast<float*>(own + o_ms), d->lr,
+                           nullptr, nullptr, st);
+  if (s) return s;
+  psb_mark(c, st);
+  // ---- all-gather: pull every other rank's requantized shard into place
+  s = psb_peer_signal(c, st);
+  if (!s) s = psb_peer_wait_ready(c, st);
+  if (s) return s;
+  psb_mark(c, st);
+  PeerSegs sm{};
+  for (int q = 0; q < R; ++q) {
+    if (q == c->rank || hi_of(q) <= lo_of(q)) continue;
+    sm.s[sm.n++] = {q, o_mc + lo_of(q) * B, o_mc + lo_of(q) * B, (hi_of(q) - lo_of(q)) * B};
+    sm.s[sm.n++] = {q, o_ms + sizeof(float) * lo_of(q), o_ms + sizeof(float) * lo_of(q),
+                    sizeof(float) * (hi_of(q) - lo_of(q))};
+  }
+  s = psb_peer_gather(c, sm, st);
+  if (!s) s = psb_peer_ack(c, st);  // done reading the peers' arenas for this step
+  if (s) return s;
+  psb_mark(c, st);
+  psb_prof_mark(c, 1, st);
+  Q8Shards ms{};
+  ms.codes[0] = reinterpret_cast<const int8_t*>(own + o_mc);
+  ms.scales[0] = reinterpret_cast<const float*>(own + o_ms);
+  ms.nbs = (size_t)-1;
+  psb_prof_mark(c, 2, st);
+  s = psb_q8_apply_launch(c, ms, 1, n, B, d->lr, reinterpret_cast<float*>(d->theta),
+                          reinterpret_cast<float*>(d->mean_out), st);
+  psb_prof_mark(c, 2, st);
   psb_mark(c, st);
   return s;
 }
@@ -609,6 +751,7 @@ static psb_status q8_step(psb_ctx* c, const psb_step_desc* d, cudaStream_t st) {
                                n, B, d->order, dpn, npr, d->lr, reinterpret_cast<float*>(d->theta),
                                reinterpret_cast<float*>(d->mean_out), st);
   }
+  if (R > 1 && c->peer_mode) return q8_step_nvlink(c, d, st, n_pad, nbs, dpn, npr);
   const bool prof_quant = R > 1;  // multi-rank: the quantizer is the dominant kernel
   if (prof_quant && c->prof) cudaEventRecord(psb_prof_event(c), st);
   for (int w = 0; w < W; ++w) {
@@ -621,11 +764,17 @@ static psb_status q8_step(psb_ctx* c, const psb_step_desc* d, cudaStream_t st) {
   float* theta = reinterpret_cast<float*>(d->theta);
   float* mean_out = reinterpret_cast<float*>(d->mean_out);
   if (R == 1) {
-    return psb_q8_reduce_launch(c, lcodes, n_pad, lscales, (size_t)R * nbs, P, 0, nb, n, B, d->order,
-                                dpn, npr, mcodes, mscales, d->lr, theta, mean_out, st);
+    Q8Workers wv{};
+    for (int q = 0; q < P; ++q) {
+      wv.codes[q] = lcodes + (size_t)q * n_pad;
+      wv.scales[q] = lscales + (size_t)q * R * nbs;
+    }
+    return psb_q8_reduce_launch(c, wv, P, 0, nb, n, B, d->order, dpn, npr, mcodes, mscales, d->lr, theta,
+                                mean_out, st);
   }
   if (!c->comm) return psb_set_err(c, PSB_ESTATE, "q8 step: communicator not initialised");
   // all-to-all of block shards: worker gid's shard q goes to rank q, slot gid
+  psb_prof_mark(c, 1, st);
   NCCL_TRY(c, ncclGroupStart(), "ncclGroupStart");
   for (int peer = 0; peer < R; ++peer) {
     for (int w = 0; w < W; ++w) {
@@ -645,18 +794,30 @@ static psb_status q8_step(psb_ctx* c, const psb_step_desc* d, cudaStream_t st) {
     }
   }
   NCCL_TRY(c, ncclGroupEnd(), "ncclGroupEnd");
+  psb_prof_mark(c, 1, st);
   const size_t blk_lo = (size_t)c->rank * nbs;
   const size_t blk_hi = std::min(nb, blk_lo + nbs);
-  s = psb_q8_reduce_launch(c, rcodes, shard_elems, rscales, nbs, P, blk_lo, blk_hi, n, B, d->order, dpn,
-                           npr, mcodes, mscales, d->lr, nullptr, nullptr, st);
+  Q8Workers wv{};
+  for (int q = 0; q < P; ++q) {
+    wv.codes[q] = rcodes + (size_t)q * shard_elems;
+    wv.scales[q] = rscales + (size_t)q * nbs;
+  }
+  s = psb_q8_reduce_launch(c, wv, P, blk_lo, blk_hi, n, B, d->order, dpn, npr, mcodes, mscales, d->lr, nullptr,
+                           nullptr, st);
   if (s) return s;
+  psb_prof_mark(c, 1, st);
   NCCL_TRY(c, ncclGroupStart(), "ncclGroupStart");
   NCCL_TRY(c, ncclAllGather(mcodes + blk_lo * B, mcodes, shard_elems, ncclInt8, c->comm, st),
            "ncclAllGather(codes)");
   NCCL_TRY(c, ncclAllGather(mscales + blk_lo, mscales, nbs, ncclFloat32, c->comm, st),
            "ncclAllGather(scales)");
   NCCL_TRY(c, ncclGroupEnd(), "ncclGroupEnd");
-  return psb_q8_apply_launch(c, mcodes, mscales, n, B, d->lr, theta, mean_out, st);
+  psb_prof_mark(c, 1, st);
+  Q8Shards ms{};
+  ms.codes[0] = mcodes;
+  ms.scales[0] = mscales;
+  ms.nbs = (size_t)-1;
+  return psb_q8_apply_launch(c, ms, 1, n, B, d->lr, theta, mean_out, st);
 }
 
 // The step on a validated descriptor; theta == NULL computes only the mean
@@ -675,6 +836,7 @@ static psb_status sync_step_core(psb_ctx* c, const psb_step_desc* d, psb_stream_
       s = compress_and_gather(c, d, st, &pl, fuse, &sp);
       if (s || fuse) return s;
       if (sp.on) return shard_apply(c, d, sp, nullptr, false, st);
+      psb_prof_mark(c, 2, st);
       if (sp.direct) {
         const uint8_t* regions[PSB_MAX_P];
         psb_peer_regions(c, regions);
@@ -690,6 +852,7 @@ static psb_status sync_step_core(psb_ctx* c, const psb_step_desc* d, psb_stream_
       else
         s = psb_sparse_mean_sgd(c, d->compressor, d->dtype, P, pl, d->k, d->order, &d->topo, d->lr,
                                 d->theta, d->n, d->mean_out, stream);
+      psb_prof_mark(c, 2, st);
       if (!s && sp.ack_after_apply) s = psb_peer_ack(c, st);
       psb_mark(c, st);
       return s;
@@ -885,7 +1048,9 @@ static psb_status async_round_pipelined(psb_ctx* c, const psb_step_desc* d, cons
                 : psb_set_err(c, PSB_ECUDA, "async pipeline: payload copy");
       if (s) return s;
     }
+    psb_prof_mark(c, 1, as);
     s = psb_peer_exchange(c, (size_t)W * pblk, tab_off, (size_t)W * (nseg + 1), as);
+    psb_prof_mark(c, 1, as);
     if (s) return s;
     const uint32_t* tabs = reinterpret_cast<const uint32_t*>(gb + tab_off);
     if (wire16)

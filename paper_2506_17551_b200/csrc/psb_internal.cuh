@@ -151,6 +151,10 @@ struct psb_ctx {
   size_t pipe_bytes = 0;
   std::vector<cudaEvent_t> prof_ev;  // pairs (start, stop)
   size_t prof_used = 0;
+  // psb_profile_read_phase: event pairs around the exchange (1) and the
+  // P-payload apply (2) of the steps, recorded while profiling is enabled
+  std::vector<cudaEvent_t> prof_ph_ev[3];
+  size_t prof_ph_used[3] = {0, 0, 0};
   // step milestones (PSB_STEP_MARKS=1, eager diagnostics: psb_debug_marks)
   int marks_on = 0;
   std::vector<cudaEvent_t> mark_ev;
@@ -220,8 +224,37 @@ static inline int psb_apply_seg_shift(int P) {
   return s;
 }
 
+// Segment list of psb_peer_gather: bytes at (rank's payload region + src_off)
+// copied to (own payload region + dst_off).
+struct PeerSeg {
+  int rank;
+  size_t src_off, dst_off, bytes;
+};
+struct PeerSegs {
+  PeerSeg s[2 * PSB_MAX_P + 2];
+  int n;
+};
+psb_status psb_peer_gather(psb_ctx* c, const PeerSegs& segs, cudaStream_t st);
+
+// Dense q8 all-reduce views.  Q8Workers: worker q's int8 codes of global
+// element e at codes[q][e - e_base] and its block scales at scales[q][blk -
+// blk_lo] (local buffers, or the peers' NVLink-mapped arenas).  Q8Shards: the
+// requantized mean of element e at codes[rank][e] / scales[rank][e / B] with
+// rank = (e / B) / nbs -- the rank that reduced that block shard.
+struct Q8Workers {
+  const int8_t* codes[PSB_MAX_P];
+  const float* scales[PSB_MAX_P];
+};
+struct Q8Shards {
+  const int8_t* codes[PSB_MAX_P];
+  const float* scales[PSB_MAX_P];
+  size_t nbs;  // blocks per shard (SIZE_MAX: one shard)
+};
+
 // Record a profiling event pair around the dominant kernel (no-op unless enabled).
 cudaEvent_t psb_prof_event(psb_ctx* c);
+// Record one event of phase 1 (exchange) / 2 (apply) on st when profiling.
+void psb_prof_mark(psb_ctx* c, int phase, cudaStream_t st);
 
 // ------------------------------------------------------------------- helpers
 psb_status psb_set_err(psb_ctx* c, psb_status s, const std::string& msg);

@@ -508,6 +508,51 @@ __global__ void k_peer_put(PeerPtrs pp, int R, int rank, size_t off, size_t word
 }
 }  // namespace
 
+namespace {
+// Segment copy from the peers' (NVLink-mapped) payload regions into ours: one
+// grid row per segment, int4 loads with PSB_PULL_U in flight per thread (u32
+// copies for a segment that is not 16-byte aligned).  The caller has waited
+// for the peers' readiness flags.
+__global__ void __launch_bounds__(256) k_peer_gather(PeerPtrs pp, int rank, PeerSegs sg) {
+  const PeerSeg g = sg.s[blockIdx.y];
+  const uint8_t* src = pp.base[g.rank] + kHdrBytes + g.src_off;
+  uint8_t* dst = pp.base[rank] + kHdrBytes + g.dst_off;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  if (((g.src_off | g.dst_off | g.bytes) & 15) == 0) {
+    const size_t nv = g.bytes / 16;
+    constexpr int U = PSB_PULL_U;
+    for (size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < nv; t0 += U * stride) {
+      int4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (t0 + u * stride < nv) v[u] = __ldcs(reinterpret_cast<const int4*>(src) + t0 + u * stride);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (t0 + u * stride < nv) reinterpret_cast<int4*>(dst)[t0 + u * stride] = v[u];
+    }
+  } else {
+    const size_t nw = g.bytes / 4;
+    for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < nw; t += stride)
+      reinterpret_cast<uint32_t*>(dst)[t] = reinterpret_cast<const uint32_t*>(src)[t];
+  }
+}
+}  // namespace
+
+psb_status psb_peer_gather(psb_ctx* c, const PeerSegs& segs, cudaStream_t st) {
+  if (segs.n <= 0) return PSB_OK;
+  size_t mx = 0;
+  for (int i = 0; i < segs.n; ++i) {
+    if (segs.s[i].bytes % 4) return psb_set_err(c, PSB_EINVAL, "peer gather: segment not a multiple of 4 bytes");
+    mx = std::max(mx, segs.s[i].bytes);
+  }
+  const unsigned gx = (unsigned)std::max<size_t>(
+      1, std::min<size_t>((mx / 16 + 255) / 256, (size_t)c->num_sms * PSB_PULL_CTAS / (size_t)segs.n + 1));
+  k_peer_gather<<<dim3(gx, (unsigned)segs.n), 256, 0, st>>>(peer_ptrs(c), c->rank, segs);
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "peer gather");
+  return PSB_OK;
+}
+
 psb_status psb_peer_put(psb_ctx* c, size_t off, size_t words, cudaStream_t st) {
   const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((words + 255) / 256, (size_t)c->num_sms));
   k_peer_put<<<grid, 256, 0, st>>>(peer_ptrs(c), c->nranks, c->rank, off, words);

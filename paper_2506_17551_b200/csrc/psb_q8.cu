@@ -195,8 +195,7 @@ __device__ __forceinline__ uint32_t ring_chunk(size_t i, size_t n, int P) {
 // scales at wscales + q*sstride + (blk - blk_lo).
 template <int VPL>
 __global__ void __launch_bounds__(256) k_q8_reduce(
-    const int8_t* __restrict__ wcodes, size_t wstride, const float* __restrict__ wscales,
-    size_t sstride, int P, size_t blk_lo, size_t blk_hi, size_t n, int order, uint32_t dpn,
+    Q8Workers wv, int P, size_t blk_lo, size_t blk_hi, size_t n, int order, uint32_t dpn,
     uint32_t npr, int8_t* __restrict__ mcodes, float* __restrict__ mscales, float coef,
     float* __restrict__ theta, float* __restrict__ mean_out, uint32_t* flags) {
   constexpr int B = VPL * 128;
@@ -205,8 +204,9 @@ __global__ void __launch_bounds__(256) k_q8_reduce(
   const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
   const size_t e_base = blk_lo * B;
   const float inv = (float)(1.0 / (double)P);
-  const bool vec_ok = ((((uintptr_t)wcodes) | ((uintptr_t)mcodes) | ((uintptr_t)theta) | wstride) & 15) == 0 &&
-                      !mean_out;
+  uintptr_t al = ((uintptr_t)mcodes) | ((uintptr_t)theta);
+  for (int q = 0; q < P; ++q) al |= (uintptr_t)wv.codes[q];
+  const bool vec_ok = (al & 15) == 0 && !mean_out;
   bool bad = false;
   RingChunk rc;
   for (size_t blk = blk_lo + warp; blk < blk_hi; blk += nwarps) {
@@ -233,8 +233,8 @@ __global__ void __launch_bounds__(256) k_q8_reduce(
       }
       if (full && same_chunk) {
         auto get4 = [&](int q) -> float4 {
-          const char4 cv = *reinterpret_cast<const char4*>(wcodes + (size_t)q * wstride + (e0 - e_base));
-          const float sc = wscales[(size_t)q * sstride + (blk - blk_lo)];
+          const char4 cv = *reinterpret_cast<const char4*>(wv.codes[q] + (e0 - e_base));
+          const float sc = wv.scales[q][blk - blk_lo];
           return make_float4(__fmul_rn((float)cv.x, sc), __fmul_rn((float)cv.y, sc),
                              __fmul_rn((float)cv.z, sc), __fmul_rn((float)cv.w, sc));
         };
@@ -250,8 +250,8 @@ __global__ void __launch_bounds__(256) k_q8_reduce(
           float mean = 0.f;
           if (e < n) {
             auto get = [&](int q) -> float {
-              const int8_t code = wcodes[(size_t)q * wstride + (e - e_base)];
-              const float sc = wscales[(size_t)q * sstride + (blk - blk_lo)];
+              const int8_t code = wv.codes[q][e - e_base];
+              const float sc = wv.scales[q][blk - blk_lo];
               return __fmul_rn((float)code, sc);
             };
             mean = __fmul_rn(fold_sum<float>(get, P, order, e, n, dpn, npr), inv);
@@ -610,19 +610,26 @@ __global__ void __launch_bounds__(256) k_q8_step1_tma(const float* __restrict__ 
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1u);
 }
 
-__global__ void __launch_bounds__(256) k_q8_apply(const int8_t* __restrict__ mcodes,
-                                                  const float* __restrict__ mscales, size_t n,
+// theta += (-lr) * mean, the mean read shard by shard from the rank that
+// reduced it (Q8Shards: local buffer, or the peers' NVLink-mapped arenas).
+__global__ void __launch_bounds__(256) k_q8_apply(Q8Shards ms, int R, size_t n,
                                                   uint32_t B, float coef, float* __restrict__ theta,
                                                   float* __restrict__ mean_out, uint32_t* flags) {
   bool bad = false;
   const size_t nv = n / 4;
-  const bool vec_ok = ((((uintptr_t)mcodes) | ((uintptr_t)theta)) & 15) == 0 && !mean_out;
+  uintptr_t al = (uintptr_t)theta;
+  for (int q = 0; q < R; ++q) al |= (uintptr_t)ms.codes[q];
+  const bool vec_ok = (al & 15) == 0 && !mean_out;
+  auto owner = [&](size_t e) { return R == 1 ? 0 : (int)((e / B) / ms.nbs); };
+  auto code_at = [&](size_t e) { return ms.codes[owner(e)][e]; };
+  auto scale_at = [&](size_t e) { return ms.scales[owner(e)][e / B]; };
   if (vec_ok) {
     for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv;
          v += (size_t)gridDim.x * blockDim.x) {
       const size_t e = v * 4;
-      const char4 cv = *reinterpret_cast<const char4*>(mcodes + e);
-      const float sc = mscales[e / B];
+      const int o = owner(e);
+      const char4 cv = *reinterpret_cast<const char4*>(ms.codes[o] + e);
+      const float sc = ms.scales[o][e / B];
       float4 th = __ldcs(reinterpret_cast<const float4*>(theta + e));
       th.x = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.x, sc)), th.x);
       th.y = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.y, sc)), th.y);
@@ -633,14 +640,14 @@ __global__ void __launch_bounds__(256) k_q8_apply(const int8_t* __restrict__ mco
     }
     for (size_t e = nv * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
          e += (size_t)gridDim.x * blockDim.x) {
-      const float th = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)mcodes[e], mscales[e / B])), theta[e]);
+      const float th = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)code_at(e), scale_at(e))), theta[e]);
       theta[e] = th;
       bad |= !is_finite(th);
     }
   } else {
     for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
          e += (size_t)gridDim.x * blockDim.x) {
-      const float mhat = __fmul_rn((float)mcodes[e], mscales[e / B]);
+      const float mhat = __fmul_rn((float)code_at(e), scale_at(e));
       const float th = __fadd_rn(__fmul_rn(coef, mhat), theta[e]);
       theta[e] = th;
       if (mean_out) mean_out[e] = mhat;
@@ -668,8 +675,7 @@ psb_status psb_q8_quant_launch(psb_ctx* c, const float* x, float* r, size_t n, u
   return PSB_OK;
 }
 
-psb_status psb_q8_reduce_launch(psb_ctx* c, const int8_t* wcodes, size_t wstride,
-                                const float* wscales, size_t sstride, int P, size_t blk_lo,
+psb_status psb_q8_reduce_launch(psb_ctx* c, const Q8Workers& wv, int P, size_t blk_lo,
                                 size_t blk_hi, size_t n, uint32_t B, psb_order order, uint32_t dpn,
                                 uint32_t npr, int8_t* mcodes, float* mscales, double lr,
                                 float* theta, float* mean_out, cudaStream_t st) {
@@ -678,7 +684,7 @@ psb_status psb_q8_reduce_launch(psb_ctx* c, const int8_t* wcodes, size_t wstride
   const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((nb + 7) / 8, (size_t)c->num_sms * 8));
   const float coef = (float)(-lr);
 #define PSB_RED(V)                                                                                \
-  k_q8_reduce<V><<<grid, 256, 0, st>>>(wcodes, wstride, wscales, sstride, P, blk_lo, blk_hi, n,    \
+  k_q8_reduce<V><<<grid, 256, 0, st>>>(wv, P, blk_lo, blk_hi, n,                                    \
                                        (int)order, dpn, npr, mcodes, mscales, coef, theta, mean_out, \
                                        c->d_flags)
   switch (B) {
@@ -744,11 +750,11 @@ psb_status psb_q8_step1_launch(psb_ctx* c, const float* g, size_t gstride, float
   return PSB_OK;
 }
 
-psb_status psb_q8_apply_launch(psb_ctx* c, const int8_t* mcodes, const float* mscales, size_t n,
+psb_status psb_q8_apply_launch(psb_ctx* c, const Q8Shards& ms, int R, size_t n,
                                uint32_t B, double lr, float* theta, float* mean_out,
                                cudaStream_t st) {
   const unsigned grid = (unsigned)std::min<size_t>((n / 4 + 255) / 256 + 1, (size_t)c->num_sms * 16);
-  k_q8_apply<<<grid, 256, 0, st>>>(mcodes, mscales, n, B, (float)(-lr), theta, mean_out, c->d_flags);
+  k_q8_apply<<<grid, 256, 0, st>>>(ms, R, n, B, (float)(-lr), theta, mean_out, c->d_flags);
   c->launches += 1;
   PSB_LAUNCH_CHECK(c, "q8 apply");
   return PSB_OK;

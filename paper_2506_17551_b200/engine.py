@@ -130,6 +130,13 @@ class Context:
                  "psb_profile_read")
         return float(ms.value), int(cnt.value)
 
+    def profile_read_phase(self, phase: int) -> Tuple[float, int]:
+        """(summed ms, event pairs) of phase 1 (exchange) or 2 (apply) since the last read."""
+        ms, cnt = ctypes.c_double(), ctypes.c_uint64()
+        self._ck(self.lib.psb_profile_read_phase(self.h, phase, ctypes.byref(ms), ctypes.byref(cnt)),
+                 "psb_profile_read_phase")
+        return float(ms.value), int(cnt.value)
+
     # --------------------------------------------------------- communicator
     @staticmethod
     def unique_id() -> bytes:

@@ -1,7 +1,9 @@
 """Probe (torchrun, PSB_STEP_MARKS=1): per-milestone device time of the
-multi-rank cfg2 step, eager, max over ranks.  argv[1] = peer mode
-(shard|full|nccl).  Milestones: [wait, compress, (segoff+signal | exchange),
-(pull, fold, publish+scatter) | apply]."""
+multi-rank step, eager, per rank.  argv[1] = peer mode (shard|full|nccl).
+PROBE_COMP=topk (cfg2; milestones [wait, compress, (segoff+signal |
+exchange), (pull, fold, publish+scatter) | apply]) or q8 (cfg3 over NVLink;
+milestones [wait_ack, quantize, flag round 1, pull codes, reduce, flag round 2,
+pull mean + ack, apply])."""
 import ctypes
 import os
 import sys
@@ -20,8 +22,9 @@ rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 torch.cuda.set_device(rank)
 dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
 n = 125_000_000
-k = n // 100
-c = Context(n, k, world, device=rank)
+comp = os.environ.get("PROBE_COMP", "topk")
+k = n // 100 if comp == "topk" else 0
+c = Context(n, max(k, 1), world, device=rank)
 init_comm(c)
 c.peer_mode(mode)
 lib = L.load()
@@ -32,7 +35,8 @@ for i, g in enumerate(gs):
     generate("llmrec", 42, rank, i, n, g[0])
 res = torch.zeros(1, n, device="cuda")
 theta = torch.zeros(n, device="cuda")
-descs = [c.step_desc(L.PSB_COMP_TOPK, g, res, theta, 0.05, k, "ring") for g in gs]
+code = L.PSB_COMP_TOPK if comp == "topk" else L.PSB_COMP_Q8
+descs = [c.step_desc(code, g, res, theta, 0.05, k, "ring" if comp == "topk" else "naive", 256) for g in gs]
 buf = (ctypes.c_float * 32)()
 acc = None
 steps = 20
