@@ -118,6 +118,20 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU legs
+def host_cpu():
+    """CPU model and core count of the host the CPU leg ran on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def cpu_reference_run(n_sample: int, P: int, k: int, threads: int, budget_s: float, min_steps: int,
                       max_steps: int, dist: str, comp: str):
     """Time the reference's own sync_data_parallel_step (oracle/_ref) on a
@@ -173,7 +187,8 @@ def reference_arm(args, cfg, world, rank):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (same mix64 generator, widened to f64)",
         "config": {"workload": name, "n_params": n, "P": P, "sample_n": n_sample},
         "impl": "reference",
-        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": kind, "sample": sample},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": kind, "sample": sample,
+                         "same_config": n_sample == n, "sample_n": n_sample, "full_n": n, **host_cpu()},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -469,8 +484,11 @@ def ours(args, cfg, world, rank, local_rank):
                                                  "topk" if comp.startswith("topk") else "none")
         line["cpu_baseline"] = {
             "value": gbs, "unit": "GB/s", "cores": 1, "kind": kind,
-            "sample": f"{done} steps of reference sync_data_parallel_step at N={n_s} (P={P}, k={k_s}), "
-                      f"median {t_s:.3f} s/step, 1 thread (the reference is single-threaded)"}
+            "sample": f"SAMPLE of the workload: {done} steps of the reference's sync_data_parallel_step at "
+                      f"N={n_s} of {n} params (P={P}, k={k_s}), median {t_s:.3f} s/step, 1 thread (the reference "
+                      f"is single-threaded); its per-element cost grows with N (stable_sort), so the GB/s at "
+                      f"full N is lower (survey: 0.007 GB/s at 125M)",
+            "same_config": n_s == n, "sample_n": n_s, "full_n": n, **host_cpu()}
     print(json.dumps(line), flush=True)
     return ctx
 

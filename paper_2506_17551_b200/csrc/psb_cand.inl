@@ -262,9 +262,27 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
             __pipeline_memcpy_async(st_val + (e0 - lo) + j, a.seg_val + src + j, sizeof(T));
           }
         } else {
-          for (uint32_t j = lane; j < ct; j += 32) {
-            a.cand_idx[e0 + j] = a.seg_idx[src + j];
-            a.cand_val[e0 + j] = a.seg_val[src + j];
+          // into the global list: 8 entries per lane in flight per batch
+          constexpr int CU = 8;
+          for (uint32_t j0 = lane; j0 < ct; j0 += 32 * CU) {
+            uint32_t ci[CU];
+            T cv[CU];
+#pragma unroll
+            for (int u = 0; u < CU; ++u) {
+              const uint32_t j = j0 + 32 * u;
+              if (j < ct) {
+                ci[u] = a.seg_idx[src + j];
+                cv[u] = a.seg_val[src + j];
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < CU; ++u) {
+              const uint32_t j = j0 + 32 * u;
+              if (j < ct) {
+                a.cand_idx[e0 + j] = ci[u];
+                a.cand_val[e0 + j] = cv[u];
+              }
+            }
           }
         }
       }
@@ -426,7 +444,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       a.r[id] = v;  // unselected candidate: undo the speculative +0
     }
   };
-  if (staged) {
+  {
     // ---- early scatter: every entry whose key differs from T is decided
     // (key > T selected, key < T not); only ties at T wait for their
     // cross-CTA rank.  The theta read-modify-write and the residual fix-ups
@@ -442,11 +460,11 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
       for (int u = 0; u < U; ++u) {
         const uint32_t j = j0 + u * blockDim.x;
         if (j < cnt) {
-          v[u] = st_val[j];
+          v[u] = staged ? st_val[j] : a.cand_val[lo + j];
           const K key = KO::key(v[u]);
           if (key != T_key) {
             actm |= 1u << u;
-            id[u] = st_idx[j];
+            id[u] = staged ? st_idx[j] : a.cand_idx[lo + j];
             if (key > T_key) selm |= 1u << u;
           }
         }
@@ -633,7 +651,7 @@ __global__ void __launch_bounds__(kCandThreads, 1) k_cand(CandArgs<T> a) {
         a.idx_out[slot] = id[c];
         a.val_out[slot] = v[c];
       }
-      if (j0 + c < cnt) scatter(id[c], v[c], sel);
+      if (j0 + c < cnt && eq) scatter(id[c], v[c], sel);  // ties; the rest went in the early scatter
       before += (unsigned long long)gt | ((unsigned long long)eq << 32);
     }
     run += tot;
