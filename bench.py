@@ -236,13 +236,14 @@ def ours(args, cfg, world, rank, local_rank):
                  for b in range(NB)]
     stream.synchronize()
     gu = [0]
-    if mode == "async":
+    pipe = mode == "async" and not os.environ.get("PSB_BENCH_NO_PIPE")
+    if pipe:
         # bounded-staleness pipeline: round r's exchange + apply on the ctx's
         # apply stream overlap round r+1's compression (psb_async_pipeline)
         ctx.async_pipeline(True)
 
     def drain():  # join the apply stream back (before timing ends / capture closes)
-        if mode == "async":
+        if pipe:
             ctx.async_sync()
 
     def step(i):
@@ -416,6 +417,7 @@ def ours(args, cfg, world, rank, local_rank):
         "config": {"workload": name, "n_params": n, "k": k, "rho": rho, "workers_per_rank": W, "P": P,
                    "launch": "eager" if args.eager else "cuda-graph of the K timed steps",
                    "compressor": comp, "order": order, "mode": mode,
+                   "async_pipeline": pipe,
                    "l2": f"inputs larger than L2: {NB} rotated {4 * n * W / 1e6:.0f} MB gradient buffers"},
         "roofline": {"bound": "hbm", "kernel": k1_name,
                      "achieved": k1_gbs, "peak": peak, "peak_source": peak_src, "unit": "GB/s",

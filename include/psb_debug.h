@@ -41,6 +41,12 @@ PSB_API int psb_debug_scan_trace(unsigned long long* out, int max_ctas);
  * entries) of its slice. */
 PSB_API int psb_debug_cand_trace(unsigned long long* out, int max_ctas);
 
+/* Device timestamps (globaltimer, ns) recorded by a 1-thread kernel at points
+ * the caller chooses (graph-capturable: the slot advances on the device);
+ * psb_debug_stamps copies up to max of them and resets the count. */
+PSB_API psb_status psb_debug_stamp(psb_ctx* ctx, psb_stream_t stream);
+PSB_API int psb_debug_stamps(unsigned long long* out, int max);
+
 #ifdef __cplusplus
 }
 #endif

@@ -735,3 +735,33 @@ extern "C" PSB_API psb_status psb_debug_exchange(psb_ctx* c, size_t bytes_per_ra
   }
   return PSB_OK;
 }
+
+// ---- diagnostics: device timestamps at step boundaries (graph-capturable;
+// the slot index advances on the device)
+namespace {
+__device__ unsigned long long g_stamps[4096];
+__device__ unsigned int g_nstamps;
+__global__ void k_stamp() {
+  const unsigned int i = atomicAdd(&g_nstamps, 1u);
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (i < 4096) g_stamps[i] = t;
+}
+}  // namespace
+
+extern "C" PSB_API psb_status psb_debug_stamp(psb_ctx* c, psb_stream_t stream) {
+  PSB_REQUIRE(c, c != nullptr, "null ctx");
+  k_stamp<<<1, 1, 0, (cudaStream_t)stream>>>();
+  PSB_LAUNCH_CHECK(c, "debug stamp");
+  return PSB_OK;
+}
+
+extern "C" PSB_API int psb_debug_stamps(unsigned long long* out, int max) {
+  unsigned int n = 0;
+  if (cudaMemcpyFromSymbol(&n, g_nstamps, sizeof(n)) != cudaSuccess) return -1;
+  const int m = (int)std::min<unsigned int>(n, (unsigned int)std::min(max, 4096));
+  if (m > 0 && cudaMemcpyFromSymbol(out, g_stamps, sizeof(unsigned long long) * m) != cudaSuccess) return -1;
+  const unsigned int z = 0;
+  cudaMemcpyToSymbol(g_nstamps, &z, sizeof(z));
+  return m;
+}
