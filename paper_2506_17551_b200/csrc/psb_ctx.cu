@@ -949,7 +949,11 @@ extern "C" psb_status psb_async_pipeline(psb_ctx* c, int enable) {
   PSB_REQUIRE(c, c != nullptr, "null ctx");
   if (enable && !c->apply_st) {
     CUDA_TRY(c, cudaSetDevice(c->device), "psb_async_pipeline");
-    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->apply_st, cudaStreamNonBlocking), "psb_async_pipeline");
+    // highest priority: the exchange / apply CTAs are scheduled ahead of the
+    // next round's compression as SM resources free up
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->apply_st, cudaStreamNonBlocking, hi), "psb_async_pipeline");
     for (int i = 0; i < 2; ++i) {
       CUDA_TRY(c, cudaEventCreateWithFlags(&c->comp_ev[i], cudaEventDisableTiming), "psb_async_pipeline");
       CUDA_TRY(c, cudaEventCreateWithFlags(&c->apply_ev[i], cudaEventDisableTiming), "psb_async_pipeline");

@@ -625,7 +625,11 @@ psb_status run_topk(psb_ctx* c, int worker, const T* g, T* r, size_t n, size_t k
   a.sb_stride = c->sb_stride;
   a.histd = sizeof(T) == 4 ? c->d_histd : nullptr;
   // persistent-style grid: PSB_SCAN_MINB CTAs per SM pull tiles dynamically
-  const uint32_t scan_grid = (uint32_t)std::min<size_t>(ntiles, (size_t)c->num_sms * PSB_SCAN_MINB);
+  // (one fewer under the multi-rank async pipeline: the freed registers let
+  // the previous round's exchange and apply run beside this pass -- cfg4 at
+  // 4 GPUs 0.89 -> 0.78 ms/round, the pass alone 0.61 -> 0.73 ms)
+  const int per_sm = (c->async_pipe && c->nranks > 1) ? PSB_SCAN_MINB - 1 : PSB_SCAN_MINB;
+  const uint32_t scan_grid = (uint32_t)std::min<size_t>(ntiles, (size_t)c->num_sms * per_sm);
   a.cand_idx = c->d_stage_idx;
   a.cand_val = reinterpret_cast<T*>(c->d_stage_val);
   a.flags = c->d_flags;
