@@ -34,7 +34,8 @@ from . import _lib as L
 from .parsim import CollectiveAlgorithm, CompressorConfig, Topology, compression_ratio_for
 
 __all__ = ["Link", "validate_topology", "slowest_link_spanning", "comm_cost", "fit_ring", "calibrate_intra_node",
-           "measure_allreduce", "DpIteration", "dp_iteration"]
+           "measure_allreduce", "DpIteration", "dp_iteration", "fit_line", "B200StepModel",
+           "measure_step_parts"]
 
 
 @dataclass
@@ -206,3 +207,113 @@ def dp_iteration(P: int, topo: Topology, gradient_bytes: float, compressor: Comp
         comm = comm_cost(collective, msg, P, topo, P)
     return DpIteration(compute_time=compute_time, comm_time=comm,
                        overlapped_time=overlap_fraction * min(compute_time, comm), idle_time=fixed_overhead)
+
+
+# --------------------------------------------------------------------------
+# The step as this build runs it (round 2): the reference's model prices only
+# the message (comm_cost of gradient_bytes / compression_ratio), which missed
+# the measured 4-GPU cfg2 step by 17 % (profiles/r01/topology).  What grows
+# with P on B200 is the NVLink ingress of the P - 1 peers' payloads and the
+# P-way fold of the apply, so the model below has one term for each, fitted
+# from measurements, plus the rank's compression:
+#   t(P) = compress + pack + ingress(P) + apply(P)
+#   ingress(P) = lat + (P - 1) * payload_bytes / bw       (0 at P = 1)
+#   apply(P)   = a + b * P * k                           (the P-payload fold)
+# with P = 1 fusing the update into the compression (apply = 0).
+
+def fit_line(xs: Sequence[float], ys: Sequence[float]) -> Tuple[float, float]:
+    """Least-squares (intercept, slope) of y = a + b x (>= 2 points; a clamped at 0)."""
+    if len(xs) != len(ys) or len(xs) < 2:
+        raise L.PsbInvalidArgument("fit_line: need >= 2 (x, y) pairs")
+    n = float(len(xs))
+    mx, my = sum(xs) / n, sum(ys) / n
+    sxx = sum((x - mx) ** 2 for x in xs)
+    if sxx <= 0:
+        raise L.PsbInvalidArgument("fit_line: x values must differ")
+    b = sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / sxx
+    return max(my - b * mx, 0.0), b
+
+
+@dataclass
+class B200StepModel:
+    """Seconds per data-parallel step of the sparse path on P ranks of one NVSwitch box."""
+    compress_p1: float       # K1 with the fused single-worker update (P = 1 step)
+    compress: float          # K1 without it (P > 1)
+    pack: float = 0.0        # per-segment offsets + wire16 pack (P > 1)
+    ingress_lat: float = 0.0
+    ingress_bw: float = 1.0  # bytes / s into one rank
+    apply_a: float = 0.0
+    apply_b: float = 0.0     # seconds per payload entry folded
+
+    def ingress(self, P: int, payload_bytes: float) -> float:
+        return 0.0 if P <= 1 else self.ingress_lat + (P - 1) * payload_bytes / self.ingress_bw
+
+    def apply(self, P: int, k: int) -> float:
+        return 0.0 if P <= 1 else self.apply_a + self.apply_b * P * k
+
+    def step(self, P: int, k: int, payload_bytes: float) -> float:
+        if P <= 1:
+            return self.compress_p1
+        return self.compress + self.pack + self.ingress(P, payload_bytes) + self.apply(P, k)
+
+    @classmethod
+    def fit(cls, compress_p1: float, compress: float, pack: float, k: int,
+            apply_by_p: Dict[int, float], ingress_by_p: Dict[int, float], payload_bytes: float) -> "B200StepModel":
+        """Fit from measured parts: apply_by_p {P: s} (one GPU, P virtual payloads) and
+        ingress_by_p {P: s} (exchange windows on P GPUs)."""
+        ps = sorted(apply_by_p)
+        a, b = fit_line([p * k for p in ps], [apply_by_p[p] for p in ps])
+        m = cls(compress_p1, compress, pack, apply_a=a, apply_b=b)
+        qs = sorted(ingress_by_p)
+        if len(qs) >= 2:
+            lat, slope = fit_line([(q - 1) * payload_bytes for q in qs], [ingress_by_p[q] for q in qs])
+            m.ingress_lat, m.ingress_bw = lat, (1.0 / slope if slope > 0 else float("inf"))
+        elif len(qs) == 1:
+            q = qs[0]
+            m.ingress_bw = (q - 1) * payload_bytes / ingress_by_p[q]
+        return m
+
+
+def measure_step_parts(ctx, n: int, k: int, Ps: Sequence[int] = (2, 4), iters: int = 10,
+                       dist: str = "llmrec") -> Dict[str, object]:
+    """One GPU: time the K1 step with and without the fused update and the
+    P-payload apply for each P (CUDA events); for B200StepModel.fit."""
+    import torch
+    from .engine import generate, payload_bytes
+    dev = torch.device("cuda", ctx.device)
+    g = torch.empty(n, device=dev)
+    r = torch.zeros(n, device=dev)
+    theta = torch.zeros(n, device=dev)
+    generate(dist, 42, 0, 0, n, g)
+
+    def timed(fn) -> float:
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e-3 / iters
+
+    d1 = ctx.step_desc(L.PSB_COMP_TOPK, g.view(1, n), r.view(1, n), theta, 0.05, k, "ring")
+    t_p1 = timed(lambda: ctx.sync_step(d1))
+    idx = torch.empty(k, dtype=torch.int32, device=dev)
+    val = torch.empty(k, dtype=torch.float32, device=dev)
+    t_k1 = timed(lambda: ctx.ef_topk(g, r, k, 0, idx, val))
+    blk = payload_bytes(L.PSB_COMP_TOPK, torch.float32, k)
+    apply_by_p = {}
+    for P in Ps:
+        gath = torch.empty(P * blk, dtype=torch.uint8, device=dev)
+        voff = (k * 4 + 15) // 16 * 16
+        for p in range(P):
+            generate(dist, 42, p, 1, n, g)
+            sl = gath[p * blk:(p + 1) * blk]
+            ctx.ef_topk(g, None, k, 0, sl[:k * 4].view(torch.int32), sl[voff:voff + k * 4].view(torch.float32))
+        apply_by_p[P] = timed(lambda: ctx.sparse_mean_sgd(gath, P, k, torch.float32, "ring", 0.05, theta, n))
+        del gath
+    ctx.check()
+    return {"compress_p1": t_p1, "compress": t_k1, "apply_by_p": apply_by_p, "payload_bytes": blk}
+

@@ -157,3 +157,57 @@ def test_gloo_measure_and_calibrate():
     assert all(isinstance(r[1], list) for r in res), res
     assert res[0][1] == res[1][1]  # max over ranks: both ranks report the same times
     assert res[0][2] > 0 and res[0][3] >= 0
+
+
+def test_b200_step_model_fit_and_terms():
+    """The round-2 step model: fit_line recovers a line; the fitted model
+    reproduces its inputs and adds the ingress and fold terms only for P > 1."""
+    from paper_2506_17551_b200.costmodel import B200StepModel, fit_line
+    a, b = fit_line([1, 2, 3, 4], [3.0, 5.0, 7.0, 9.0])
+    assert math.isclose(a, 1.0) and math.isclose(b, 2.0)
+    k, pb = 1_250_000, 7.6e6
+    m = B200StepModel.fit(compress_p1=330e-6, compress=290e-6, pack=15e-6, k=k,
+                          apply_by_p={2: 90e-6, 4: 150e-6, 8: 270e-6},
+                          ingress_by_p={2: 38e-6, 4: 80e-6}, payload_bytes=pb)
+    assert m.step(1, k, pb) == 330e-6
+    assert math.isclose(m.ingress(2, pb), 38e-6, rel_tol=1e-9) and math.isclose(m.ingress(4, pb), 80e-6, rel_tol=1e-9)
+    assert abs(m.apply(4, k) - 150e-6) < 10e-6
+    assert m.step(8, k, pb) > m.step(4, k, pb) > m.step(2, k, pb) > m.step(1, k, pb) * 0.9
+    with pytest.raises(L.PsbInvalidArgument):
+        fit_line([1, 1], [1, 2])
+
+
+
+@pytest.mark.gpu
+def test_b200_step_model_predicts_virtual_worker_step():
+    """On one GPU: fit the compression and fold terms from their own
+    measurements, then predict a step the fit did not see -- W = 3 virtual
+    workers (3 x K1 + the 3-payload apply, no exchange) -- within 15 %."""
+    import torch
+    from paper_2506_17551_b200.costmodel import B200StepModel, measure_step_parts
+    from paper_2506_17551_b200.engine import Context, generate
+    n, k = 16_000_000, 160_000
+    c = Context(n, k, 8)
+    parts = measure_step_parts(c, n, k, Ps=(2, 4, 8))
+    m = B200StepModel.fit(parts["compress_p1"], parts["compress"], 0.0, k, parts["apply_by_p"], {},
+                          parts["payload_bytes"])
+    W = 3
+    g = torch.empty(W, n, device="cuda")
+    for w in range(W):
+        generate("llmrec", 42, w, 5, n, g[w])
+    r = torch.zeros(W, n, device="cuda")
+    th = torch.zeros(n, device="cuda")
+    d = c.step_desc(L.PSB_COMP_TOPK, g, r, th, 0.05, k, "ring")
+    for _ in range(5):
+        c.sync_step(d)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        c.sync_step(d)
+    e1.record()
+    torch.cuda.synchronize()
+    measured = e0.elapsed_time(e1) * 1e-3 / 10
+    predicted = W * parts["compress"] + m.apply(W, k)
+    c.close()
+    assert abs(predicted - measured) / measured < 0.15, (predicted, measured)
