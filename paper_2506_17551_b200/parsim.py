@@ -261,11 +261,17 @@ def decompress(c: CompressedGradient) -> torch.Tensor:
     if isinstance(p, SignBitPayload):
         if p.sign_bytes.numel() != (p.dim + 7) // 8:
             raise L.PsbInvalidArgument("decompress: sign byte count does not match dim")
-        sb = p.sign_bytes.to(device="cuda", dtype=torch.uint8)
-        bits = ((sb.view(-1, 1) >> torch.arange(8, device=sb.device, dtype=torch.uint8)) & 1)
-        pos = bits.view(-1)[: p.dim].bool()
-        s = torch.full((p.dim,), p.scale, dtype=torch.float64, device="cuda")
-        return torch.where(pos, s, -s)
+        # +-scale per sign bit on the device: the 1-bit mean kernel with one
+        # worker (mean = value * (1/1), exact), as parsim_b200.hpp does
+        nw = (p.dim + 31) // 32
+        words = torch.zeros(nw * 4, dtype=torch.uint8, device="cuda")
+        words[: p.sign_bytes.numel()] = p.sign_bytes.to(device="cuda", dtype=torch.uint8)
+        scale = torch.tensor([p.scale], dtype=torch.float64, device="cuda")
+        out = torch.empty(p.dim, dtype=torch.float64, device="cuda")
+        ctx = _ctx(max(p.dim, 1))
+        ctx.onebit_mean_sgd(words.view(torch.int32), scale, p.dim, torch.float64, "naive", 0.0, None, mean_out=out)
+        ctx.check()
+        return out
     if p.indices.numel() != p.values.numel():
         raise L.PsbInvalidArgument("decompress: index/value count mismatch")
     vals = as_vector(p.values)

@@ -235,23 +235,24 @@ def train(users: int, items: int, dim: int, train_users: Sequence[int], train_it
                     lo, hi = shard(p)
                     g = grads[p]
                     ctx.bpr_gradient(snap, users, items, dim, *dev(batch[lo:hi]), grad=g, want_loss=False)
+                    onebit = None
                     if compressed:  # ef_compress_step then decompress (trainer.hpp:248)
                         if compressor == "topk":
                             idx, val = ctx.ef_topk(g, res[p], top_k)
                             g = ctx.decompress_topk(idx, val, n)
                         else:
-                            words, scale = ctx.ef_onebit(g, res[p])
-                            bits = (words.view(torch.uint8).unsqueeze(1) >> torch.arange(
-                                8, device="cuda", dtype=torch.uint8)) & 1
-                            pos = bits.reshape(-1)[:n].bool()
-                            s = scale.to(torch.float64)
-                            g = torch.where(pos, s, -s)
+                            onebit = ctx.ef_onebit(g, res[p])
                     history.append(theta.clone())
                     if len(history) > 3:
                         history.popleft()
-                    # async_step: theta - eta/(1+tau) * g  (strategies.hpp:125-129)
+                    # async_step: theta - eta/(1+tau) * g  (strategies.hpp:125-129);
+                    # a 1-bit message is applied straight from its sign words
+                    # (the one-worker 1-bit mean is +-scale exactly)
                     scale = lr / (1.0 + float(tau))
-                    ctx.dense_mean_sgd(g.unsqueeze(0), "naive", scale, theta)
+                    if onebit is not None:
+                        ctx.onebit_mean_sgd(onebit[0], onebit[1], n, torch.float64, "naive", scale, theta)
+                    else:
+                        ctx.dense_mean_sgd(g.unsqueeze(0), "naive", scale, theta)
                     updates += 1
         ctx.check()
     finally:

@@ -21,7 +21,8 @@ def test_sampler_and_init_match_reference_stream():
 
 
 @pytest.mark.parametrize("mode,kind,k,P", [("sync", "none", 0, 2), ("sync", "topk", 30, 2), ("sync", "topk", 30, 4),
-                                           ("async", "topk", 30, 4), ("async", "none", 0, 2)])
+                                           ("async", "topk", 30, 4), ("async", "none", 0, 2),
+                                           ("sync", "onebit", 0, 2), ("async", "onebit", 0, 4)])
 def test_train_matches_reference(mode, kind, k, P):
     users, items, dim, steps, batch, lr, seed = 30, 50, 8, 120, 32, 0.05, 7
     rng = np.random.default_rng(1)

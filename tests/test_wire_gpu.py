@@ -88,3 +88,18 @@ def test_facade_round_trips_as_the_reference_test():
     assert ps.compression_ratio_for(ps.CompressorConfig(ps.CompressorKind.onebit, 0), 64) == pytest.approx(512 / 24)
     assert ps.compression_ratio_for(ps.CompressorConfig(ps.CompressorKind.none, 0), 64) == 1.0
     assert ps.compression_ratio_for(ps.CompressorConfig(ps.CompressorKind.topk, 8), 8) < 1.0
+
+
+@pytest.mark.parametrize("n", [1, 7, 33, 1000, 1 << 20])
+def test_decompress_signbit_on_device(n):
+    """decompress(SignBitPayload) (compression.hpp:118-126): +-scale per sign
+    bit, ragged last byte, through the device 1-bit kernel."""
+    rng = np.random.default_rng(n)
+    signs = rng.integers(0, 2, n).astype(bool)
+    sb = np.packbits(signs, bitorder="little")
+    scale = float(rng.random()) + 0.25
+    got = ps.decompress(ps.CompressedGradient(ps.SignBitPayload(n, scale, torch.from_numpy(sb))))
+    want = np.where(signs, scale, -scale)
+    assert got.dtype == torch.float64 and np.array_equal(got.cpu().numpy(), want)
+    with pytest.raises(L.PsbInvalidArgument):
+        ps.decompress(ps.CompressedGradient(ps.SignBitPayload(n + 8, scale, torch.from_numpy(sb))))
