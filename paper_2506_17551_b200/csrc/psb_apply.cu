@@ -149,8 +149,7 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
   T* sval = reinterpret_cast<T*>(pre + (size_t)P * NW);  // [vcap] staged values
   __shared__ uint32_t lo[PSB_MAX_P], vb[PSB_MAX_P + 1];
   __shared__ T coefs[PSB_MAX_P];
-  __shared__ unsigned long long sh_scan[32];
-  __shared__ uint32_t sh_lbase;
+  __shared__ uint16_t wlist[apply_threads(PT) / 32][1024];  // per-warp touched-index list
   if (ASYNC && threadIdx.x < (unsigned)P) coefs[threadIdx.x] = (T)(-wscale.v[threadIdx.x]);
   const T inv = (T)(1.0 / (double)P);
   bool bad = false;
@@ -264,52 +263,57 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
     }
     APPLY_MARK(1);
     __syncthreads();
-    // list mode (sharded multi-rank apply): every touched index of the
-    // segment gets one slot of the update list, in (word, bit) order
-    uint32_t lpos = 0;
-    if (list_idx) {
-      uint32_t cnt = 0;
-      for (uint32_t w = threadIdx.x; w < NW; w += blockDim.x) {
-        uint32_t uni = 0;
-        for (int q = 0; q < P; ++q) uni |= bm[(size_t)q * NW + w];
-        cnt += __popc(uni);
-      }
-      unsigned long long tsum;
-      const uint32_t ex = (uint32_t)block_exscan_u64(cnt, sh_scan, &tsum);
-      if (threadIdx.x == 0) sh_lbase = atomicAdd(list_cnt, (uint32_t)tsum);
-      __syncthreads();
-      lpos = sh_lbase + ex;
-    }
-    // 2. fold and update by bitmap word: a thread takes word w of the
-    //    segment, ORs the P workers' words, and folds each touched index;
-    //    theta loads of up to U indices are issued together
-    for (uint32_t w = threadIdx.x; w < NW; w += blockDim.x) {
+    // 2. fold and update.  Each warp compacts the touched indices of 32
+    //    bitmap words at a time into its shared list (word, bit order), then
+    //    folds them lane-parallel: the lanes' work no longer follows the
+    //    words' popcounts, and neighbouring lanes read neighbouring theta
+    //    sectors.  theta loads of up to U indices are issued together.
+    for (uint32_t w0 = (threadIdx.x >> 5) << 5; w0 < NW; w0 += blockDim.x) {
+      const uint32_t w = w0 + lane;  // NW is a multiple of 32 (S >= 2^10)
       uint32_t uni = 0;
       for (int q = 0; q < P; ++q) uni |= bm[(size_t)q * NW + w];
-      while (uni) {
-        uint32_t bs[U];
+      const uint32_t c = __popc(uni);
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += t;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      if (!total) continue;  // uniform across the warp
+      uint16_t* wl = wlist[threadIdx.x >> 5];
+      for (uint32_t off = incl - c; uni; uni &= uni - 1) wl[off++] = (uint16_t)((w << 5) | (__ffs(uni) - 1));
+      uint32_t lbase = 0;
+      if (list_idx) {  // list mode (sharded multi-rank apply): one slot per touched index
+        if (lane == 0) lbase = atomicAdd(list_cnt, total);
+        lbase = __shfl_sync(0xffffffffu, lbase, 0);
+      }
+      __syncwarp();
+      for (uint32_t t0 = lane; t0 < total; t0 += 32 * U) {
+        uint32_t li[U];
         T th[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          bs[u] = 32;
-          if (uni) {
-            bs[u] = __ffs(uni) - 1;
-            uni &= uni - 1;
-            th[u] = theta ? theta[seg_base + w * 32 + bs[u]] : T(0);
+          const uint32_t t = t0 + 32 * u;
+          li[u] = 0xffffffffu;
+          if (t < total) {
+            li[u] = wl[t];
+            th[u] = theta ? theta[seg_base + li[u]] : T(0);
           }
         }
         auto finish = [&](auto get) {
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            if (bs[u] >= 32) continue;
-            const uint32_t bit = 1u << bs[u], below = bit - 1u;
-            const size_t i = seg_base + w * 32 + bs[u];
-            auto g = [&](int q2) { return get(q2, bit, below); };
+            if (li[u] == 0xffffffffu) continue;
+            const uint32_t ww = li[u] >> 5;
+            const uint32_t bit = 1u << (li[u] & 31), below = bit - 1u;
+            const size_t i = seg_base + li[u];
+            auto g = [&](int q2) { return get(q2, ww, bit, below); };
             T t = th[u];
             if (ASYNC) {
               auto step = [&](int q2) {
                 const T x = add_rn(mul_rn(coefs[q2], g(q2)), t);
-                t = (bm[(size_t)q2 * NW + w] & bit) ? x : t;
+                t = (bm[(size_t)q2 * NW + ww] & bit) ? x : t;
               };
               if constexpr (PT > 0) {
 #pragma unroll
@@ -328,29 +332,30 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
               bad |= !is_finite(t);
             }
             if (list_idx) {
-              list_idx[lpos] = (uint32_t)i;
-              list_val[lpos] = t;
-              ++lpos;
+              const uint32_t lp = lbase + t0 + 32 * u;
+              list_idx[lp] = (uint32_t)i;
+              list_val[lp] = t;
             }
           }
         };
         if (staged) {
           // branch-free: every worker's lookup is issued; absent ones read a
           // clamped (unused) slot and contribute +0
-          finish([&](int q2, uint32_t bit, uint32_t below) -> T {
-            const uint32_t word = bm[(size_t)q2 * NW + w];
-            const uint32_t at = min(vb[q2] + pre[(size_t)q2 * NW + w] + __popc(word & below), vcap - 1);
+          finish([&](int q2, uint32_t ww, uint32_t bit, uint32_t below) -> T {
+            const uint32_t word = bm[(size_t)q2 * NW + ww];
+            const uint32_t at = min(vb[q2] + pre[(size_t)q2 * NW + ww] + __popc(word & below), vcap - 1);
             const T x = sval[at];
             return (word & bit) ? x : T(0);
           });
         } else {
-          finish([&](int q2, uint32_t bit, uint32_t below) -> T {
-            const uint32_t word = bm[(size_t)q2 * NW + w];
+          finish([&](int q2, uint32_t ww, uint32_t bit, uint32_t below) -> T {
+            const uint32_t word = bm[(size_t)q2 * NW + ww];
             if (!(word & bit)) return T(0);
-            return pl_val<T>(v, q2, lo[q2] + pre[(size_t)q2 * NW + w] + __popc(word & below));
+            return pl_val<T>(v, q2, lo[q2] + pre[(size_t)q2 * NW + ww] + __popc(word & below));
           });
         }
       }
+      __syncwarp();  // the list is rewritten by the warp's next chunk
     }
     APPLY_MARK(2);
   }
