@@ -116,9 +116,9 @@ __global__ void __launch_bounds__(256) k_seg_offsets(PayloadView v, int P, uint3
 // batched so the global loads of a thread overlap, and staged in shared
 // memory as (local index, value) when tot <= vcap.  Each worker's touched
 // indices become a presence bitmap; the first entry of a worker in each
-// bitmap word records its rank there, so the position of index i in worker
-// q2's list is pre[q2][w] + popc(word & below) (only words holding a set bit
-// are ever queried, so no scan is needed).  The lowest worker touching i owns
+// bitmap word records its flat entry index there, so the entry of index i in
+// worker q2's list is pre[q2][w] + popc(word & below) (only words holding a
+// set bit are ever queried, so no scan is needed).  The lowest worker touching i owns
 // it: it folds the P dense values (+0 where absent) in the configured
 // reference order and updates theta once (async: applies the present workers
 // in order).  Dependent global round trips per segment: segment offsets,
@@ -126,6 +126,9 @@ __global__ void __launch_bounds__(256) k_seg_offsets(PayloadView v, int P, uint3
 // compile time (worker lookup in registers); PT == 0 is the generic kernel.
 #ifndef PSB_APPLY_U
 #define PSB_APPLY_U 2
+#endif
+#ifndef PSB_APPLY_U1
+#define PSB_APPLY_U1 2
 #endif
 // CTA shape per compile-time P (measured on B200): 256 threads x 4 CTAs/SM,
 // and 128 x 6 for P = 8 (more segments in flight; P = 8 324 -> 269 us).
@@ -140,7 +143,8 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
                       WorkerCoefs wscale, T* __restrict__ theta, size_t n, T* __restrict__ mean_out,
                       uint32_t* __restrict__ list_idx, T* __restrict__ list_val, uint32_t* list_cnt,
                       uint32_t* flags) {
-  constexpr int U = PSB_APPLY_U;  // entries per thread per batch
+  constexpr int U = PSB_APPLY_U;    // touched indices per thread per batch (fold)
+  constexpr int U1 = PSB_APPLY_U1;  // entries per thread per batch (bitmaps + staging)
   const int P = PT > 0 ? PT : P_rt;
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t NW = (1u << seg_shift) >> 5;  // bitmap words per worker
@@ -162,7 +166,8 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
   // a peer timed out in the exchange (flag 8, psb_peer.cu): its payload slot
   // may hold the previous step's data, so theta is left untouched and the
   // step reports PSB_ESTATE at the caller's psb_check
-  if (flags != nullptr && (__ldcg(flags) & 8u)) return;
+  // (checked once the first segment's offsets are in, so the two loads overlap)
+  const uint32_t flag0 = flags != nullptr ? __ldcg(flags) : 0u;
   if (range) {  // segment range decided on the device (sharded multi-rank apply)
     seg_lo = range[0];
     nseg = range[1] - range[0];
@@ -196,6 +201,7 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
     }
     __syncthreads();
     APPLY_MARK(0);
+    if (flag0 & 8u) return;  // uniform across the CTA
     const uint32_t tot = vb[P];
     if (!tot) continue;  // uniform across the CTA
     const bool staged = tot <= vcap;
@@ -223,12 +229,12 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
       return q;
     };
     // 1. presence bitmaps, word ranks, staging; a batch issues all its loads first
-    for (uint32_t e0 = threadIdx.x; e0 < tot; e0 += U * blockDim.x) {
-      uint32_t il[U], ilp[U], r[U];
-      T val[U];
-      int qq[U];
+    for (uint32_t e0 = threadIdx.x; e0 < tot; e0 += U1 * blockDim.x) {
+      uint32_t il[U1], ilp[U1];
+      T val[U1];
+      int qq[U1];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
+      for (int u = 0; u < U1; ++u) {
         const uint32_t e = e0 + u * blockDim.x;
         qq[u] = -1;
         if (e < tot) {
@@ -237,7 +243,6 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
           const uint32_t rq = e - base;
           const uint32_t j = lo[q] + rq;
           qq[u] = q;
-          r[u] = rq;
           if (v.idx16) {  // wire16: the in-segment offset is stored directly
             const uint16_t* lo16 = reinterpret_cast<const uint16_t*>(pl_block(v, q));
             il[u] = lo16[j];
@@ -251,11 +256,12 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
         }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
+      for (int u = 0; u < U1; ++u) {
         if (qq[u] < 0) continue;
         const uint32_t w = il[u] >> 5;
         atomicOr(&bm[(size_t)qq[u] * NW + w], 1u << (il[u] & 31));
-        if (ilp[u] == 0xffffffffu || (ilp[u] >> 5) != w) pre[(size_t)qq[u] * NW + w] = r[u];
+        // the flat entry index of the word's first entry: vb[q] + rank
+        if (ilp[u] == 0xffffffffu || (ilp[u] >> 5) != w) pre[(size_t)qq[u] * NW + w] = e0 + u * blockDim.x;
         if (staged) sval[e0 + u * blockDim.x] = val[u];
         // warm L2 with theta at this index: phase 2 reads it after the barrier
         if (theta) asm volatile("prefetch.global.L2 [%0];" ::"l"(theta + seg_base + il[u]));
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
           // clamped (unused) slot and contribute +0
           finish([&](int q2, uint32_t ww, uint32_t bit, uint32_t below) -> T {
             const uint32_t word = bm[(size_t)q2 * NW + ww];
-            const uint32_t at = min(vb[q2] + pre[(size_t)q2 * NW + ww] + __popc(word & below), vcap - 1);
+            const uint32_t at = min(pre[(size_t)q2 * NW + ww] + __popc(word & below), vcap - 1);
             const T x = sval[at];
             return (word & bit) ? x : T(0);
           });
@@ -351,7 +357,7 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
           finish([&](int q2, uint32_t ww, uint32_t bit, uint32_t below) -> T {
             const uint32_t word = bm[(size_t)q2 * NW + ww];
             if (!(word & bit)) return T(0);
-            return pl_val<T>(v, q2, lo[q2] + pre[(size_t)q2 * NW + ww] + __popc(word & below));
+            return pl_val<T>(v, q2, lo[q2] - vb[q2] + pre[(size_t)q2 * NW + ww] + __popc(word & below));
           });
         }
       }
