@@ -110,183 +110,315 @@ __global__ void __launch_bounds__(256) k_seg_offsets(PayloadView v, int P, uint3
     row[s] = k;
 }
 
-// Bitmap-rank apply (P >= 2).  One CTA per segment of S = 2^seg_shift
-// indices.  The segment's entries of all P workers form one flat range
-// e in [0, tot) (worker q owns [vb[q], vb[q+1])); they are loaded once,
-// batched so the global loads of a thread overlap, and staged in shared
-// memory as (local index, value) when tot <= vcap.  Each worker's touched
+// Bitmap-rank apply (P >= 2), one segment of S = 2^seg_shift indices at a
+// time.  The segment's entries of all P workers form one flat range
+// e in [0, tot) (worker q owns [vb[q], vb[q+1])).  Each worker's touched
 // indices become a presence bitmap; the first entry of a worker in each
-// bitmap word records its flat entry index there, so the entry of index i in
-// worker q2's list is pre[q2][w] + popc(word & below) (only words holding a
-// set bit are ever queried, so no scan is needed).  The lowest worker touching i owns
-// it: it folds the P dense values (+0 where absent) in the configured
-// reference order and updates theta once (async: applies the present workers
-// in order).  Dependent global round trips per segment: segment offsets,
-// entry loads, theta -- the rest is shared memory.  PT > 0 fixes P at
-// compile time (worker lookup in registers); PT == 0 is the generic kernel.
+// bitmap word records that entry's position in the value stage there, so the
+// value of index i in worker q2's list sits at pre[q2][w] + popc(word &
+// below) (only words holding a set bit are ever queried, so no scan is
+// needed).  The lowest worker touching i owns it: it folds the P dense values
+// (+0 where absent) in the configured reference order and updates theta once
+// (async: applies the present workers in order).  PT > 0 fixes P at compile
+// time (worker lookup in registers); PT == 0 is the generic kernel.
+//
+// TMA (the default for gathered f32/f64 top-k and wire16 payloads):
+// persistent CTAs, and each segment's entries (index and value ranges of the
+// P workers, widened to 16-byte boundaries) arrive in shared memory by 1-D
+// bulk copies on an mbarrier, double-buffered: warp 0 issues the copies of
+// the CTA's next segment between the two phases of the current one, so the
+// entry loads overlap the current fold and the dependent global round trips
+// left per segment are the theta loads.  A segment too large for the stage
+// reads its entries from global memory (the non-TMA path).
+// Without TMA (q8 values, direct / sharded multi-rank views): one CTA per
+// segment, entries loaded by the threads in batches and staged when tot <=
+// vcap.
 #ifndef PSB_APPLY_U
 #define PSB_APPLY_U 2
 #endif
 #ifndef PSB_APPLY_U1
 #define PSB_APPLY_U1 2
 #endif
-// CTA shape per compile-time P (measured on B200): 256 threads x 4 CTAs/SM,
-// and 128 x 6 for P = 8 (more segments in flight; P = 8 324 -> 269 us).
-__host__ __device__ constexpr int apply_threads(int PT) { return PT == 8 ? 128 : 256; }
-__host__ __device__ constexpr int apply_minb(int PT) { return PT == 8 ? 6 : 4; }
+// CTA shapes (measured on B200): non-TMA 256 threads x 4 CTAs/SM, and
+// 128 x 6 for P = 8 (more segments in flight; P = 8 324 -> 269 us); TMA
+// 256 x 3 (the double-buffered stage).
+#ifndef PSB_APPLY_TMA_MINB
+#define PSB_APPLY_TMA_MINB 3
+#endif
+__host__ __device__ constexpr int apply_threads(int PT, bool TMA) { return TMA ? 256 : PT == 8 ? 128 : 256; }
+__host__ __device__ constexpr int apply_minb(int PT, bool TMA) { return TMA ? PSB_APPLY_TMA_MINB : PT == 8 ? 6 : 4; }
 
-template <class T, bool ASYNC, int PT>
-__global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
+template <class T, bool ASYNC, int PT, bool TMA>
+__global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
     k_sparse_apply_bm(PayloadView v, int P_rt, uint32_t nseg, uint32_t seg_lo, const uint32_t* __restrict__ range,
-                      int seg_shift, uint32_t vcap,
+                      int seg_shift, uint32_t vcap, uint32_t ci_bytes, uint32_t cv_bytes,
                       const uint32_t* __restrict__ seg_off, int order, uint32_t dpn, uint32_t npr, T coef,
                       WorkerCoefs wscale, T* __restrict__ theta, size_t n, T* __restrict__ mean_out,
                       uint32_t* __restrict__ list_idx, T* __restrict__ list_val, uint32_t* list_cnt,
                       uint32_t* flags) {
   constexpr int U = PSB_APPLY_U;    // touched indices per thread per batch (fold)
-  constexpr int U1 = PSB_APPLY_U1;  // entries per thread per batch (bitmaps + staging)
+  constexpr int U1 = PSB_APPLY_U1;  // entries per thread per batch (global entry loads)
   const int P = PT > 0 ? PT : P_rt;
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t NW = (1u << seg_shift) >> 5;  // bitmap words per worker
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem);  // [P][NW] presence bits
-  uint32_t* pre = bm + (size_t)P * NW;                 // [P][NW] rank of a word's first entry
-  T* sval = reinterpret_cast<T*>(pre + (size_t)P * NW);  // [vcap] staged values
-  __shared__ uint32_t lo[PSB_MAX_P], vb[PSB_MAX_P + 1];
+  uint32_t* pre = bm + (size_t)P * NW;                 // [P][NW] stage position of a word's first entry
+  unsigned char* stage0 = reinterpret_cast<unsigned char*>(pre + (size_t)P * NW);
+  // segment descriptors, double-buffered under TMA: first payload position,
+  // flat entry bases, stage positions of each worker's first index / value
+  __shared__ uint32_t lo_s[2][PSB_MAX_P], vb_s[2][PSB_MAX_P + 1], bi_s[2][PSB_MAX_P], bv_s[2][PSB_MAX_P];
+  __shared__ uint32_t stg_s[2];
+  __shared__ __align__(8) uint64_t mbar[2];
   __shared__ T coefs[PSB_MAX_P];
-  __shared__ uint16_t wlist[apply_threads(PT) / 32][1024];  // per-warp touched-index list
+  __shared__ uint16_t wlist[apply_threads(PT, TMA) / 32][1024];  // per-warp touched-index list
   if (ASYNC && threadIdx.x < (unsigned)P) coefs[threadIdx.x] = (T)(-wscale.v[threadIdx.x]);
   const T inv = (T)(1.0 / (double)P);
   bool bad = false;
   RingChunk rc;
   const uint32_t lane = threadIdx.x & 31;
+  const bool warp0 = threadIdx.x < 32;
+  const uint32_t ib = v.idx16 ? 2u : 4u;  // bytes per stored index
 
 #ifdef PSB_APPLY_TRACE
   unsigned long long t_prev = gtimer();
 #endif
   // a peer timed out in the exchange (flag 8, psb_peer.cu): its payload slot
   // may hold the previous step's data, so theta is left untouched and the
-  // step reports PSB_ESTATE at the caller's psb_check
-  // (checked once the first segment's offsets are in, so the two loads overlap)
+  // step reports PSB_ESTATE at the caller's psb_check (checked once the
+  // first segment's offsets are in, so the two loads overlap; no copy is
+  // issued when it is set)
   const uint32_t flag0 = flags != nullptr ? __ldcg(flags) : 0u;
   if (range) {  // segment range decided on the device (sharded multi-rank apply)
     seg_lo = range[0];
     nseg = range[1] - range[0];
   }
-  for (uint32_t seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
-    __syncthreads();  // the previous segment is done with shared memory
-    if (threadIdx.x < 32) {
-      uint32_t l = 0, cnt = 0;
-      if (lane < (uint32_t)P) {
-        const uint32_t* row = v.wpr ? reinterpret_cast<const uint32_t*>(v.rank_base[lane / v.wpr] + v.tab_off) +
-                                          (size_t)lane * (nseg + 1)
-                                    : seg_off + (size_t)lane * (nseg + 1);
-        l = row[seg];
-        cnt = row[seg + 1] - l;
-      }
-      uint32_t incl = cnt;
+  // warp 0, lanes < P: worker lane's payload positions [l, l + cnt) in segment seg
+  auto fetch = [&](uint32_t seg, uint32_t& l, uint32_t& cnt) {
+    l = 0;
+    cnt = 0;
+    if (lane < (uint32_t)P) {
+      const uint32_t* row = v.wpr ? reinterpret_cast<const uint32_t*>(v.rank_base[lane / v.wpr] + v.tab_off) +
+                                        (size_t)lane * (nseg + 1)
+                                  : seg_off + (size_t)lane * (nseg + 1);
+      l = row[seg];
+      cnt = row[seg + 1] - l;
+    }
+  };
+  auto warp_incl = [&](uint32_t x) {
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= (uint32_t)o) incl += t;
-      }
-      if (lane < (uint32_t)P) {
-        lo[lane] = l;
-        vb[lane + 1] = incl;
-      }
-      if (lane == 0) vb[0] = 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += t;
     }
-    {
-      uint4* b4 = reinterpret_cast<uint4*>(bm);
-      for (uint32_t w = threadIdx.x; w < ((uint32_t)P * NW) >> 2; w += blockDim.x) b4[w] = make_uint4(0, 0, 0, 0);
+    return x;
+  };
+  // warp 0: descriptor of a segment into buffer b; under TMA also issue its
+  // bulk copies when the widened ranges fit the stage
+  auto describe = [&](int b, uint32_t l, uint32_t cnt) {
+    const uint32_t incl = warp_incl(cnt);
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    uint32_t bi = incl - cnt, bv = incl - cnt;  // non-TMA / unstaged: the flat entry index
+    bool fits = false;
+    uint32_t ai = 0, li = 0, av = 0, lv = 0, oi = 0, ov = 0, si = 0, sv = 0;
+    if (TMA && tot) {
+      const uint32_t EI = 16u / ib, EV = 16u / (uint32_t)sizeof(T);
+      ai = l & ~(EI - 1);
+      li = cnt ? ((l + cnt + EI - 1) & ~(EI - 1)) - ai : 0;
+      av = l & ~(EV - 1);
+      lv = cnt ? ((l + cnt + EV - 1) & ~(EV - 1)) - av : 0;
+      const uint32_t ii = warp_incl(li), iv = warp_incl(lv);
+      oi = ii - li;
+      ov = iv - lv;
+      si = __shfl_sync(0xffffffffu, ii, 31) * ib;
+      sv = __shfl_sync(0xffffffffu, iv, 31) * (uint32_t)sizeof(T);
+      fits = si <= ci_bytes && sv <= cv_bytes;
+      if (fits) {
+        bi = oi + (l - ai);
+        bv = ov + (l - av);
+      }
+    } else if (!TMA) {
+      fits = tot <= vcap;
     }
+    if (lane < (uint32_t)P) {
+      lo_s[b][lane] = l;
+      vb_s[b][lane + 1] = incl;
+      bi_s[b][lane] = bi;
+      bv_s[b][lane] = bv;
+    }
+    if (lane == 0) {
+      vb_s[b][0] = 0;
+      stg_s[b] = fits ? 1u : 0u;
+    }
+    if (TMA && fits) {
+      if (lane == 0) mbar_expect_tx(&mbar[b], si + sv);
+      __syncwarp();
+      if (cnt) {
+        unsigned char* st = stage0 + (size_t)b * (ci_bytes + cv_bytes);
+        const uint8_t* blk = pl_block(v, (int)lane);
+        tma_load_1d(st + (size_t)oi * ib, blk + (size_t)ai * ib, li * ib, &mbar[b]);
+        tma_load_1d(st + ci_bytes + (size_t)ov * sizeof(T), blk + v.val_off + (size_t)av * sizeof(T),
+                    lv * (uint32_t)sizeof(T), &mbar[b]);
+      }
+    }
+  };
+
+  uint32_t par = 0;        // TMA: mbarrier phase parity per buffer
+  uint32_t nl = 0, nc = 0;  // TMA, warp 0: offsets of the CTA's next segment
+  if (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&mbar[0], 1);
+      mbar_init(&mbar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    if (warp0 && blockIdx.x < nseg) {
+      uint32_t l, cnt;
+      fetch(blockIdx.x, l, cnt);
+      if (!(flag0 & 8u)) describe(0, l, cnt);
+      if (blockIdx.x + gridDim.x < nseg) fetch(blockIdx.x + gridDim.x, nl, nc);
+    }
+  }
+  {
+    uint4* b4 = reinterpret_cast<uint4*>(bm);
+    for (uint32_t w = threadIdx.x; w < ((uint32_t)P * NW) >> 2; w += blockDim.x) b4[w] = make_uint4(0, 0, 0, 0);
+  }
+  int b = 0;
+  for (uint32_t seg = blockIdx.x; seg < nseg; seg += gridDim.x, b = TMA ? b ^ 1 : 0) {
+    if (!TMA) {
+      __syncthreads();  // the previous segment is done with the descriptor
+      if (warp0) {
+        uint32_t l, cnt;
+        fetch(seg, l, cnt);
+        describe(0, l, cnt);
+      }
+    }
+    // the bitmaps are all-zero here: cleared before the loop, and phase 2
+    // re-zeroes the words it consumed
     __syncthreads();
     APPLY_MARK(0);
     if (flag0 & 8u) return;  // uniform across the CTA
+    const uint32_t* lo = lo_s[b];
+    const uint32_t* vb = vb_s[b];
     const uint32_t tot = vb[P];
-    if (!tot) continue;  // uniform across the CTA
-    const bool staged = tot <= vcap;
+    const bool staged = stg_s[b] != 0;
     const size_t seg_base = (size_t)(seg_lo + seg) << seg_shift;
-    uint32_t vbr[PT > 0 ? PT : 1];
-    if constexpr (PT > 0) {
-#pragma unroll
-      for (int p = 0; p < PT; ++p) vbr[p] = vb[p];
-    }
-    // worker owning flat entry e, and the flat index of that worker's first entry
-    auto worker_of = [&](uint32_t e, uint32_t& base) {
-      int q = 0;
-      base = 0;
+    unsigned char* st = stage0 + (TMA ? (size_t)b * (ci_bytes + cv_bytes) : 0);
+    const T* sval = reinterpret_cast<const T*>(st + (TMA ? ci_bytes : 0));
+    const uint32_t scap = TMA ? cv_bytes / (uint32_t)sizeof(T) : vcap;  // value slots of the stage
+    if (tot) {
+      uint32_t vbr[PT > 0 ? PT : 1];
       if constexpr (PT > 0) {
 #pragma unroll
-        for (int p = 1; p < PT; ++p)
-          if (e >= vbr[p]) {
-            q = p;
-            base = vbr[p];
-          }
-      } else {
-        for (int p = 1; p < P; ++p) q += e >= vb[p];
-        base = vb[q];
+        for (int p = 0; p < PT; ++p) vbr[p] = vb[p];
       }
-      return q;
-    };
-    // 1. presence bitmaps, word ranks, staging; a batch issues all its loads first
-    for (uint32_t e0 = threadIdx.x; e0 < tot; e0 += U1 * blockDim.x) {
-      uint32_t il[U1], ilp[U1];
-      T val[U1];
-      int qq[U1];
+      // worker owning flat entry e, and the flat index of that worker's first entry
+      auto worker_of = [&](uint32_t e, uint32_t& base) {
+        int q = 0;
+        base = 0;
+        if constexpr (PT > 0) {
 #pragma unroll
-      for (int u = 0; u < U1; ++u) {
-        const uint32_t e = e0 + u * blockDim.x;
-        qq[u] = -1;
-        if (e < tot) {
+          for (int p = 1; p < PT; ++p)
+            if (e >= vbr[p]) {
+              q = p;
+              base = vbr[p];
+            }
+        } else {
+          for (int p = 1; p < P; ++p) q += e >= vb[p];
+          base = vb[q];
+        }
+        return q;
+      };
+      auto mark = [&](int q, uint32_t il, uint32_t ilp, uint32_t r) {
+        const uint32_t w = il >> 5;
+        atomicOr(&bm[(size_t)q * NW + w], 1u << (il & 31));
+        if (ilp == 0xffffffffu || (ilp >> 5) != w) pre[(size_t)q * NW + w] = bv_s[b][q] + r;
+        // warm L2 with theta at this index: phase 2 reads it after the barrier
+#ifndef PSB_APPLY_NO_PF
+        if (theta) asm volatile("prefetch.global.L2 [%0];" ::"l"(theta + seg_base + il));
+#endif
+      };
+      // 1. presence bitmaps and word positions
+      if (TMA && staged) {
+        mbar_wait(&mbar[b], (par >> b) & 1u);
+        par ^= 1u << b;
+        for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x) {
           uint32_t base;
           const int q = worker_of(e, base);
-          const uint32_t rq = e - base;
-          const uint32_t j = lo[q] + rq;
-          qq[u] = q;
-          if (v.idx16) {  // wire16: the in-segment offset is stored directly
-            const uint16_t* lo16 = reinterpret_cast<const uint16_t*>(pl_block(v, q));
-            il[u] = lo16[j];
-            ilp[u] = rq ? (uint32_t)lo16[j - 1] : 0xffffffffu;
+          const uint32_t r = e - base, pos = bi_s[b][q] + r;
+          uint32_t il, ilp = 0xffffffffu;
+          if (v.idx16) {
+            const uint16_t* s16 = reinterpret_cast<const uint16_t*>(st);
+            il = s16[pos];
+            if (r) ilp = s16[pos - 1];
           } else {
-            const uint32_t* idx = pl_idx(v, q);
-            il[u] = (uint32_t)(idx[j] - seg_base);
-            ilp[u] = rq ? (uint32_t)(idx[j - 1] - seg_base) : 0xffffffffu;
+            const uint32_t* s32 = reinterpret_cast<const uint32_t*>(st);
+            il = s32[pos] - (uint32_t)seg_base;
+            if (r) ilp = s32[pos - 1] - (uint32_t)seg_base;
           }
-          if (staged) val[u] = pl_val<T>(v, q, j);
+          mark(q, il, ilp, r);
         }
-      }
+      } else {
+        // entries from global memory; a batch issues all its loads first
+        T* sv_w = reinterpret_cast<T*>(st);
+        for (uint32_t e0 = threadIdx.x; e0 < tot; e0 += U1 * blockDim.x) {
+          uint32_t il[U1], ilp[U1], rr[U1];
+          T val[U1];
+          int qq[U1];
 #pragma unroll
-      for (int u = 0; u < U1; ++u) {
-        if (qq[u] < 0) continue;
-        const uint32_t w = il[u] >> 5;
-        atomicOr(&bm[(size_t)qq[u] * NW + w], 1u << (il[u] & 31));
-        // the flat entry index of the word's first entry: vb[q] + rank
-        if (ilp[u] == 0xffffffffu || (ilp[u] >> 5) != w) pre[(size_t)qq[u] * NW + w] = e0 + u * blockDim.x;
-        if (staged) sval[e0 + u * blockDim.x] = val[u];
-        // warm L2 with theta at this index: phase 2 reads it after the barrier
-        if (theta) asm volatile("prefetch.global.L2 [%0];" ::"l"(theta + seg_base + il[u]));
+          for (int u = 0; u < U1; ++u) {
+            const uint32_t e = e0 + u * blockDim.x;
+            qq[u] = -1;
+            if (e < tot) {
+              uint32_t base;
+              const int q = worker_of(e, base);
+              const uint32_t rq = e - base;
+              const uint32_t j = lo[q] + rq;
+              qq[u] = q;
+              rr[u] = rq;
+              if (v.idx16) {  // wire16: the in-segment offset is stored directly
+                const uint16_t* lo16 = reinterpret_cast<const uint16_t*>(pl_block(v, q));
+                il[u] = lo16[j];
+                ilp[u] = rq ? (uint32_t)lo16[j - 1] : 0xffffffffu;
+              } else {
+                const uint32_t* idx = pl_idx(v, q);
+                il[u] = (uint32_t)(idx[j] - seg_base);
+                ilp[u] = rq ? (uint32_t)(idx[j - 1] - seg_base) : 0xffffffffu;
+              }
+              if (!TMA && staged) val[u] = pl_val<T>(v, q, j);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U1; ++u) {
+            if (qq[u] < 0) continue;
+            mark(qq[u], il[u], ilp[u], rr[u]);
+            if (!TMA && staged) sv_w[e0 + u * blockDim.x] = val[u];
+          }
+        }
       }
     }
     APPLY_MARK(1);
     __syncthreads();
+    // the CTA's next segment: descriptor and bulk copies into the other buffer
+    // (its previous user finished before this iteration's first barrier)
+    if (TMA && warp0 && seg + gridDim.x < nseg) {
+      describe(b ^ 1, nl, nc);
+      if (seg + 2 * gridDim.x < nseg) fetch(seg + 2 * gridDim.x, nl, nc);
+    }
+    if (!tot) continue;  // uniform across the CTA
     // 2. fold and update.  Each warp compacts the touched indices of 32
     //    bitmap words at a time into its shared list (word, bit order), then
     //    folds them lane-parallel: the lanes' work no longer follows the
     //    words' popcounts, and neighbouring lanes read neighbouring theta
-    //    sectors.  theta loads of up to U indices are issued together.
+    //    sectors.  theta loads of up to U indices are issued together; the
+    //    consumed bitmap words are re-zeroed for the next segment.
     for (uint32_t w0 = (threadIdx.x >> 5) << 5; w0 < NW; w0 += blockDim.x) {
       const uint32_t w = w0 + lane;  // NW is a multiple of 32 (S >= 2^10)
       uint32_t uni = 0;
       for (int q = 0; q < P; ++q) uni |= bm[(size_t)q * NW + w];
       const uint32_t c = __popc(uni);
-      uint32_t incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= (uint32_t)o) incl += t;
-      }
+      const uint32_t incl = warp_incl(c);
       const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      if (!total) continue;  // uniform across the warp
+      if (!total) continue;  // uniform across the warp (and the words are zero)
       uint16_t* wl = wlist[threadIdx.x >> 5];
       for (uint32_t off = incl - c; uni; uni &= uni - 1) wl[off++] = (uint16_t)((w << 5) | (__ffs(uni) - 1));
       uint32_t lbase = 0;
@@ -349,7 +481,7 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
           // clamped (unused) slot and contribute +0
           finish([&](int q2, uint32_t ww, uint32_t bit, uint32_t below) -> T {
             const uint32_t word = bm[(size_t)q2 * NW + ww];
-            const uint32_t at = min(pre[(size_t)q2 * NW + ww] + __popc(word & below), vcap - 1);
+            const uint32_t at = min(pre[(size_t)q2 * NW + ww] + __popc(word & below), scap - 1);
             const T x = sval[at];
             return (word & bit) ? x : T(0);
           });
@@ -362,6 +494,7 @@ __global__ void __launch_bounds__(apply_threads(PT), apply_minb(PT))
         }
       }
       __syncwarp();  // the list is rewritten by the warp's next chunk
+      for (int q = 0; q < P; ++q) bm[(size_t)q * NW + w] = 0u;
     }
     APPLY_MARK(2);
   }
@@ -496,33 +629,55 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
     tab = c->d_seg_off;
   }
   const uint32_t vcap = c->apply_vcap;
-  const size_t smem = (((size_t)P * 8) << (seg_shift - 5)) + (size_t)vcap * sizeof(T);
+  // TMA-staged entries: gathered / wire16 f32-f64 top-k payloads on 16-byte
+  // boundaries (q8 values and the direct view keep the thread-loaded path)
+  const bool tma = !c->apply_no_tma && !v.q8 && !v.wpr && ((uintptr_t)v.base & 15) == 0 &&
+                   (v.block_bytes & 15) == 0 && (v.val_off & 15) == 0;
+  const uint32_t ib = v.idx16 ? 2 : 4;
+  const uint32_t ci = (uint32_t)psb_align16(((size_t)vcap + 16 * (size_t)P) * ib);
+  const uint32_t cv = (uint32_t)psb_align16(((size_t)vcap + 8 * (size_t)P) * sizeof(T));
+  const size_t smem = (((size_t)P * 8) << (seg_shift - 5)) + (tma ? 2 * ((size_t)ci + cv) : (size_t)vcap * sizeof(T));
   WorkerCoefs ws{};
   if (async_mode)
     for (int q = 0; q < P; ++q) ws.v[q] = wscale_host[q];
-  // one CTA per segment: many segments in flight hide the dependent loads
-  const unsigned grid = (unsigned)std::min<size_t>(nseg, 1u << 20);
-  auto launch = [&](auto kern, T* mo) {
+  const int PTi = P == 2 || P == 4 || P == 8 ? P : 0;
+  auto launch = [&](auto kern, T* mo, bool is_tma) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, apply_threads(P == 2 || P == 4 || P == 8 ? P : 0), smem, st>>>(v, P, nseg, 0u, nullptr, seg_shift,
-                                                                               vcap, tab, (int)order, dpn, npr, coef, ws,
-                                  theta, n, mo, nullptr, nullptr, nullptr, c->d_flags);
+    const int thr = apply_threads(PTi, is_tma);
+    // TMA: persistent CTAs (the stage pipelines a CTA's consecutive
+    // segments); otherwise one CTA per segment, many in flight
+    unsigned grid = (unsigned)std::min<size_t>(nseg, 1u << 20);
+    if (is_tma) {
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, thr, smem);
+      grid = (unsigned)std::min<size_t>(nseg, (size_t)c->num_sms * (size_t)std::max(occ, 1));
+    }
+    kern<<<grid, thr, smem, st>>>(v, P, nseg, 0u, nullptr, seg_shift, vcap, ci, cv, tab, (int)order, dpn, npr, coef,
+                                  ws, theta, n, mo, nullptr, nullptr, nullptr, c->d_flags);
   };
-  if (async_mode) {
-    switch (P) {
-      case 2: launch(k_sparse_apply_bm<T, true, 2>, nullptr); break;
-      case 4: launch(k_sparse_apply_bm<T, true, 4>, nullptr); break;
-      case 8: launch(k_sparse_apply_bm<T, true, 8>, nullptr); break;
-      default: launch(k_sparse_apply_bm<T, true, 0>, nullptr);
-    }
-  } else {
-    switch (P) {
-      case 2: launch(k_sparse_apply_bm<T, false, 2>, mean_out); break;
-      case 4: launch(k_sparse_apply_bm<T, false, 4>, mean_out); break;
-      case 8: launch(k_sparse_apply_bm<T, false, 8>, mean_out); break;
-      default: launch(k_sparse_apply_bm<T, false, 0>, mean_out);
-    }
-  }
+#define PSB_APPLY_LAUNCH(ASY, MO)                                                                       \
+  do {                                                                                                  \
+    if (tma) {                                                                                          \
+      switch (P) {                                                                                      \
+        case 2: launch(k_sparse_apply_bm<T, ASY, 2, true>, MO, true); break;                            \
+        case 4: launch(k_sparse_apply_bm<T, ASY, 4, true>, MO, true); break;                            \
+        case 8: launch(k_sparse_apply_bm<T, ASY, 8, true>, MO, true); break;                            \
+        default: launch(k_sparse_apply_bm<T, ASY, 0, true>, MO, true);                                  \
+      }                                                                                                 \
+    } else {                                                                                            \
+      switch (P) {                                                                                      \
+        case 2: launch(k_sparse_apply_bm<T, ASY, 2, false>, MO, false); break;                          \
+        case 4: launch(k_sparse_apply_bm<T, ASY, 4, false>, MO, false); break;                          \
+        case 8: launch(k_sparse_apply_bm<T, ASY, 8, false>, MO, false); break;                          \
+        default: launch(k_sparse_apply_bm<T, ASY, 0, false>, MO, false);                                \
+      }                                                                                                 \
+    }                                                                                                   \
+  } while (0)
+  if (async_mode)
+    PSB_APPLY_LAUNCH(true, nullptr);
+  else
+    PSB_APPLY_LAUNCH(false, mean_out);
+#undef PSB_APPLY_LAUNCH
   c->launches += 1;
   PSB_LAUNCH_CHECK(c, "psb_sparse_mean_sgd");
   return PSB_OK;
@@ -564,22 +719,23 @@ psb_status shard_fold_impl(psb_ctx* c, int P, const uint32_t* sidx, const T* sva
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // persistent CTAs over the device-decided segment range
-    kern<<<c->num_sms * 4, apply_threads(P == 2 || P == 4 || P == 8 ? P : 0), smem, st>>>(v, P, 0u, 0u, range, seg_shift, vcap, srow, (int)order, dpn, npr, coef,
-                                            ws, theta, n, nullptr, list_idx, list_val, list_cnt, c->d_flags);
+    kern<<<c->num_sms * 4, apply_threads(P == 2 || P == 4 || P == 8 ? P : 0, false), smem, st>>>(
+        v, P, 0u, 0u, range, seg_shift, vcap, 0u, 0u, srow, (int)order, dpn, npr, coef, ws, theta, n, nullptr, list_idx,
+        list_val, list_cnt, c->d_flags);
   };
   if (async_mode) {
     switch (P) {
-      case 2: launch(k_sparse_apply_bm<T, true, 2>); break;
-      case 4: launch(k_sparse_apply_bm<T, true, 4>); break;
-      case 8: launch(k_sparse_apply_bm<T, true, 8>); break;
-      default: launch(k_sparse_apply_bm<T, true, 0>);
+      case 2: launch(k_sparse_apply_bm<T, true, 2, false>); break;
+      case 4: launch(k_sparse_apply_bm<T, true, 4, false>); break;
+      case 8: launch(k_sparse_apply_bm<T, true, 8, false>); break;
+      default: launch(k_sparse_apply_bm<T, true, 0, false>);
     }
   } else {
     switch (P) {
-      case 2: launch(k_sparse_apply_bm<T, false, 2>); break;
-      case 4: launch(k_sparse_apply_bm<T, false, 4>); break;
-      case 8: launch(k_sparse_apply_bm<T, false, 8>); break;
-      default: launch(k_sparse_apply_bm<T, false, 0>);
+      case 2: launch(k_sparse_apply_bm<T, false, 2, false>); break;
+      case 4: launch(k_sparse_apply_bm<T, false, 4, false>); break;
+      case 8: launch(k_sparse_apply_bm<T, false, 8, false>); break;
+      default: launch(k_sparse_apply_bm<T, false, 0, false>);
     }
   }
   c->launches += 1;

@@ -119,6 +119,7 @@ struct psb_ctx {
   int prof = 0;
   int predict = 1;  // K1 threshold prediction (PSB_NO_PREDICT=1 disables)
   uint32_t apply_vcap = 2048;  // PSB_APPLY_VCAP: staged entries per apply segment
+  bool apply_no_tma = false;   // PSB_APPLY_NO_TMA: thread-loaded apply entries (A/B)
   int q8_no_tma = 0;   // PSB_Q8_NO_TMA=1: register double-buffer kernel for the one-worker q8 step
   int q8_unfused = 0;  // PSB_Q8_UNFUSED=1: single-rank q8 step as quant + reduce (diagnostics)
   // NVLink peer exchange (psb_peer.cu)
@@ -309,6 +310,7 @@ static __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, u
 }
 
 static inline size_t psb_align16(size_t b) { return (b + 15) & ~(size_t)15; }
+static __device__ __forceinline__ size_t psb_align16_d(size_t b) { return (b + 15) & ~(size_t)15; }
 
 // Key of |x|: the magnitude bits, monotone in |x| for finite values and +-0
 // (SURVEY.md parity fact 1).
