@@ -142,6 +142,12 @@ __global__ void __launch_bounds__(256) k_seg_offsets(PayloadView v, int P, uint3
 // CTA shapes (measured on B200): non-TMA 256 threads x 4 CTAs/SM, and
 // 128 x 6 for P = 8 (more segments in flight; P = 8 324 -> 269 us); TMA
 // 256 x 3 (the double-buffered stage).
+// bitmap words per worker of psb_apply_seg_shift(P) (psb_internal.cuh)
+__host__ __device__ constexpr int apply_nw(int P) {
+  int sh = 15;
+  while (sh > 10 && ((long)P * 8) << (sh - 5) > PSB_APPLY_BM_BYTES) --sh;
+  return (1 << sh) >> 5;
+}
 #ifndef PSB_APPLY_TMA_MINB
 #define PSB_APPLY_TMA_MINB 3
 #endif
@@ -160,7 +166,9 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
   constexpr int U1 = PSB_APPLY_U1;  // entries per thread per batch (global entry loads)
   const int P = PT > 0 ? PT : P_rt;
   extern __shared__ __align__(16) unsigned char smem[];
-  const uint32_t NW = (1u << seg_shift) >> 5;  // bitmap words per worker
+  // bitmap words per worker (a compile-time constant for PT > 0, so every
+  // shared-memory lookup below has an immediate per-worker offset)
+  const uint32_t NW = PT > 0 ? (uint32_t)apply_nw(PT) : (1u << seg_shift) >> 5;
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem);  // [P][NW] presence bits
   uint32_t* pre = bm + (size_t)P * NW;                 // [P][NW] stage position of a word's first entry
   unsigned char* stage0 = reinterpret_cast<unsigned char*>(pre + (size_t)P * NW);
@@ -302,6 +310,23 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
     const uint32_t tot = vb[P];
     const bool staged = stg_s[b] != 0;
     const size_t seg_base = (size_t)(seg_lo + seg) << seg_shift;
+    // bitmap slot of worker q: (q - rot) mod P, so a fold over slots 0..P-1
+    // is the reference order when it is one rotation of the workers for the
+    // whole segment (naive: rot 0; ring: the segment lies in one ring chunk,
+    // rot = its start); otherwise (ring across a chunk boundary,
+    // multi-node hierarchical) slot = worker and the per-index order below
+    int rot = 0;
+    bool plain = ASYNC || order == PSB_ORDER_NAIVE || (order == PSB_ORDER_HIER && dpn >= (uint32_t)P);
+    if (!ASYNC && order == PSB_ORDER_RING) {
+      const size_t last = min(seg_base + ((size_t)1 << seg_shift), n) - 1;
+      const int r0 = rc.start_for(seg_base, n, P);
+      if (rc.lo <= seg_base && last < rc.hi) {
+        rot = r0;
+        plain = true;
+      }
+    }
+    auto slot_of = [&](int q) { return q - rot + (q < rot ? P : 0); };
+    auto worker_at = [&](int sl) { return sl + rot - (sl + rot >= P ? P : 0); };
     unsigned char* st = stage0 + (TMA ? (size_t)b * (ci_bytes + cv_bytes) : 0);
     const T* sval = reinterpret_cast<const T*>(st + (TMA ? ci_bytes : 0));
     const uint32_t scap = TMA ? cv_bytes / (uint32_t)sizeof(T) : vcap;  // value slots of the stage
@@ -330,8 +355,9 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
       };
       auto mark = [&](int q, uint32_t il, uint32_t ilp, uint32_t r) {
         const uint32_t w = il >> 5;
-        atomicOr(&bm[(size_t)q * NW + w], 1u << (il & 31));
-        if (ilp == 0xffffffffu || (ilp >> 5) != w) pre[(size_t)q * NW + w] = bv_s[b][q] + r;
+        const int sl = slot_of(q);
+        atomicOr(&bm[(size_t)sl * NW + w], 1u << (il & 31));
+        if (ilp == 0xffffffffu || (ilp >> 5) != w) pre[(size_t)sl * NW + w] = bv_s[b][q] + r;
         // warm L2 with theta at this index: phase 2 reads it after the barrier
 #ifndef PSB_APPLY_NO_PF
         if (theta) asm volatile("prefetch.global.L2 [%0];" ::"l"(theta + seg_base + il));
@@ -341,10 +367,8 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
       if (TMA && staged) {
         mbar_wait(&mbar[b], (par >> b) & 1u);
         par ^= 1u << b;
-        for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x) {
-          uint32_t base;
-          const int q = worker_of(e, base);
-          const uint32_t r = e - base, pos = bi_s[b][q] + r;
+        auto staged_entry = [&](int q, uint32_t r) {
+          const uint32_t pos = bi_s[b][q] + r;
           uint32_t il, ilp = 0xffffffffu;
           if (v.idx16) {
             const uint16_t* s16 = reinterpret_cast<const uint16_t*>(st);
@@ -356,6 +380,18 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
             if (r) ilp = s32[pos - 1] - (uint32_t)seg_base;
           }
           mark(q, il, ilp, r);
+        };
+        if constexpr (PT > 0 && (apply_threads(PT, TMA) / 32) % PT == 0) {
+          // warps own workers: warp w takes worker w % P, part w / P of its entries
+          const int wid = threadIdx.x >> 5, q = wid % PT, nparts = (int)(blockDim.x >> 5) / PT;
+          const uint32_t cq = vb[q + 1] - vb[q];
+          for (uint32_t r = (uint32_t)(wid / PT) * 32 + lane; r < cq; r += (uint32_t)nparts * 32) staged_entry(q, r);
+        } else {
+          for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x) {
+            uint32_t base;
+            const int q = worker_of(e, base);
+            staged_entry(q, e - base);
+          }
         }
       } else {
         // entries from global memory; a batch issues all its loads first
@@ -448,7 +484,7 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
             const size_t i = seg_base + li[u];
             auto g = [&](int q2) { return get(q2, ww, bit, below); };
             T t = th[u];
-            if (ASYNC) {
+            if (ASYNC) {  // slot = worker
               auto step = [&](int q2) {
                 const T x = add_rn(mul_rn(coefs[q2], g(q2)), t);
                 t = (bm[(size_t)q2 * NW + ww] & bit) ? x : t;
@@ -460,8 +496,20 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
                 for (int q2 = 0; q2 < P; ++q2) step(q2);
               }
             } else {
-              const int rs = order == PSB_ORDER_RING ? rc.start_for(i, n, P) : 0;
-              const T mean = mul_rn(fold_sum_start<T>(g, P, order, rs, dpn, npr), inv);
+              T sum;
+              if (plain) {  // the reference order is the slot order
+                sum = g(0);
+                if constexpr (PT > 0) {
+#pragma unroll
+                  for (int s2 = 1; s2 < PT; ++s2) sum = add_rn(sum, g(s2));
+                } else {
+                  for (int s2 = 1; s2 < P; ++s2) sum = add_rn(sum, g(s2));
+                }
+              } else {
+                const int rs = order == PSB_ORDER_RING ? rc.start_for(i, n, P) : 0;
+                sum = fold_sum_start<T>(g, P, order, rs, dpn, npr);
+              }
+              const T mean = mul_rn(sum, inv);
               t = add_rn(mul_rn(coef, mean), t);
               if (mean_out) mean_out[i] = mean;
             }
@@ -486,10 +534,11 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
             return (word & bit) ? x : T(0);
           });
         } else {
-          finish([&](int q2, uint32_t ww, uint32_t bit, uint32_t below) -> T {
+          finish([&](int q2, uint32_t ww, uint32_t bit, uint32_t below) -> T {  // q2: slot
             const uint32_t word = bm[(size_t)q2 * NW + ww];
             if (!(word & bit)) return T(0);
-            return pl_val<T>(v, q2, lo[q2] - vb[q2] + pre[(size_t)q2 * NW + ww] + __popc(word & below));
+            const int q = worker_at(q2);
+            return pl_val<T>(v, q, lo[q] - vb[q] + pre[(size_t)q2 * NW + ww] + __popc(word & below));
           });
         }
       }
