@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(256) k_seg_offsets(PayloadView v, int P, uint3
 #endif
 // CTA shapes (measured on B200): non-TMA 256 threads x 4 CTAs/SM, and
 // 128 x 6 for P = 8 (more segments in flight; P = 8 324 -> 269 us); TMA
-// 256 x 3 (the double-buffered stage).
+// 256 x 4 with a 1792-entry stage (P = 8 186 -> 170 us vs 3 CTAs/SM).
 // bitmap words per worker of psb_apply_seg_shift(P) (psb_internal.cuh)
 __host__ __device__ constexpr int apply_nw(int P) {
   int sh = 15;
@@ -149,7 +149,7 @@ __host__ __device__ constexpr int apply_nw(int P) {
   return (1 << sh) >> 5;
 }
 #ifndef PSB_APPLY_TMA_MINB
-#define PSB_APPLY_TMA_MINB 3
+#define PSB_APPLY_TMA_MINB 4
 #endif
 __host__ __device__ constexpr int apply_threads(int PT, bool TMA) { return TMA ? 256 : PT == 8 ? 128 : 256; }
 __host__ __device__ constexpr int apply_minb(int PT, bool TMA) { return TMA ? PSB_APPLY_TMA_MINB : PT == 8 ? 6 : 4; }
@@ -261,10 +261,9 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
       if (lane == 0) mbar_expect_tx(&mbar[b], si + sv);
       __syncwarp();
       if (cnt) {
-        unsigned char* st = stage0 + (size_t)b * (ci_bytes + cv_bytes);
         const uint8_t* blk = pl_block(v, (int)lane);
-        tma_load_1d(st + (size_t)oi * ib, blk + (size_t)ai * ib, li * ib, &mbar[b]);
-        tma_load_1d(st + ci_bytes + (size_t)ov * sizeof(T), blk + v.val_off + (size_t)av * sizeof(T),
+        tma_load_1d(stage0 + (size_t)oi * ib, blk + (size_t)ai * ib, li * ib, &mbar[b]);
+        tma_load_1d(stage0 + ci_bytes + (size_t)b * cv_bytes + (size_t)ov * sizeof(T), blk + v.val_off + (size_t)av * sizeof(T),
                     lv * (uint32_t)sizeof(T), &mbar[b]);
       }
     }
@@ -327,8 +326,10 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
     }
     auto slot_of = [&](int q) { return q - rot + (q < rot ? P : 0); };
     auto worker_at = [&](int sl) { return sl + rot - (sl + rot >= P ? P : 0); };
-    unsigned char* st = stage0 + (TMA ? (size_t)b * (ci_bytes + cv_bytes) : 0);
-    const T* sval = reinterpret_cast<const T*>(st + (TMA ? ci_bytes : 0));
+    // TMA: one index stage (read by phase 1 only, so the next segment's
+    // copies may overwrite it once phase 1 is done) and two value stages
+    unsigned char* st = stage0;
+    const T* sval = reinterpret_cast<const T*>(st + (TMA ? ci_bytes + (size_t)b * cv_bytes : 0));
     const uint32_t scap = TMA ? cv_bytes / (uint32_t)sizeof(T) : vcap;  // value slots of the stage
     if (tot) {
       uint32_t vbr[PT > 0 ? PT : 1];
@@ -683,9 +684,10 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
   const bool tma = !c->apply_no_tma && !v.q8 && !v.wpr && ((uintptr_t)v.base & 15) == 0 &&
                    (v.block_bytes & 15) == 0 && (v.val_off & 15) == 0;
   const uint32_t ib = v.idx16 ? 2 : 4;
-  const uint32_t ci = (uint32_t)psb_align16(((size_t)vcap + 16 * (size_t)P) * ib);
-  const uint32_t cv = (uint32_t)psb_align16(((size_t)vcap + 8 * (size_t)P) * sizeof(T));
-  const size_t smem = (((size_t)P * 8) << (seg_shift - 5)) + (tma ? 2 * ((size_t)ci + cv) : (size_t)vcap * sizeof(T));
+  const size_t tcap = c->apply_tma_cap;  // entries per TMA stage (+ the 16-byte widening)
+  const uint32_t ci = (uint32_t)psb_align16((tcap + 16 * (size_t)P) * ib);
+  const uint32_t cv = (uint32_t)psb_align16((tcap + 8 * (size_t)P) * sizeof(T));
+  const size_t smem = (((size_t)P * 8) << (seg_shift - 5)) + (tma ? (size_t)ci + 2 * (size_t)cv : (size_t)vcap * sizeof(T));
   WorkerCoefs ws{};
   if (async_mode)
     for (int q = 0; q < P; ++q) ws.v[q] = wscale_host[q];

@@ -90,6 +90,8 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   if (const char* qt = getenv("PSB_Q8_NO_TMA")) c->q8_no_tma = qt[0] != '0';
   if (const char* qu = getenv("PSB_Q8_UNFUSED")) c->q8_unfused = qu[0] != '0';
   if (const char* nt = getenv("PSB_APPLY_NO_TMA")) c->apply_no_tma = nt[0] != '0';
+  if (const char* tc = getenv("PSB_APPLY_TMA_CAP"))
+    c->apply_tma_cap = (uint32_t)std::min(8192l, std::max(64l, atol(tc)));
   if (const char* vc = getenv("PSB_APPLY_VCAP")) c->apply_vcap = (uint32_t)std::min(16384l, std::max(0l, atol(vc))) & ~1u;
   auto fail = [&](cudaError_t e) {
     psb_ctx_destroy(c);

@@ -120,6 +120,9 @@ struct psb_ctx {
   int predict = 1;  // K1 threshold prediction (PSB_NO_PREDICT=1 disables)
   uint32_t apply_vcap = 2048;  // PSB_APPLY_VCAP: staged entries per apply segment
   bool apply_no_tma = false;   // PSB_APPLY_NO_TMA: thread-loaded apply entries (A/B)
+  // PSB_APPLY_TMA_CAP: entries per TMA stage; 1792 fits a cfg2 segment (at
+  // most 1759 entries at P = 2..8) and 4 CTAs per SM
+  uint32_t apply_tma_cap = 1792;
   int q8_no_tma = 0;   // PSB_Q8_NO_TMA=1: register double-buffer kernel for the one-worker q8 step
   int q8_unfused = 0;  // PSB_Q8_UNFUSED=1: single-rank q8 step as quant + reduce (diagnostics)
   // NVLink peer exchange (psb_peer.cu)
