@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
   // segment descriptors, double-buffered under TMA: first payload position,
   // flat entry bases, stage positions of each worker's first index / value
   __shared__ uint32_t lo_s[2][PSB_MAX_P], vb_s[2][PSB_MAX_P + 1], bi_s[2][PSB_MAX_P], bv_s[2][PSB_MAX_P];
-  __shared__ uint32_t stg_s[2];
+  __shared__ uint32_t stg_s[2], rot_s[2];
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ T coefs[PSB_MAX_P];
   __shared__ uint16_t wlist[apply_threads(PT, TMA) / 32][1024];  // per-warp touched-index list
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
   };
   // warp 0: descriptor of a segment into buffer b; under TMA also issue its
   // bulk copies when the widened ranges fit the stage
-  auto describe = [&](int b, uint32_t l, uint32_t cnt) {
+  auto describe = [&](int b, uint32_t seg, uint32_t l, uint32_t cnt) {
     const uint32_t incl = warp_incl(cnt);
     const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
     uint32_t bi = incl - cnt, bv = incl - cnt;  // non-TMA / unstaged: the flat entry index
@@ -256,6 +256,15 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
     if (lane == 0) {
       vb_s[b][0] = 0;
       stg_s[b] = fits ? 1u : 0u;
+      // bitmap slot rotation (phase 2): one ring chunk for the whole segment?
+      uint32_t rs = 0;
+      if (!ASYNC && order == PSB_ORDER_RING) {
+        const size_t b0 = (size_t)(seg_lo + seg) << seg_shift;
+        const size_t last = min(b0 + ((size_t)1 << seg_shift), n) - 1;
+        const int r0 = rc.start_for(b0, n, P);
+        rs = (rc.lo <= b0 && last < rc.hi) ? (uint32_t)r0 : 0x80000000u;  // high bit: per-index order
+      }
+      rot_s[b] = rs;
     }
     if (TMA && fits) {
       if (lane == 0) mbar_expect_tx(&mbar[b], si + sv);
@@ -281,7 +290,7 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
     if (warp0 && blockIdx.x < nseg) {
       uint32_t l, cnt;
       fetch(blockIdx.x, l, cnt);
-      if (!(flag0 & 8u)) describe(0, l, cnt);
+      if (!(flag0 & 8u)) describe(0, blockIdx.x, l, cnt);
       if (blockIdx.x + gridDim.x < nseg) fetch(blockIdx.x + gridDim.x, nl, nc);
     }
   }
@@ -296,7 +305,7 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
       if (warp0) {
         uint32_t l, cnt;
         fetch(seg, l, cnt);
-        describe(0, l, cnt);
+        describe(0, seg, l, cnt);
       }
     }
     // the bitmaps are all-zero here: cleared before the loop, and phase 2
@@ -314,16 +323,10 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
     // whole segment (naive: rot 0; ring: the segment lies in one ring chunk,
     // rot = its start); otherwise (ring across a chunk boundary,
     // multi-node hierarchical) slot = worker and the per-index order below
-    int rot = 0;
-    bool plain = ASYNC || order == PSB_ORDER_NAIVE || (order == PSB_ORDER_HIER && dpn >= (uint32_t)P);
-    if (!ASYNC && order == PSB_ORDER_RING) {
-      const size_t last = min(seg_base + ((size_t)1 << seg_shift), n) - 1;
-      const int r0 = rc.start_for(seg_base, n, P);
-      if (rc.lo <= seg_base && last < rc.hi) {
-        rot = r0;
-        plain = true;
-      }
-    }
+    const uint32_t rsv = rot_s[b];
+    const int rot = (int)(rsv & 0x7fffffffu);
+    const bool plain = ASYNC || order == PSB_ORDER_NAIVE || (order == PSB_ORDER_HIER && dpn >= (uint32_t)P) ||
+                       (order == PSB_ORDER_RING && !(rsv >> 31));
     auto slot_of = [&](int q) { return q - rot + (q < rot ? P : 0); };
     auto worker_at = [&](int sl) { return sl + rot - (sl + rot >= P ? P : 0); };
     // TMA: one index stage (read by phase 1 only, so the next segment's
@@ -438,7 +441,7 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
     // the CTA's next segment: descriptor and bulk copies into the other buffer
     // (its previous user finished before this iteration's first barrier)
     if (TMA && warp0 && seg + gridDim.x < nseg) {
-      describe(b ^ 1, nl, nc);
+      describe(b ^ 1, seg + gridDim.x, nl, nc);
       if (seg + 2 * gridDim.x < nseg) fetch(seg + 2 * gridDim.x, nl, nc);
     }
     if (!tot) continue;  // uniform across the CTA
