@@ -257,6 +257,17 @@ def ours(args, cfg, world, rank, local_rank):
         if world > 1:
             dist.barrier()
 
+    align = torch.zeros(1, device=dev)
+
+    def align_start():
+        # device-side rendezvous on the timing stream right before the start
+        # event: the host barrier leaves ranks launching up to ~1.6 ms apart
+        # (measured at N = 4), and a rank that starts early would time its
+        # wait for the late one at the first exchange
+        if world > 1:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(align)
+
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
             step(i)
@@ -288,6 +299,7 @@ def ours(args, cfg, world, rank, local_rank):
         barrier()
         torch.cuda.synchronize(dev)
         with ClockSampler(local_rank) as clk:
+            align_start()
             e0.record(stream)
             if graph is not None:
                 graph.replay()
@@ -326,6 +338,10 @@ def ours(args, cfg, world, rank, local_rank):
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step, k1_avg_ms, ex_step_ms, ap_step_ms = (float(x) for x in t)
+        by_rank = torch.zeros(world, device=dev, dtype=torch.float64)  # each rank's own step time
+        by_rank[rank] = ms_local
+        if world > 1:
+            dist.all_reduce(by_rank)
 
         # ---- e2e through the public API: pinned host gradient in, theta out
         host_g = [torch.empty(W, n, pin_memory=True) for _ in range(2)]
@@ -348,6 +364,7 @@ def ours(args, cfg, world, rank, local_rank):
         barrier()
         torch.cuda.synchronize(dev)
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        align_start()
         f0.record(stream)
         s_in.wait_stream(stream)
         for i in range(e_steps):
@@ -474,6 +491,7 @@ def ours(args, cfg, world, rank, local_rank):
                                 "frac": bw / 900.0, "what": how}
         if ap_step_ms > 0:
             line["apply_ms_per_step"] = ap_step_ms
+        line["ms_per_step_by_rank"] = [round(float(x), 4) for x in by_rank]
     if comp.startswith("topk"):
         st = ctx.topk_stats(0)
         line["config"]["k1_last_call"] = {kk: st[kk] for kk in ("candidates", "predicted_valid", "first_radix_level",
