@@ -1,2 +1,1 @@
-timeout 600 python -m pytest tests/test_apply_gpu.py -x -q 2>&1 | tail -2
-python tools/probe_apply.py ring; PROBE_P=8 python tools/probe_apply.py naive; PSB_APPLY_NO_TMA=1 PROBE_P=8 python tools/probe_apply.py ring
+for lib in libpsb.so libpsb_u1.so libpsb_u3.so; do echo "== $lib"; PSB_LIB=$lib PROBE_P=2,4,8 python tools/probe_apply.py ring; done
