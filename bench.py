@@ -468,8 +468,9 @@ def ours(args, cfg, world, rank, local_rank):
                 how = ("NVLink pulls: every remote worker's int8 codes of this rank's block shard, then every "
                        "rank's requantized shard (window: two flag rounds, both pulls and the shard reduce)")
         elif comp in ("topk", "topk_q8"):
-            if comp == "topk" and not os.environ.get("PSB_NO_WIRE16") and os.environ.get("PSB_PEER_MODE", "1") == "1" \
-                    and not os.environ.get("PSB_NO_PEER"):
+            pm = "0" if os.environ.get("PSB_NO_PEER") else os.environ.get("PSB_PEER_MODE", "5")
+            direct = comp == "topk" and pm in ("4", "5")
+            if comp == "topk" and not os.environ.get("PSB_NO_WIRE16") and pm in ("1", "4", "5"):
                 seg_shift = 15
                 while seg_shift > 10 and (P * 8) << (seg_shift - 5) > 16 * 1024:
                     seg_shift -= 1
@@ -479,8 +480,13 @@ def ours(args, cfg, world, rank, local_rank):
             else:
                 from paper_2506_17551_b200.engine import payload_bytes
                 blk = payload_bytes(comp_code, torch.float32, k)
-                how = ("NCCL all-gather of the payloads" if os.environ.get("PSB_NO_PEER") or
-                       os.environ.get("PSB_PEER_MODE", "1") == "0" else "NVLink pull of the payloads")
+                how = ("NCCL all-gather of the payloads" if pm == "0" else "NVLink pull of the payloads")
+            if direct:
+                # the exchange is fused into the apply: its TMA stage reads the
+                # peers' arenas in place, so the window is the apply
+                how = ("NVLink reads of the peers' wire16 payloads + offset rows, in place, by the TMA-staged "
+                       "apply (exchange fused into the fold; window = the apply kernel)")
+                ex_step_ms = ap_step_ms
             bytes_in = (P - W) * blk
         else:
             bytes_in, how = None, comp

@@ -139,21 +139,23 @@ PSB_API psb_status psb_allgather(psb_ctx* ctx, void* buf, size_t bytes_per_rank,
 /* Sparse exchange + apply of psb_sync_step / psb_async_round with nranks > 1,
  * over NVLink peer memory (CUDA IPC arenas, device-side sequence flags, set
  * up collectively on first use) unless mode 0:
- *   1 (default) pull: after K1 every rank copies the peers' payloads (and
- *     their producer-computed per-segment offset rows) into its arena, each
- *     CTA waiting only for its own peer, then applies all P payloads;
+ *   5 (default) auto: 4 for top-k f32/f64, 1 for top-k int8;
+ *   1 pull: after K1 every rank copies the peers' payloads (and their
+ *     producer-computed per-segment offset rows) into its arena, each CTA
+ *     waiting only for its own peer, then applies all P payloads;
  *   3 push: K1 stores each CTA's finished payload range straight into every
  *     peer's arena (top-k f32/f64; top-k int8 falls back to 1), then every
  *     rank applies all P payloads from its own arena;
  *   2 sharded: each rank pulls only the payload entries of its share of the
  *     index space (balanced on the device), folds them into theta and an
  *     update list, then applies the other ranks' lists;
- *   4 direct: no copy -- the apply reads every peer's payload and offset
- *     rows in place from its arena over NVLink (measured slower: the apply
- *     is latency-bound and remote loads lengthen its chains);
+ *   4 direct: no copy -- the apply reads every peer's wire16 payload and
+ *     offset rows in place from its arena over NVLink, its TMA stage
+ *     bringing the next segment's remote entries in while it folds the
+ *     current one (the fastest measured on B200 for top-k f32: DESIGN.md
+ *     section 4);
  *   0 NCCL all-gather of the payloads, then the full apply.
- * Results are bitwise identical in every mode (1 is the fastest measured on
- * B200: DESIGN.md section 4).  Environment at ctx creation: PSB_NO_PEER=1 -> 0,
+ * Results are bitwise identical in every mode.  Environment at ctx creation: PSB_NO_PEER=1 -> 0,
  * PSB_SHARD=1 -> 2, PSB_PEER_MODE=<n> -> n.  Steps with mean_out never shard. */
 PSB_API psb_status psb_peer_mode(psb_ctx* ctx, int mode);
 /* 1 once the peer arenas are mapped. */

@@ -682,9 +682,12 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
     tab = c->d_seg_off;
   }
   const uint32_t vcap = c->apply_vcap;
-  // TMA-staged entries: gathered / wire16 f32-f64 top-k payloads on 16-byte
-  // boundaries (q8 values and the direct view keep the thread-loaded path)
-  const bool tma = !c->apply_no_tma && !v.q8 && !v.wpr && ((uintptr_t)v.base & 15) == 0 &&
+  // TMA-staged entries: f32/f64 top-k payloads (gathered, wire16, or read in
+  // place from the peers' arenas) on 16-byte boundaries; q8 values keep the
+  // thread-loaded path
+  bool direct_ok = true;  // direct view: every rank's arena on 16-byte boundaries
+  for (int r = 0; v.wpr && r < (P + v.wpr - 1) / v.wpr; ++r) direct_ok &= ((uintptr_t)v.rank_base[r] & 15) == 0;
+  const bool tma = !c->apply_no_tma && !v.q8 && direct_ok && ((uintptr_t)v.base & 15) == 0 &&
                    (v.block_bytes & 15) == 0 && (v.val_off & 15) == 0;
   const uint32_t ib = v.idx16 ? 2 : 4;
   const size_t tcap = c->apply_tma_cap;  // entries per TMA stage (+ the 16-byte widening)
@@ -1025,13 +1028,19 @@ psb_status psb_sparse_apply_wire16(psb_ctx* c, psb_dtype dt, int P, const void* 
                             n, (float*)mean_out, st, tab, &v);
 }
 
-// Direct multi-rank apply: the P payloads and their offset rows are read in
-// place from every rank's NVLink-mapped arena (no pull copy).
+// Direct multi-rank apply: the P payloads (standard, or wire16 when
+// `wire16`) and their offset rows are read in place from every rank's
+// NVLink-mapped arena (no pull copy; the TMA stage brings them in).
 psb_status psb_sparse_apply_direct(psb_ctx* c, psb_compressor comp, psb_dtype dt, int P, int W,
                                    const uint8_t* const* rank_region, size_t k, size_t tab_off, psb_order order,
                                    const psb_topology* topo, double lr, const double* wscale, int async_mode,
-                                   void* theta, size_t n, void* mean_out, cudaStream_t st) {
+                                   void* theta, size_t n, void* mean_out, cudaStream_t st, bool wire16) {
   PayloadView v = make_view(comp, dt, rank_region[c->rank], k);
+  if (wire16) {
+    v.block_bytes = psb_wire16_bytes(dt, k);
+    v.val_off = psb_align16(2 * k);
+    v.idx16 = 1;
+  }
   v.wpr = W;
   v.tab_off = tab_off;
   for (int r = 0; r < c->nranks; ++r) v.rank_base[r] = rank_region[r];

@@ -79,12 +79,12 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   if (const char* np = getenv("PSB_NO_PEER")) c->peer_mode = np[0] == '0';
   if (const char* sh = getenv("PSB_SHARD")) c->shard_mode = sh[0] != '0';
   if (const char* nw = getenv("PSB_NO_WIRE16")) c->no_wire16 = nw[0] != '0';
-  if (const char* pm = getenv("PSB_PEER_MODE")) {  // 0 nccl, 1 pull, 2 shard, 3 push, 4 direct
+  if (const char* pm = getenv("PSB_PEER_MODE")) {  // 0 nccl, 1 pull, 2 shard, 3 push, 4 direct, 5 auto
     const int m = atoi(pm);
     c->peer_mode = m > 0;
     c->shard_mode = m == 2;
     c->push_mode = m == 3;
-    c->direct_mode = m == 4;
+    c->direct_mode = m == 4 ? 1 : m == 5 ? 2 : 0;
   }
   if (const char* sm = getenv("PSB_STEP_MARKS")) c->marks_on = sm[0] != '0';
   if (const char* qt = getenv("PSB_Q8_NO_TMA")) c->q8_no_tma = qt[0] != '0';
@@ -426,11 +426,15 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
   // full exchange pushed by K1 itself (top-k values; the q8 payload is finished after K1)
   const bool push = peer && !shard && c->push_mode && d->compressor == PSB_COMP_TOPK && plan != nullptr;
   // direct: the apply reads every peer's arena in place (no pull copy)
-  const bool direct = peer && !shard && !push && c->direct_mode && plan != nullptr && P >= 2;
-  // pull mode, top-k f32/f64: the arena slots carry wire16 payloads (u16
-  // in-segment index | value: 6 instead of 8 bytes per entry on NVLink);
-  // K1 writes the standard payload into local scratch and k_pack16 converts
-  const bool wire16 = peer && !shard && !push && !direct && plan != nullptr && P >= 2 &&
+  // (auto, the default: direct for top-k f32/f64, whose apply stages the
+  // remote entries by TMA; pull for top-k int8)
+  const bool direct = peer && !shard && !push && plan != nullptr && P >= 2 &&
+                      (c->direct_mode == 1 || (c->direct_mode == 2 && d->compressor == PSB_COMP_TOPK));
+  // pull / direct mode, top-k f32/f64: the arena slots carry wire16 payloads
+  // (u16 in-segment index | value: 6 instead of 8 bytes per entry on
+  // NVLink); K1 writes the standard payload into local scratch and k_pack16
+  // converts
+  const bool wire16 = peer && !shard && !push && plan != nullptr && P >= 2 &&
                       d->compressor == PSB_COMP_TOPK && !c->no_wire16;
   const size_t pblk = wire16 ? psb_wire16_bytes(d->dtype, d->k) : blk;  // arena slot stride
   psb_status s;
@@ -844,7 +848,7 @@ static psb_status sync_step_core(psb_ctx* c, const psb_step_desc* d, psb_stream_
         const uint8_t* regions[PSB_MAX_P];
         psb_peer_regions(c, regions);
         s = psb_sparse_apply_direct(c, d->compressor, d->dtype, P, d->workers, regions, d->k, sp.tab_off, d->order,
-                                    &d->topo, d->lr, nullptr, 0, d->theta, d->n, d->mean_out, st);
+                                    &d->topo, d->lr, nullptr, 0, d->theta, d->n, d->mean_out, st, sp.wire16);
       } else if (sp.wire16)
         s = psb_sparse_apply_wire16(c, d->dtype, P, pl, d->k, reinterpret_cast<const uint32_t*>(pl + sp.tab_off),
                                     d->order, &d->topo, d->lr, nullptr, 0, d->theta, d->n, d->mean_out, st);
@@ -1124,7 +1128,7 @@ extern "C" psb_status psb_async_round(psb_ctx* c, const psb_step_desc* d, uint32
     const uint8_t* regions[PSB_MAX_P];
     psb_peer_regions(c, regions);
     s = psb_sparse_apply_direct(c, d->compressor, d->dtype, P, d->workers, regions, d->k, sp.tab_off, PSB_ORDER_NAIVE,
-                                nullptr, 0.0, scale.data(), 1, d->theta, d->n, nullptr, st);
+                                nullptr, 0.0, scale.data(), 1, d->theta, d->n, nullptr, st, sp.wire16);
     if (!s) s = psb_peer_ack(c, st);
   } else if (sp.wire16) {
     s = psb_sparse_apply_wire16(c, d->dtype, P, pl, d->k, reinterpret_cast<const uint32_t*>(pl + sp.tab_off),

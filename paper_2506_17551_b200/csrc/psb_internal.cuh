@@ -132,7 +132,8 @@ struct psb_ctx {
   void* peer_base[PSB_MAX_P] = {};  // every rank's arena mapped here (own included)
   int shard_mode = 0;           // sharded multi-rank sparse apply (psb_peer_mode 2 / PSB_SHARD=1)
   int push_mode = 0;            // full exchange: K1 pushes its payload to the peers (psb_peer_mode 3)
-  int direct_mode = 0;          // the apply reads the peers' arenas in place (psb_peer_mode 4)
+  int direct_mode = 2;          // the apply reads the peers' arenas in place: 1 always (psb_peer_mode 4),
+                                // 2 auto for top-k f32/f64 (psb_peer_mode 5, the default)
   int no_wire16 = 0;            // PSB_NO_WIRE16=1: 32-bit indices on the NVLink exchange
   // set by the step driver around one worker's K1 call in push mode: the
   // peers' payload-region bases and this worker's slot offset in them
@@ -211,7 +212,7 @@ psb_status psb_sparse_apply_wire16(psb_ctx* c, psb_dtype dt, int P, const void* 
 psb_status psb_sparse_apply_direct(psb_ctx* c, psb_compressor comp, psb_dtype dt, int P, int W,
                                    const uint8_t* const* rank_region, size_t k, size_t tab_off, psb_order order,
                                    const psb_topology* topo, double lr, const double* wscale, int async_mode,
-                                   void* theta, size_t n, void* mean_out, cudaStream_t st);
+                                   void* theta, size_t n, void* mean_out, cudaStream_t st, bool wire16);
 psb_status psb_shard_fold(psb_ctx* c, psb_dtype dt, int P, const uint32_t* sidx, const void* sval,
                           const uint32_t* srow, const uint32_t* range, int seg_shift, psb_order order,
                           const psb_topology* topo, double lr, const double* wscale, int async_mode, void* theta,

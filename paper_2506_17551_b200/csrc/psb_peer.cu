@@ -648,11 +648,11 @@ psb_status psb_shard_finish(psb_ctx* c, psb_dtype dt, size_t list_off, size_t li
 
 extern "C" psb_status psb_peer_mode(psb_ctx* c, int mode) {
   PSB_REQUIRE(c, c != nullptr, "null ctx");
-  PSB_REQUIRE(c, mode >= 0 && mode <= 4, "psb_peer_mode: mode must be 0..4");
+  PSB_REQUIRE(c, mode >= 0 && mode <= 5, "psb_peer_mode: mode must be 0..5");
   c->peer_mode = mode > 0;
   c->shard_mode = mode == 2;
   c->push_mode = mode == 3;
-  c->direct_mode = mode == 4;
+  c->direct_mode = mode == 4 ? 1 : mode == 5 ? 2 : 0;
   return PSB_OK;
 }
 

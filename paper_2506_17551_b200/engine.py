@@ -155,10 +155,12 @@ class Context:
                  "psb_allgather")
 
     def peer_mode(self, mode) -> None:
-        """Multi-rank sparse exchange (psb_peer_mode): "pull" (1, default), "push"
-        (3: K1 stores its payload into the peers' NVLink arenas), "shard" (2),
-        "nccl" (0)."""
-        m = {"pull": 1, "full": 1, "push": 3, "shard": 2, "direct": 4, "nccl": 0, True: 1, False: 0}.get(mode, mode)
+        """Multi-rank sparse exchange (psb_peer_mode): "auto" (5, default: direct
+        for top-k f32/f64, pull for top-k int8), "direct" (4: the apply reads
+        the peers' NVLink arenas in place), "pull" (1), "push" (3: K1 stores
+        its payload into the peers' arenas), "shard" (2), "nccl" (0)."""
+        m = {"auto": 5, "full": 5, "pull": 1, "push": 3, "shard": 2, "direct": 4, "nccl": 0, True: 5,
+             False: 0}.get(mode, mode)
         self._ck(self.lib.psb_peer_mode(self.h, int(m)), "psb_peer_mode")
 
     @property

@@ -141,7 +141,8 @@ def test_payload_exchange_modes(comp, order, W, peer, steps):
 
 
 def _worker_full_size(rank, nranks, uid, comp, q):
-    """Bench size (cfg2: 125M, top-k 1% + EF, pull/wire16 exchange; cfg3:
+    """Bench size (cfg2: 125M, top-k 1% + EF, default exchange: the apply
+    reads the peers' wire16 arenas in place; cfg3:
     125M dense q8, NCCL all-to-all + all-gather): the multi-rank step must
     equal, bit for bit, the same P workers run as virtual workers on one GPU
     -- a path the oracle pins at small sizes (test_apply_gpu.py)."""
