@@ -440,3 +440,43 @@ def test_async_pipeline_graph_capture(cuda):
         c.close()
     assert torch.equal(out[0][0].view(torch.int32), out[1][0].view(torch.int32))
     assert torch.equal(out[0][1].view(torch.int32), out[1][1].view(torch.int32))
+
+
+@pytest.mark.parametrize("env", [{"PSB_APPLY_TMA_CAP": "64"}, {"PSB_APPLY_TMA_CAP": "600"},
+                                 {"PSB_APPLY_NO_TMA": "1"}, {"PSB_APPLY_NO_TMA": "1", "PSB_APPLY_VCAP": "256"}])
+@pytest.mark.parametrize("P,order", [(2, "ring"), (4, "naive"), (8, "ring"), (5, "hierarchical")])
+def test_sparse_apply_stage_paths(cuda, env, P, order):
+    """The TMA-staged apply with segments that do not fit its stage (a tiny
+    stage: every or some segment takes the thread-loaded path inside the
+    persistent kernel), and the one-CTA-per-segment kernel (q8 / sharded
+    views) staged and unstaged: all bit-exact with the oracle fold.  Ring
+    segments straddle the P ring chunks (n not a multiple of S)."""
+    import os
+    from paper_2506_17551_b200.engine import Context
+    dt = np.float32
+    n, k = 70_001, 2_500
+    idx, val = make_payloads(P, n, k, dt, seed=P * 13 + len(env))
+    theta_h = O.generate("uniform", 9, 0, 0, n).astype(dt)
+    dense = np.zeros((P, n), dtype=dt)
+    for p in range(P):
+        dense[p, idx[p].astype(np.int64)] = val[p]
+    dpn, npr = (2, 2) if order == "hierarchical" else (0, 1)
+    mean_h = O.fold_mean(dense, order, dpn, npr)
+    want = theta_h.copy()
+    O.axpy_(-0.05, mean_h, want)
+    old = {kk: os.environ.get(kk) for kk in env}
+    os.environ.update(env)
+    try:
+        c = Context(n, k, P)
+    finally:
+        for kk, vv in old.items():
+            if vv is None:
+                os.environ.pop(kk, None)
+            else:
+                os.environ[kk] = vv
+    theta = torch.from_numpy(theta_h.copy()).cuda()
+    topo = topology(1, npr, dpn) if dpn else None
+    c.sparse_mean_sgd(pack_payloads(idx, val, torch.float32), P, k, torch.float32, order, 0.05, theta, n, None, topo)
+    c.check()
+    c.close()
+    assert np.array_equal(bits(tnp(theta)), bits(want))
