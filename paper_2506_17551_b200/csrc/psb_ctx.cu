@@ -89,6 +89,7 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   if (const char* sm = getenv("PSB_STEP_MARKS")) c->marks_on = sm[0] != '0';
   if (const char* qt = getenv("PSB_Q8_NO_TMA")) c->q8_no_tma = qt[0] != '0';
   if (const char* qu = getenv("PSB_Q8_UNFUSED")) c->q8_unfused = qu[0] != '0';
+  if (const char* qd = getenv("PSB_Q8_DIRECT_APPLY")) c->q8_direct_apply = qd[0] != '0';
   if (const char* nt = getenv("PSB_APPLY_NO_TMA")) c->apply_no_tma = nt[0] != '0';
   if (const char* tc = getenv("PSB_APPLY_TMA_CAP"))
     c->apply_tma_cap = (uint32_t)std::min(8192l, std::max(64l, atol(tc)));
@@ -692,26 +693,43 @@ static psb_status q8_step_nvlink(psb_ctx* c, const psb_step_desc* d, cudaStream_
   if (!s) s = psb_peer_wait_ready(c, st);
   if (s) return s;
   psb_mark(c, st);
-  PeerSegs sm{};
-  for (int q = 0; q < R; ++q) {
-    if (q == c->rank || hi_of(q) <= lo_of(q)) continue;
-    sm.s[sm.n++] = {q, o_mc + lo_of(q) * B, o_mc + lo_of(q) * B, (hi_of(q) - lo_of(q)) * B};
-    sm.s[sm.n++] = {q, o_ms + sizeof(float) * lo_of(q), o_ms + sizeof(float) * lo_of(q),
-                    sizeof(float) * (hi_of(q) - lo_of(q))};
-  }
-  s = psb_peer_gather(c, sm, st);
-  if (!s) s = psb_peer_ack(c, st);  // done reading the peers' arenas for this step
-  if (s) return s;
-  psb_mark(c, st);
-  psb_prof_mark(c, 1, st);
   Q8Shards ms{};
-  ms.codes[0] = reinterpret_cast<const int8_t*>(own + o_mc);
-  ms.scales[0] = reinterpret_cast<const float*>(own + o_ms);
-  ms.nbs = (size_t)-1;
+  int ms_r = 1;
+  if (c->q8_direct_apply) {
+    // the apply reads every other rank's requantized shard in place over
+    // NVLink (no pull of the mean), acknowledging once it is done
+    const uint8_t* regions[PSB_MAX_P];
+    psb_peer_regions(c, regions);
+    for (int q = 0; q < R; ++q) {
+      ms.codes[q] = reinterpret_cast<const int8_t*>(regions[q] + o_mc);
+      ms.scales[q] = reinterpret_cast<const float*>(regions[q] + o_ms);
+    }
+    ms.nbs = nbs;
+    ms_r = R;
+    psb_mark(c, st);
+    psb_prof_mark(c, 1, st);
+  } else {
+    PeerSegs sm{};
+    for (int q = 0; q < R; ++q) {
+      if (q == c->rank || hi_of(q) <= lo_of(q)) continue;
+      sm.s[sm.n++] = {q, o_mc + lo_of(q) * B, o_mc + lo_of(q) * B, (hi_of(q) - lo_of(q)) * B};
+      sm.s[sm.n++] = {q, o_ms + sizeof(float) * lo_of(q), o_ms + sizeof(float) * lo_of(q),
+                      sizeof(float) * (hi_of(q) - lo_of(q))};
+    }
+    s = psb_peer_gather(c, sm, st);
+    if (!s) s = psb_peer_ack(c, st);  // done reading the peers' arenas for this step
+    if (s) return s;
+    psb_mark(c, st);
+    psb_prof_mark(c, 1, st);
+    ms.codes[0] = reinterpret_cast<const int8_t*>(own + o_mc);
+    ms.scales[0] = reinterpret_cast<const float*>(own + o_ms);
+    ms.nbs = (size_t)-1;
+  }
   psb_prof_mark(c, 2, st);
-  s = psb_q8_apply_launch(c, ms, 1, n, B, d->lr, reinterpret_cast<float*>(d->theta),
+  s = psb_q8_apply_launch(c, ms, ms_r, n, B, d->lr, reinterpret_cast<float*>(d->theta),
                           reinterpret_cast<float*>(d->mean_out), st);
   psb_prof_mark(c, 2, st);
+  if (!s && c->q8_direct_apply) s = psb_peer_ack(c, st);
   psb_mark(c, st);
   return s;
 }

@@ -620,23 +620,44 @@ __global__ void __launch_bounds__(256) k_q8_apply(Q8Shards ms, int R, size_t n,
   uintptr_t al = (uintptr_t)theta;
   for (int q = 0; q < R; ++q) al |= (uintptr_t)ms.codes[q];
   const bool vec_ok = (al & 15) == 0 && !mean_out;
-  auto owner = [&](size_t e) { return R == 1 ? 0 : (int)((e / B) / ms.nbs); };
+  const int lb = 31 - __clz((int)B);  // B is a power of two (128..1024): no 64-bit divisions
+  const uint32_t nbs32 = (uint32_t)(ms.nbs < 0xffffffffu ? ms.nbs : 0xffffffffu);
+  auto owner = [&](size_t e) { return R == 1 ? 0 : (int)((uint32_t)(e >> lb) / nbs32); };
   auto code_at = [&](size_t e) { return ms.codes[owner(e)][e]; };
-  auto scale_at = [&](size_t e) { return ms.scales[owner(e)][e / B]; };
+  auto scale_at = [&](size_t e) { return ms.scales[owner(e)][e >> lb]; };
   if (vec_ok) {
-    for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv;
-         v += (size_t)gridDim.x * blockDim.x) {
-      const size_t e = v * 4;
-      const int o = owner(e);
-      const char4 cv = *reinterpret_cast<const char4*>(ms.codes[o] + e);
-      const float sc = ms.scales[o][e / B];
-      float4 th = __ldcs(reinterpret_cast<const float4*>(theta + e));
-      th.x = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.x, sc)), th.x);
-      th.y = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.y, sc)), th.y);
-      th.z = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.z, sc)), th.z);
-      th.w = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.w, sc)), th.w);
-      __stcs(reinterpret_cast<float4*>(theta + e), th);
-      bad |= !is_finite(th.x) || !is_finite(th.y) || !is_finite(th.z) || !is_finite(th.w);
+    // U float4 groups per thread per iteration, every load issued before any
+    // use (U x 20 B in flight per thread; coalesced: group u of the warp is
+    // 32 consecutive float4)
+    constexpr int U = 4;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t v0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v0 < nv; v0 += U * stride) {
+      char4 cv[U];
+      float sc[U];
+      float4 th[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t v = v0 + u * stride;
+        if (v < nv) {
+          const size_t e = v * 4;
+          const int o = owner(e);
+          cv[u] = *reinterpret_cast<const char4*>(ms.codes[o] + e);
+          sc[u] = ms.scales[o][e >> lb];
+          th[u] = __ldcs(reinterpret_cast<const float4*>(theta + e));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t v = v0 + u * stride;
+        if (v >= nv) continue;
+        float4 t = th[u];
+        t.x = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv[u].x, sc[u])), t.x);
+        t.y = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv[u].y, sc[u])), t.y);
+        t.z = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv[u].z, sc[u])), t.z);
+        t.w = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv[u].w, sc[u])), t.w);
+        __stcs(reinterpret_cast<float4*>(theta + v * 4), t);
+        bad |= !is_finite(t.x) || !is_finite(t.y) || !is_finite(t.z) || !is_finite(t.w);
+      }
     }
     for (size_t e = nv * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
          e += (size_t)gridDim.x * blockDim.x) {
@@ -753,7 +774,7 @@ psb_status psb_q8_step1_launch(psb_ctx* c, const float* g, size_t gstride, float
 psb_status psb_q8_apply_launch(psb_ctx* c, const Q8Shards& ms, int R, size_t n,
                                uint32_t B, double lr, float* theta, float* mean_out,
                                cudaStream_t st) {
-  const unsigned grid = (unsigned)std::min<size_t>((n / 4 + 255) / 256 + 1, (size_t)c->num_sms * 16);
+  const unsigned grid = (unsigned)std::min<size_t>((n / 4 + 255) / 256 + 1, (size_t)c->num_sms * 8);
   k_q8_apply<<<grid, 256, 0, st>>>(ms, R, n, B, (float)(-lr), theta, mean_out, c->d_flags);
   c->launches += 1;
   PSB_LAUNCH_CHECK(c, "q8 apply");
