@@ -89,6 +89,7 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   if (const char* sm = getenv("PSB_STEP_MARKS")) c->marks_on = sm[0] != '0';
   if (const char* qt = getenv("PSB_Q8_NO_TMA")) c->q8_no_tma = qt[0] != '0';
   if (const char* qu = getenv("PSB_Q8_UNFUSED")) c->q8_unfused = qu[0] != '0';
+  if (const char* qp = getenv("PSB_Q8_NO_PIPE")) c->q8_no_pipe = qp[0] != '0';
   if (const char* qd = getenv("PSB_Q8_DIRECT_APPLY")) c->q8_direct_apply = qd[0] != '0';
   if (const char* nt = getenv("PSB_APPLY_NO_TMA")) c->apply_no_tma = nt[0] != '0';
   if (const char* tc = getenv("PSB_APPLY_TMA_CAP"))

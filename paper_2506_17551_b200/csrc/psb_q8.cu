@@ -308,6 +308,78 @@ __global__ void __launch_bounds__(256) k_q8_reduce(
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1u);
 }
 
+// k_q8_reduce for the multi-rank path's common case (compile-time P, the
+// plain worker-order fold -- naive, or hierarchical within one node -- full
+// blocks, no theta): each warp holds the codes and scales of its NEXT block in
+// registers while it folds the current one, so a block's loads overlap the
+// previous block's fold / requantize instead of exposing DRAM latency per
+// block.  Same per-element operations as k_q8_reduce.
+template <int VPL, int PT>
+__global__ void __launch_bounds__(256) k_q8_reduce_pipe(Q8Workers wv, size_t blk_lo, size_t blk_hi,
+                                                        int8_t* __restrict__ mcodes, float* __restrict__ mscales) {
+  constexpr int B = VPL * 128;
+  const int lane = threadIdx.x & 31;
+  const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  const size_t e_base = blk_lo * B;
+  const float inv = (float)(1.0 / (double)PT);
+  char4 cc[PT][VPL], cn[PT][VPL];
+  float sc[PT], sn[PT];
+  auto load = [&](size_t blk, char4 (&c)[PT][VPL], float (&sv)[PT]) {
+#pragma unroll
+    for (int q = 0; q < PT; ++q) {
+#pragma unroll
+      for (int it = 0; it < VPL; ++it)
+        c[q][it] = *reinterpret_cast<const char4*>(wv.codes[q] + (blk * B - e_base) + (size_t)it * 128 + lane * 4);
+      sv[q] = wv.scales[q][blk - blk_lo];
+    }
+  };
+  size_t blk = blk_lo + warp;
+  if (blk < blk_hi) load(blk, cc, sc);
+  for (; blk < blk_hi; blk += nwarps) {
+    const size_t nxt = blk + nwarps;
+    if (nxt < blk_hi) load(nxt, cn, sn);
+    float m[VPL][4];
+    float amax = 0.f;
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+      float4 acc = make_float4(__fmul_rn((float)cc[0][it].x, sc[0]), __fmul_rn((float)cc[0][it].y, sc[0]),
+                               __fmul_rn((float)cc[0][it].z, sc[0]), __fmul_rn((float)cc[0][it].w, sc[0]));
+#pragma unroll
+      for (int q = 1; q < PT; ++q) {
+        acc.x = __fadd_rn(acc.x, __fmul_rn((float)cc[q][it].x, sc[q]));
+        acc.y = __fadd_rn(acc.y, __fmul_rn((float)cc[q][it].y, sc[q]));
+        acc.z = __fadd_rn(acc.z, __fmul_rn((float)cc[q][it].z, sc[q]));
+        acc.w = __fadd_rn(acc.w, __fmul_rn((float)cc[q][it].w, sc[q]));
+      }
+      m[it][0] = __fmul_rn(acc.x, inv);
+      m[it][1] = __fmul_rn(acc.y, inv);
+      m[it][2] = __fmul_rn(acc.z, inv);
+      m[it][3] = __fmul_rn(acc.w, inv);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) amax = fmaxf(amax, fabsf(m[it][c]));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const float scale = __fdiv_rn(amax, 127.0f);
+    const float rinv = __frcp_rn(scale);
+    if (lane == 0) mscales[blk] = scale;
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+      const size_t e0 = blk * B + (size_t)it * 128 + lane * 4;
+      *reinterpret_cast<char4*>(mcodes + e0) =
+          make_char4((signed char)q8_code(m[it][0], scale, rinv), (signed char)q8_code(m[it][1], scale, rinv),
+                     (signed char)q8_code(m[it][2], scale, rinv), (signed char)q8_code(m[it][3], scale, rinv));
+    }
+#pragma unroll
+    for (int q = 0; q < PT; ++q) {
+      sc[q] = sn[q];
+#pragma unroll
+      for (int it = 0; it < VPL; ++it) cc[q][it] = cn[q][it];
+    }
+  }
+}
+
 // Single-rank fused step (R == 1): per block of B elements, each local worker
 // q's p = r + g is quantized (codes stay in registers), r' = p - xhat written,
 // and xhat = code*scale folded in the reference order; the mean is requantized
@@ -701,6 +773,41 @@ psb_status psb_q8_reduce_launch(psb_ctx* c, const Q8Workers& wv, int P, size_t b
                                 uint32_t npr, int8_t* mcodes, float* mscales, double lr,
                                 float* theta, float* mean_out, cudaStream_t st) {
   if (blk_hi <= blk_lo) return PSB_OK;
+  // common multi-rank case: the pipelined kernel over the full blocks, the
+  // generic one for a ragged last block
+  uintptr_t al = (uintptr_t)mcodes;
+  for (int q = 0; q < P; ++q) al |= (uintptr_t)wv.codes[q];
+  const bool plain = order == PSB_ORDER_NAIVE || (order == PSB_ORDER_HIER && dpn >= (uint32_t)P);
+  if (!c->q8_no_pipe && plain && !theta && !mean_out && (al & 15) == 0 && (P == 2 || P == 4 || P == 8)) {
+    const size_t full_hi = std::min(blk_hi, n / B);
+    if (full_hi > blk_lo) {
+      const size_t nbf = full_hi - blk_lo;
+      const unsigned g2 = (unsigned)std::max<size_t>(1, std::min<size_t>((nbf + 7) / 8, (size_t)c->num_sms * 8));
+      // register budget: the double buffer holds P * B / 128 char4 per lane
+      const int vpl = (int)(B / 128);
+#define PSB_REDP(V, PP) k_q8_reduce_pipe<V, PP><<<g2, 256, 0, st>>>(wv, blk_lo, full_hi, mcodes, mscales)
+      if (P == 2 && vpl == 1) PSB_REDP(1, 2);
+      else if (P == 2 && vpl == 2) PSB_REDP(2, 2);
+      else if (P == 2 && vpl == 4) PSB_REDP(4, 2);
+      else if (P == 4 && vpl == 1) PSB_REDP(1, 4);
+      else if (P == 4 && vpl == 2) PSB_REDP(2, 4);
+      else if (P == 8 && vpl == 1) PSB_REDP(1, 8);
+      else goto generic;
+#undef PSB_REDP
+      c->launches += 1;
+      PSB_LAUNCH_CHECK(c, "q8 reduce");
+      if (full_hi == blk_hi) return PSB_OK;
+      // the ragged last block: the workers' pointers rebased to it
+      Q8Workers wt = wv;
+      for (int q = 0; q < P; ++q) {
+        wt.codes[q] += (full_hi - blk_lo) * B;
+        wt.scales[q] += full_hi - blk_lo;
+      }
+      return psb_q8_reduce_launch(c, wt, P, full_hi, blk_hi, n, B, order, dpn, npr, mcodes, mscales, lr, theta,
+                                  mean_out, st);
+    }
+  }
+generic:
   const size_t nb = blk_hi - blk_lo;
   const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((nb + 7) / 8, (size_t)c->num_sms * 8));
   const float coef = (float)(-lr);
