@@ -682,6 +682,117 @@ __global__ void __launch_bounds__(256) k_q8_step1_tma(const float* __restrict__ 
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1u);
 }
 
+// The quantizer of the multi-rank path (EF on: x and r streamed) with the
+// same TMA ring as k_q8_step1_tma: one elected thread streams tiles of 8
+// blocks of x and r into kQ8Stages shared-memory stages; each warp quantizes
+// one block (same per-element operations as k_q8_quant) and stores its codes,
+// scale and residual.
+template <int VPL>
+__global__ void __launch_bounds__(256) k_q8_quant_tma(const float* __restrict__ x, float* __restrict__ r, size_t n,
+                                                      int8_t* __restrict__ codes, float* __restrict__ scales,
+                                                      uint32_t* flags) {
+  constexpr int B = VPL * 128;
+  constexpr int TE = 8 * B;
+  constexpr uint32_t kArr = TE * 4;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* sx = reinterpret_cast<float*>(smem);  // [stage][TE]
+  float* sr = sx + (size_t)kQ8Stages * TE;
+  __shared__ __align__(8) uint64_t full[kQ8Stages];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t ntiles_full = n / TE;
+  const size_t my_tiles = ntiles_full > blockIdx.x ? (ntiles_full - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kQ8Stages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](size_t i) {
+    const int s = (int)(i % kQ8Stages);
+    const size_t base = (blockIdx.x + i * gridDim.x) * (size_t)TE;
+    mbar_expect_tx(&full[s], 2 * kArr);
+    tma_load_1d(sx + (size_t)s * TE, x + base, kArr, &full[s]);
+    tma_load_1d(sr + (size_t)s * TE, r + base, kArr, &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (size_t i = 0; i < my_tiles && i < (size_t)kQ8Stages; ++i) issue(i);
+  bool bad = false;
+  auto process = [&](const float* px, const float* pr, size_t lo, bool from_smem) {
+    float p[VPL][4];
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+      const int o = it * 128 + lane * 4;
+      float4 xv, rv;
+      if (from_smem) {
+        xv = *reinterpret_cast<const float4*>(px + o);
+        rv = *reinterpret_cast<const float4*>(pr + o);
+      } else {
+        xv = make_float4(0.f, 0.f, 0.f, 0.f);
+        rv = xv;
+        float* xp = &xv.x;
+        float* rp = &rv.x;
+        for (int c = 0; c < 4; ++c)
+          if (lo + o + c < n) {
+            xp[c] = px[o + c];
+            rp[c] = pr[o + c];
+          }
+      }
+      p[it][0] = __fadd_rn(rv.x, xv.x);
+      p[it][1] = __fadd_rn(rv.y, xv.y);
+      p[it][2] = __fadd_rn(rv.z, xv.z);
+      p[it][3] = __fadd_rn(rv.w, xv.w);
+    }
+    float amax = 0.f;
+#pragma unroll
+    for (int it = 0; it < VPL; ++it)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        amax = fmaxf(amax, fabsf(p[it][c]));
+        bad |= !is_finite(p[it][c]);
+      }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const float scale = __fdiv_rn(amax, 127.0f);
+    const float inv = __frcp_rn(scale);
+    if (lane == 0) scales[lo / B] = scale;
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+      const size_t e = lo + (size_t)it * 128 + lane * 4;
+      int q[4];
+      float res[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        q[c] = q8_code(p[it][c], scale, inv);
+        res[c] = __fsub_rn(p[it][c], __fmul_rn((float)q[c], scale));
+      }
+      if (from_smem) {
+        *reinterpret_cast<char4*>(codes + e) =
+            make_char4((signed char)q[0], (signed char)q[1], (signed char)q[2], (signed char)q[3]);
+        __stcs(reinterpret_cast<float4*>(r + e), make_float4(res[0], res[1], res[2], res[3]));
+      } else {
+        for (int c = 0; c < 4; ++c)
+          if (e + c < n) {
+            codes[e + c] = (int8_t)q[c];
+            r[e + c] = res[c];
+          }
+      }
+    }
+  };
+  for (size_t i = 0; i < my_tiles; ++i) {
+    const int s = (int)(i % kQ8Stages);
+    mbar_wait(&full[s], (uint32_t)((i / kQ8Stages) & 1));
+    const size_t base = (blockIdx.x + i * gridDim.x) * (size_t)TE;
+    const size_t off = (size_t)s * TE + (size_t)wid * B;
+    process(sx + off, sr + off, base + (size_t)wid * B, true);
+    __syncthreads();  // every warp is done with stage s
+    if (threadIdx.x == 0 && i + kQ8Stages < my_tiles) issue(i + kQ8Stages);
+  }
+  if (blockIdx.x == 0) {  // ragged tail: CTA 0, one block per warp
+    for (size_t lo = ntiles_full * TE + (size_t)wid * B; lo < n; lo += 8 * (size_t)B)
+      process(x + lo, r + lo, lo, false);
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1u);
+}
+
 // theta += (-lr) * mean, the mean read shard by shard from the rank that
 // reduced it (Q8Shards: local buffer, or the peers' NVLink-mapped arenas).
 __global__ void __launch_bounds__(256) k_q8_apply(Q8Shards ms, int R, size_t n,
@@ -755,6 +866,25 @@ __global__ void __launch_bounds__(256) k_q8_apply(Q8Shards ms, int R, size_t n,
 psb_status psb_q8_quant_launch(psb_ctx* c, const float* x, float* r, size_t n, uint32_t B,
                                int8_t* codes, float* scales, cudaStream_t st) {
   const size_t nb = (n + B - 1) / B;
+  if (r != nullptr && !c->q8_no_tma && ((((uintptr_t)x) | ((uintptr_t)r) | ((uintptr_t)codes)) & 15) == 0 &&
+      (B == 128 || B == 256 || B == 512)) {  // B = 1024: the register-pipelined kernel below
+    const size_t smem = (size_t)kQ8Stages * 2 * 8 * B * sizeof(float);
+    const unsigned tgrid = (unsigned)std::max<size_t>(1, std::min<size_t>((n / (8 * B)) + 1, (size_t)c->num_sms * 2));
+#define PSB_QT(V)                                                                                           \
+  do {                                                                                                      \
+    cudaFuncSetAttribute(k_q8_quant_tma<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+    k_q8_quant_tma<V><<<tgrid, 256, smem, st>>>(x, r, n, codes, scales, c->d_flags);                        \
+  } while (0)
+    switch (B) {
+      case 128: PSB_QT(1); break;
+      case 256: PSB_QT(2); break;
+      default: PSB_QT(4); break;
+    }
+#undef PSB_QT
+    c->launches += 1;
+    PSB_LAUNCH_CHECK(c, "psb_q8_quantize");
+    return PSB_OK;
+  }
   const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((nb + 7) / 8, (size_t)c->num_sms * 8));
   switch (B) {
     case 128: k_q8_quant<1><<<grid, 256, 0, st>>>(x, r, n, codes, scales, c->d_flags); break;
@@ -836,7 +966,7 @@ psb_status psb_q8_step1_launch(psb_ctx* c, const float* g, size_t gstride, float
   const float coef = (float)(-lr);
   if (c->prof) cudaEventRecord(psb_prof_event(c), st);
   const bool hier = order == PSB_ORDER_HIER && dpn < (uint32_t)P;
-  const bool tma = P == 1 && r != nullptr && !c->q8_no_tma &&
+  const bool tma = P == 1 && r != nullptr && !c->q8_no_tma && B <= 512 &&  // B = 1024 tiles exceed smem
                    ((((uintptr_t)g) | ((uintptr_t)r) | ((uintptr_t)theta) | ((uintptr_t)mean_out)) & 15) == 0;
   if (tma) {
     const size_t smem = (size_t)kQ8Stages * 3 * 8 * B * sizeof(float);
@@ -850,8 +980,7 @@ psb_status psb_q8_step1_launch(psb_ctx* c, const float* g, size_t gstride, float
       case 128: PSB_T1(1); break;
       case 256: PSB_T1(2); break;
       case 512: PSB_T1(4); break;
-      case 1024: return psb_set_err(c, PSB_EINVAL, "q8: B=1024 tiles exceed shared memory");
-      default: return psb_set_err(c, PSB_EINVAL, "q8: block must be 128, 256, 512 or 1024");
+      default: return psb_set_err(c, PSB_EINVAL, "q8: block must be 128, 256 or 512 here");
     }
 #undef PSB_T1
     if (c->prof) cudaEventRecord(psb_prof_event(c), st);

@@ -480,3 +480,24 @@ def test_sparse_apply_stage_paths(cuda, env, P, order):
     c.check()
     c.close()
     assert np.array_equal(bits(tnp(theta)), bits(want))
+
+
+@pytest.mark.parametrize("block", [128, 512, 1024])
+@pytest.mark.parametrize("W", [1, 2])
+def test_q8_step_block_sizes(ctx, block, W):
+    """Dense q8 sync step for every block size (the TMA-staged kernels serve
+    B <= 512, the register-pipelined ones B = 1024), n not a multiple of the
+    8-block tile, no mean_out: bit-exact with the oracle composite."""
+    n, lr = 300_007, 0.05
+    theta_h = np.zeros(n, dtype=np.float32)
+    res_h = np.zeros((W, n), dtype=np.float32)
+    theta = torch.zeros(n, device="cuda")
+    res = torch.zeros(W, n, device="cuda")
+    for step in range(3):
+        g_h = np.stack([O.generate("llmrec", 7, w, step, n) for w in range(W)])
+        d = ctx.step_desc(COMPS["q8"], torch.from_numpy(g_h).cuda(), res, theta, lr, 0, "naive", block)
+        ctx.sync_step(d)
+        ctx.check()
+        O.sync_step(g_h, theta_h, lr, "q8", 0, "naive", res_h, 0, 1, block)
+        assert np.array_equal(bits(tnp(theta)), bits(theta_h)), step
+        assert np.array_equal(bits(tnp(res)), bits(res_h)), step
