@@ -25,6 +25,8 @@ psb_status psb_q8_reduce_launch(psb_ctx* c, const Q8Workers& wv, int P, size_t b
 psb_status psb_q8_step1_launch(psb_ctx* c, const float* g, size_t gstride, float* r, size_t rstride,
                                int P, size_t n, uint32_t B, psb_order order, uint32_t dpn, uint32_t npr,
                                double lr, float* theta, float* mean_out, cudaStream_t st);
+psb_status psb_q8_apply_tma_launch(psb_ctx* c, const Q8Shards& ms, const float* scales, size_t n, uint32_t B,
+                                   double lr, float* theta, cudaStream_t st);
 psb_status psb_q8_apply_launch(psb_ctx* c, const Q8Shards& ms, int R, size_t n, uint32_t B, double lr,
                                float* theta, float* mean_out, cudaStream_t st);
 
@@ -696,6 +698,33 @@ static psb_status q8_step_nvlink(psb_ctx* c, const psb_step_desc* d, cudaStream_
   psb_mark(c, st);
   Q8Shards ms{};
   int ms_r = 1;
+  const bool tma_apply = !c->q8_no_tma && B <= 512 && d->theta != nullptr && d->mean_out == nullptr &&
+                         ((uintptr_t)d->theta & 15) == 0;
+  if (tma_apply) {
+    // gather only the other ranks' mean scales (4 B per block); the TMA apply
+    // streams theta and reads every shard's mean codes in place over NVLink
+    PeerSegs sm{};
+    for (int q = 0; q < R; ++q) {
+      if (q == c->rank || hi_of(q) <= lo_of(q)) continue;
+      sm.s[sm.n++] = {q, o_ms + sizeof(float) * lo_of(q), o_ms + sizeof(float) * lo_of(q),
+                      sizeof(float) * (hi_of(q) - lo_of(q))};
+    }
+    s = psb_peer_gather(c, sm, st);
+    if (s) return s;
+    const uint8_t* regions[PSB_MAX_P];
+    psb_peer_regions(c, regions);
+    for (int q = 0; q < R; ++q) ms.codes[q] = reinterpret_cast<const int8_t*>(regions[q] + o_mc);
+    ms.nbs = nbs;
+    psb_mark(c, st);
+    psb_prof_mark(c, 1, st);
+    psb_prof_mark(c, 2, st);
+    s = psb_q8_apply_tma_launch(c, ms, reinterpret_cast<const float*>(own + o_ms), n, B, d->lr,
+                                reinterpret_cast<float*>(d->theta), st);
+    psb_prof_mark(c, 2, st);
+    if (!s) s = psb_peer_ack(c, st);  // done reading the peers' arenas for this step
+    psb_mark(c, st);
+    return s;
+  }
   if (c->q8_direct_apply) {
     // the apply reads every other rank's requantized shard in place over
     // NVLink (no pull of the mean), acknowledging once it is done

@@ -861,6 +861,82 @@ __global__ void __launch_bounds__(256) k_q8_apply(Q8Shards ms, int R, size_t n,
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
 }
 
+// theta += (-lr) * mean over TMA-staged tiles: one elected thread streams
+// tiles of 8 blocks of theta (local) and of the requantized mean codes --
+// read in place from the rank that reduced each block's shard, over NVLink
+// for the other ranks (1-D bulk copies from the mapped arenas, split at shard
+// boundaries) -- into a ring of kQ8Stages stages; each warp applies one block.
+// The scales are local (gathered beforehand, 4 B per block).  Replaces the
+// pull of the mean shards + k_q8_apply: the remote code reads overlap the
+// theta stream.
+template <int VPL>
+__global__ void __launch_bounds__(256) k_q8_apply_tma(Q8Shards ms, const float* __restrict__ scales, size_t n,
+                                                      float coef, float* __restrict__ theta, uint32_t* flags) {
+  constexpr int B = VPL * 128;
+  constexpr int TE = 8 * B;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* sth = reinterpret_cast<float*>(smem);                                        // [stage][TE]
+  int8_t* scd = reinterpret_cast<int8_t*>(smem + (size_t)kQ8Stages * TE * sizeof(float));  // [stage][TE]
+  __shared__ __align__(8) uint64_t full[kQ8Stages];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t ntiles_full = n / TE;
+  const size_t my_tiles = ntiles_full > blockIdx.x ? (ntiles_full - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const size_t nbs = ms.nbs;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kQ8Stages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](size_t i) {
+    const int s = (int)(i % kQ8Stages);
+    const size_t base = (blockIdx.x + i * gridDim.x) * (size_t)TE;
+    mbar_expect_tx(&full[s], TE * 4 + TE);
+    tma_load_1d(sth + (size_t)s * TE, theta + base, TE * 4, &full[s]);
+    size_t cur = base / B;
+    const size_t end = cur + 8;
+    while (cur < end) {  // the tile's codes, one bulk copy per owning rank
+      const size_t o = cur / nbs;
+      const size_t stop = min(end, (o + 1) * nbs);
+      tma_load_1d(scd + (size_t)s * TE + (cur * B - base), ms.codes[o] + cur * B, (uint32_t)((stop - cur) * B),
+                  &full[s]);
+      cur = stop;
+    }
+  };
+  if (threadIdx.x == 0)
+    for (size_t i = 0; i < my_tiles && i < (size_t)kQ8Stages; ++i) issue(i);
+  bool bad = false;
+  for (size_t i = 0; i < my_tiles; ++i) {
+    const int s = (int)(i % kQ8Stages);
+    const size_t base = (blockIdx.x + i * gridDim.x) * (size_t)TE;
+    const size_t blk = base / B + wid;
+    const float sc = scales[blk];  // issued before the wait
+    mbar_wait(&full[s], (uint32_t)((i / kQ8Stages) & 1));
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+      const int o = wid * B + it * 128 + lane * 4;
+      const char4 cv = *reinterpret_cast<const char4*>(scd + (size_t)s * TE + o);
+      float4 th = *reinterpret_cast<const float4*>(sth + (size_t)s * TE + o);
+      th.x = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.x, sc)), th.x);
+      th.y = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.y, sc)), th.y);
+      th.z = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.z, sc)), th.z);
+      th.w = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)cv.w, sc)), th.w);
+      __stcs(reinterpret_cast<float4*>(theta + base + o), th);
+      bad |= !is_finite(th.x) || !is_finite(th.y) || !is_finite(th.z) || !is_finite(th.w);
+    }
+    __syncthreads();  // every warp is done with stage s
+    if (threadIdx.x == 0 && i + kQ8Stages < my_tiles) issue(i + kQ8Stages);
+  }
+  if (blockIdx.x == 0) {  // ragged tail (elements past the last full tile): CTA 0, direct loads
+    for (size_t e = ntiles_full * TE + threadIdx.x; e < n; e += blockDim.x) {
+      const size_t blk = e / B;
+      const float th = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)ms.codes[blk / nbs][e], scales[blk])), theta[e]);
+      theta[e] = th;
+      bad |= !is_finite(th);
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1u);
+}
+
 }  // namespace
 
 psb_status psb_q8_quant_launch(psb_ctx* c, const float* x, float* r, size_t n, uint32_t B,
@@ -1004,6 +1080,27 @@ psb_status psb_q8_step1_launch(psb_ctx* c, const float* g, size_t gstride, float
   if (c->prof) cudaEventRecord(psb_prof_event(c), st);
   c->launches += 1;
   PSB_LAUNCH_CHECK(c, "q8 fused step");
+  return PSB_OK;
+}
+
+psb_status psb_q8_apply_tma_launch(psb_ctx* c, const Q8Shards& ms, const float* scales, size_t n, uint32_t B,
+                                   double lr, float* theta, cudaStream_t st) {
+  const size_t smem = (size_t)kQ8Stages * 8 * B * 5;
+  const unsigned tgrid = (unsigned)std::max<size_t>(1, std::min<size_t>((n / (8 * B)) + 1, (size_t)c->num_sms * 4));
+#define PSB_QA(V)                                                                                           \
+  do {                                                                                                      \
+    cudaFuncSetAttribute(k_q8_apply_tma<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+    k_q8_apply_tma<V><<<tgrid, 256, smem, st>>>(ms, scales, n, (float)(-lr), theta, c->d_flags);            \
+  } while (0)
+  switch (B) {
+    case 128: PSB_QA(1); break;
+    case 256: PSB_QA(2); break;
+    case 512: PSB_QA(4); break;
+    default: return psb_set_err(c, PSB_EINVAL, "q8 TMA apply: block must be 128, 256 or 512");
+  }
+#undef PSB_QA
+  c->launches += 1;
+  PSB_LAUNCH_CHECK(c, "q8 apply");
   return PSB_OK;
 }
 
