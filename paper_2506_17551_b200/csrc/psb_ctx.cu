@@ -92,6 +92,7 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   if (const char* qt = getenv("PSB_Q8_NO_TMA")) c->q8_no_tma = qt[0] != '0';
   if (const char* qu = getenv("PSB_Q8_UNFUSED")) c->q8_unfused = qu[0] != '0';
   if (const char* qp = getenv("PSB_Q8_NO_PIPE")) c->q8_no_pipe = qp[0] != '0';
+  if (const char* qs = getenv("PSB_Q8_SCALES_INPLACE")) c->q8_scales_inplace = qs[0] != '0';
   if (const char* qd = getenv("PSB_Q8_DIRECT_APPLY")) c->q8_direct_apply = qd[0] != '0';
   if (const char* nt = getenv("PSB_APPLY_NO_TMA")) c->apply_no_tma = nt[0] != '0';
   if (const char* tc = getenv("PSB_APPLY_TMA_CAP"))
@@ -703,23 +704,29 @@ static psb_status q8_step_nvlink(psb_ctx* c, const psb_step_desc* d, cudaStream_
   if (tma_apply) {
     // gather only the other ranks' mean scales (4 B per block); the TMA apply
     // streams theta and reads every shard's mean codes in place over NVLink
-    PeerSegs sm{};
-    for (int q = 0; q < R; ++q) {
-      if (q == c->rank || hi_of(q) <= lo_of(q)) continue;
-      sm.s[sm.n++] = {q, o_ms + sizeof(float) * lo_of(q), o_ms + sizeof(float) * lo_of(q),
-                      sizeof(float) * (hi_of(q) - lo_of(q))};
+    const float* lscales = nullptr;  // nullptr: the scales are read in place too
+    if (!c->q8_scales_inplace) {
+      PeerSegs sm{};
+      for (int q = 0; q < R; ++q) {
+        if (q == c->rank || hi_of(q) <= lo_of(q)) continue;
+        sm.s[sm.n++] = {q, o_ms + sizeof(float) * lo_of(q), o_ms + sizeof(float) * lo_of(q),
+                        sizeof(float) * (hi_of(q) - lo_of(q))};
+      }
+      s = psb_peer_gather(c, sm, st);
+      if (s) return s;
+      lscales = reinterpret_cast<const float*>(own + o_ms);
     }
-    s = psb_peer_gather(c, sm, st);
-    if (s) return s;
     const uint8_t* regions[PSB_MAX_P];
     psb_peer_regions(c, regions);
-    for (int q = 0; q < R; ++q) ms.codes[q] = reinterpret_cast<const int8_t*>(regions[q] + o_mc);
+    for (int q = 0; q < R; ++q) {
+      ms.codes[q] = reinterpret_cast<const int8_t*>(regions[q] + o_mc);
+      ms.scales[q] = reinterpret_cast<const float*>(regions[q] + o_ms);
+    }
     ms.nbs = nbs;
     psb_mark(c, st);
     psb_prof_mark(c, 1, st);
     psb_prof_mark(c, 2, st);
-    s = psb_q8_apply_tma_launch(c, ms, reinterpret_cast<const float*>(own + o_ms), n, B, d->lr,
-                                reinterpret_cast<float*>(d->theta), st);
+    s = psb_q8_apply_tma_launch(c, ms, lscales, n, B, d->lr, reinterpret_cast<float*>(d->theta), st);
     psb_prof_mark(c, 2, st);
     if (!s) s = psb_peer_ack(c, st);  // done reading the peers' arenas for this step
     psb_mark(c, st);

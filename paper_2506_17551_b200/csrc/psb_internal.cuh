@@ -120,6 +120,7 @@ struct psb_ctx {
   int predict = 1;  // K1 threshold prediction (PSB_NO_PREDICT=1 disables)
   uint32_t apply_vcap = 2048;  // PSB_APPLY_VCAP: staged entries per apply segment
   bool q8_no_pipe = false;       // PSB_Q8_NO_PIPE: the generic q8 reduce only (A/B)
+  bool q8_scales_inplace = false;  // PSB_Q8_SCALES_INPLACE: the TMA apply reads remote mean scales in place
   bool q8_direct_apply = false;  // PSB_Q8_DIRECT_APPLY: the q8 apply reads the peers' mean shards in place
   bool apply_no_tma = false;   // PSB_APPLY_NO_TMA: thread-loaded apply entries (A/B)
   // PSB_APPLY_TMA_CAP: entries per TMA stage; 1792 fits a cfg2 segment (at

@@ -909,7 +909,7 @@ __global__ void __launch_bounds__(256) k_q8_apply_tma(Q8Shards ms, const float* 
     const int s = (int)(i % kQ8Stages);
     const size_t base = (blockIdx.x + i * gridDim.x) * (size_t)TE;
     const size_t blk = base / B + wid;
-    const float sc = scales[blk];  // issued before the wait
+    const float sc = scales ? scales[blk] : ms.scales[blk / nbs][blk];  // issued before the wait
     mbar_wait(&full[s], (uint32_t)((i / kQ8Stages) & 1));
 #pragma unroll
     for (int it = 0; it < VPL; ++it) {
@@ -929,7 +929,8 @@ __global__ void __launch_bounds__(256) k_q8_apply_tma(Q8Shards ms, const float* 
   if (blockIdx.x == 0) {  // ragged tail (elements past the last full tile): CTA 0, direct loads
     for (size_t e = ntiles_full * TE + threadIdx.x; e < n; e += blockDim.x) {
       const size_t blk = e / B;
-      const float th = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)ms.codes[blk / nbs][e], scales[blk])), theta[e]);
+      const float sb = scales ? scales[blk] : ms.scales[blk / nbs][blk];
+      const float th = __fadd_rn(__fmul_rn(coef, __fmul_rn((float)ms.codes[blk / nbs][e], sb)), theta[e]);
       theta[e] = th;
       bad |= !is_finite(th);
     }
