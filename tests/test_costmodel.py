@@ -181,17 +181,18 @@ def test_b200_step_model_fit_and_terms():
 @pytest.mark.gpu
 def test_b200_step_model_predicts_virtual_worker_step():
     """On one GPU: fit the compression and fold terms from their own
-    measurements, then predict a step the fit did not see -- W = 3 virtual
-    workers (3 x K1 + the 3-payload apply, no exchange) -- within 15 %."""
+    measurements at P = 2 and 8, then predict a step the fit did not see --
+    W = 4 virtual workers (4 x K1 + the 4-payload apply, no exchange) --
+    within 15 %."""
     import torch
     from paper_2506_17551_b200.costmodel import B200StepModel, measure_step_parts
     from paper_2506_17551_b200.engine import Context, generate
     n, k = 16_000_000, 160_000
     c = Context(n, k, 8)
-    parts = measure_step_parts(c, n, k, Ps=(2, 4, 8))
+    parts = measure_step_parts(c, n, k, Ps=(2, 8))
     m = B200StepModel.fit(parts["compress_p1"], parts["compress"], 0.0, k, parts["apply_by_p"], {},
                           parts["payload_bytes"])
-    W = 3
+    W = 4
     g = torch.empty(W, n, device="cuda")
     for w in range(W):
         generate("llmrec", 42, w, 5, n, g[w])
