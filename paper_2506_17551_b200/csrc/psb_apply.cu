@@ -157,7 +157,7 @@ __host__ __device__ constexpr int apply_minb(int PT, bool TMA) { return TMA ? PS
 template <class T, bool ASYNC, int PT, bool TMA>
 __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
     k_sparse_apply_bm(PayloadView v, int P_rt, uint32_t nseg, uint32_t seg_lo, const uint32_t* __restrict__ range,
-                      int seg_shift, uint32_t vcap, uint32_t ci_bytes, uint32_t cv_bytes,
+                      int seg_shift, uint32_t vcap, uint32_t ci_bytes, uint32_t cv_bytes, uint32_t light_max,
                       const uint32_t* __restrict__ seg_off, int order, uint32_t dpn, uint32_t npr, T coef,
                       WorkerCoefs wscale, T* __restrict__ theta, size_t n, T* __restrict__ mean_out,
                       uint32_t* __restrict__ list_idx, T* __restrict__ list_val, uint32_t* list_cnt,
@@ -223,7 +223,13 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
   // warp 0: descriptor of a segment into buffer b; under TMA also issue its
   // bulk copies when the widened ranges fit the stage
   auto describe = [&](int b, uint32_t seg, uint32_t l, uint32_t cnt) {
-    const uint32_t incl = warp_incl(cnt);
+    uint32_t incl = warp_incl(cnt);
+    // a segment of at most light_max entries is k_sparse_apply_light's:
+    // described as empty here
+    if (TMA && __shfl_sync(0xffffffffu, incl, 31) <= light_max) {
+      cnt = 0;
+      incl = 0;
+    }
     const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
     uint32_t bi = incl - cnt, bv = incl - cnt;  // non-TMA / unstaged: the flat entry index
     bool fits = false;
@@ -554,6 +560,103 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
   if (bad) atomicOr(flags, 1u);
 }
 
+// Segments of at most 32 entries (most of the index space of a skewed
+// gradient: 60 % of cfg2's segments hold ~17), one warp each: a lane per
+// entry, the lanes holding the same index found with __match_any_sync; the
+// lowest one (the lowest worker) folds the P values (+0 where absent) in the
+// reference order and updates theta once -- no bitmaps, no CTA barriers.
+// Bitwise the same arithmetic as k_sparse_apply_bm.
+template <class T, bool ASYNC>
+__global__ void __launch_bounds__(256) k_sparse_apply_light(PayloadView v, int P, uint32_t nseg, int seg_shift,
+                                                            uint32_t light_max, const uint32_t* __restrict__ seg_off,
+                                                            int order, uint32_t dpn, uint32_t npr, T coef,
+                                                            WorkerCoefs wscale, T* __restrict__ theta, size_t n,
+                                                            T* __restrict__ mean_out, uint32_t* flags) {
+  __shared__ int sq[8][32];
+  __shared__ T sv[8][32];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (flags != nullptr && (__ldcg(flags) & 8u)) return;  // a peer timed out: theta untouched
+  const T inv = (T)(1.0 / (double)P);
+  bool bad = false;
+  RingChunk rc;
+  const uint32_t warp = blockIdx.x * (blockDim.x >> 5) + wid, nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t seg = warp; seg < nseg; seg += nwarps) {
+    uint32_t l = 0, cnt = 0;
+    if (lane < (uint32_t)P) {
+      const uint32_t* row = v.wpr ? reinterpret_cast<const uint32_t*>(v.rank_base[lane / v.wpr] + v.tab_off) +
+                                        (size_t)lane * (nseg + 1)
+                                  : seg_off + (size_t)lane * (nseg + 1);
+      l = row[seg];
+      cnt = row[seg + 1] - l;
+    }
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += t;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (tot == 0 || tot > light_max) continue;  // uniform; heavy segments are the TMA kernel's
+    // worker of entry `lane`: the lowest p with lane < incl_p
+    int q = -1;
+    uint32_t base = 0, lq = 0;
+    for (int p = P - 1; p >= 0; --p) {
+      const uint32_t ip = __shfl_sync(0xffffffffu, incl, p), cp = __shfl_sync(0xffffffffu, cnt, p);
+      const uint32_t pl = __shfl_sync(0xffffffffu, l, p);
+      if (lane < ip && lane >= ip - cp) {
+        q = p;
+        base = ip - cp;
+        lq = pl;
+      }
+    }
+    const size_t seg_base = (size_t)seg << seg_shift;
+    uint32_t i32 = 0xffffffffu;
+    T x = T(0);
+    if (lane < tot) {
+      const uint32_t j = lq + (lane - base);
+      if (v.idx16)
+        i32 = (uint32_t)seg_base + reinterpret_cast<const uint16_t*>(pl_block(v, q))[j];
+      else
+        i32 = pl_idx(v, q)[j];
+      x = pl_val<T>(v, q, j);
+    }
+    sq[wid][lane] = q;
+    sv[wid][lane] = x;
+    const unsigned act = __ballot_sync(0xffffffffu, lane < tot);
+    const unsigned grp = __match_any_sync(0xffffffffu, i32);
+    __syncwarp();
+    if (lane < tot && (__ffs(grp) - 1) == (int)lane) {  // the group's owner: its lowest worker
+      const size_t i = i32;
+      const unsigned mem = grp & act;
+      auto g = [&](int qq) -> T {
+        for (unsigned m = mem; m; m &= m - 1) {
+          const int ml = __ffs(m) - 1;
+          if (sq[wid][ml] == qq) return sv[wid][ml];
+        }
+        return T(0);
+      };
+      T t = theta ? theta[i] : T(0);
+      if (ASYNC) {
+        for (unsigned m = mem; m; m &= m - 1) {  // present workers in worker order
+          const int ml = __ffs(m) - 1;
+          t = add_rn(mul_rn((T)(-wscale.v[sq[wid][ml]]), sv[wid][ml]), t);
+        }
+      } else {
+        const int rs = order == PSB_ORDER_RING ? rc.start_for(i, n, P) : 0;
+        const T mean = mul_rn(fold_sum_start<T>(g, P, order, rs, dpn, npr), inv);
+        t = add_rn(mul_rn(coef, mean), t);
+        if (mean_out) mean_out[i] = mean;
+      }
+      if (theta) {
+        theta[i] = t;
+        bad |= !is_finite(t);
+      }
+    }
+    __syncwarp();
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1u);
+}
+
 // P == 1: one payload, every touched index owned by worker 0.
 template <class T, bool ASYNC>
 __global__ void k_sparse_apply1(PayloadView v, size_t k, T coef, T* __restrict__ theta,
@@ -698,6 +801,9 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
   if (async_mode)
     for (int q = 0; q < P; ++q) ws.v[q] = wscale_host[q];
   const int PTi = P == 2 || P == 4 || P == 8 ? P : 0;
+  // segments of <= 32 entries: one warp each (k_sparse_apply_light), the
+  // TMA kernel skips them
+  const uint32_t light = tma && P >= 4 ? c->apply_light : 0u;  // P = 2: measured 81 -> 85 us, off
   auto launch = [&](auto kern, T* mo, bool is_tma) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int thr = apply_threads(PTi, is_tma);
@@ -709,9 +815,19 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, thr, smem);
       grid = (unsigned)std::min<size_t>(nseg, (size_t)c->num_sms * (size_t)std::max(occ, 1));
     }
-    kern<<<grid, thr, smem, st>>>(v, P, nseg, 0u, nullptr, seg_shift, vcap, ci, cv, tab, (int)order, dpn, npr, coef,
-                                  ws, theta, n, mo, nullptr, nullptr, nullptr, c->d_flags);
+    kern<<<grid, thr, smem, st>>>(v, P, nseg, 0u, nullptr, seg_shift, vcap, ci, cv, is_tma ? light : 0u, tab,
+                                  (int)order, dpn, npr, coef, ws, theta, n, mo, nullptr, nullptr, nullptr, c->d_flags);
   };
+  if (light) {
+    const unsigned lgrid = (unsigned)std::min<size_t>((nseg + 7) / 8, (size_t)c->num_sms * 16);
+    if (async_mode)
+      k_sparse_apply_light<T, true><<<lgrid, 256, 0, st>>>(v, P, nseg, seg_shift, light, tab, (int)order, dpn, npr,
+                                                            coef, ws, theta, n, nullptr, c->d_flags);
+    else
+      k_sparse_apply_light<T, false><<<lgrid, 256, 0, st>>>(v, P, nseg, seg_shift, light, tab, (int)order, dpn, npr,
+                                                             coef, ws, theta, n, mean_out, c->d_flags);
+    c->launches += 1;
+  }
 #define PSB_APPLY_LAUNCH(ASY, MO)                                                                       \
   do {                                                                                                  \
     if (tma) {                                                                                          \
@@ -777,7 +893,7 @@ psb_status shard_fold_impl(psb_ctx* c, int P, const uint32_t* sidx, const T* sva
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // persistent CTAs over the device-decided segment range
     kern<<<c->num_sms * 4, apply_threads(P == 2 || P == 4 || P == 8 ? P : 0, false), smem, st>>>(
-        v, P, 0u, 0u, range, seg_shift, vcap, 0u, 0u, srow, (int)order, dpn, npr, coef, ws, theta, n, nullptr, list_idx,
+        v, P, 0u, 0u, range, seg_shift, vcap, 0u, 0u, 0u, srow, (int)order, dpn, npr, coef, ws, theta, n, nullptr, list_idx,
         list_val, list_cnt, c->d_flags);
   };
   if (async_mode) {

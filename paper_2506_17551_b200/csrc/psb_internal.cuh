@@ -126,6 +126,7 @@ struct psb_ctx {
   // PSB_APPLY_TMA_CAP: entries per TMA stage; 1792 fits a cfg2 segment (at
   // most 1759 entries at P = 2..8) and 4 CTAs per SM
   uint32_t apply_tma_cap = 1792;
+  uint32_t apply_light = 32;  // PSB_APPLY_LIGHT: segments of <= this many entries go one warp each (0: off)
   int q8_no_tma = 0;   // PSB_Q8_NO_TMA=1: register double-buffer kernel for the one-worker q8 step
   int q8_unfused = 0;  // PSB_Q8_UNFUSED=1: single-rank q8 step as quant + reduce (diagnostics)
   // NVLink peer exchange (psb_peer.cu)

@@ -501,3 +501,54 @@ def test_q8_step_block_sizes(ctx, block, W):
         O.sync_step(g_h, theta_h, lr, "q8", 0, "naive", res_h, 0, 1, block)
         assert np.array_equal(bits(tnp(theta)), bits(theta_h)), step
         assert np.array_equal(bits(tnp(res)), bits(res_h)), step
+
+
+def skewed_payloads(P, n, k, dtype, seed):
+    """A hot quarter of the index space holding most entries (heavy segments)
+    and a sparse rest (segments of a few entries: the one-warp light path),
+    with cross-worker collisions in both, +-0 values."""
+    rng = np.random.default_rng(seed)
+    idx = np.zeros((P, k), dtype=np.uint32)
+    val = np.zeros((P, k), dtype=dtype)
+    hot = rng.choice(n // 4, size=min(n // 4, 2 * k), replace=False)
+    for p in range(P):
+        kh = (3 * k) // 4
+        cold = rng.choice(np.arange(n // 4, n), size=k - kh, replace=False)
+        idx[p] = np.sort(np.concatenate([rng.choice(hot, size=kh, replace=False), cold]))
+        v = rng.standard_normal(k).astype(dtype)
+        v[rng.random(k) < 0.05] = dtype(0.0)
+        v[rng.random(k) < 0.05] = -dtype(0.0)
+        val[p] = v
+    return idx, val
+
+
+@pytest.mark.parametrize("P,order,dpn,npr", [(4, "ring", 0, 1), (8, "naive", 0, 1), (8, "ring", 0, 1),
+                                             (16, "hierarchical", 4, 2), (5, "ring", 0, 1)])
+@pytest.mark.parametrize("asynch", [False, True])
+def test_sparse_apply_light_and_heavy_segments(ctx, P, order, dpn, npr, asynch):
+    """Mixed light (<= 32 entries: one warp each) and heavy (TMA-staged)
+    segments in one apply, mean and async: bit-exact with the oracle."""
+    dt = np.float32
+    n, k = 2_000_003, 6_000
+    idx, val = skewed_payloads(P, n, k, dt, seed=P * 31 + len(order) + asynch)
+    theta_h = O.generate("uniform", 3, 0, 0, n).astype(dt)
+    pl = pack_payloads(idx, val, torch.float32)
+    theta = torch.from_numpy(theta_h.copy()).cuda()
+    want = theta_h.copy()
+    if asynch:
+        scales = [0.05 / (1.0 + (p % 3)) for p in range(P)]
+        for p in range(P):
+            d = np.zeros(n, dtype=dt)
+            d[idx[p].astype(np.int64)] = val[p]
+            O.axpy_(-scales[p], d, want)
+        ctx.sparse_async_apply(pl, P, k, torch.float32, scales, theta)
+    else:
+        dense = np.zeros((P, n), dtype=dt)
+        for p in range(P):
+            dense[p, idx[p].astype(np.int64)] = val[p]
+        mean_h = O.fold_mean(dense, order, dpn, npr)
+        O.axpy_(-0.05, mean_h, want)
+        topo = topology(1, npr, dpn) if dpn else None
+        ctx.sparse_mean_sgd(pl, P, k, torch.float32, order, 0.05, theta, n, None, topo)
+    ctx.check()
+    assert np.array_equal(bits(tnp(theta)), bits(want))

@@ -1,1 +1,3 @@
-for lib in libpsb.so libpsb_u1.so libpsb_u3.so; do echo "== $lib"; PSB_LIB=$lib PROBE_P=2,4,8 python tools/probe_apply.py ring; done
+timeout 600 python -m pytest tests/test_apply_gpu.py -q -x 2>&1 | tail -2
+echo "== light 32 (default)"; python tools/probe_apply.py ring; PROBE_P=8 python tools/probe_apply.py naive
+echo "== light off"; PSB_APPLY_LIGHT=0 python tools/probe_apply.py ring
