@@ -803,7 +803,9 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
   const int PTi = P == 2 || P == 4 || P == 8 ? P : 0;
   // segments of <= 32 entries: one warp each (k_sparse_apply_light), the
   // TMA kernel skips them
-  const uint32_t light = tma && P >= 4 ? c->apply_light : 0u;  // P = 2: measured 81 -> 85 us, off
+  // (P = 2: measured 81 -> 85 us; direct view: the warp's remote row / entry
+  // loads are slower than the TMA stage, N = 4 0.421 -> 0.429 ms: both off)
+  const uint32_t light = tma && P >= 4 && !v.wpr ? c->apply_light : 0u;
   auto launch = [&](auto kern, T* mo, bool is_tma) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int thr = apply_threads(PTi, is_tma);

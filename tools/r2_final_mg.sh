@@ -1,8 +1,8 @@
 # final multi-GPU check: GPU tests on 4 GPUs, then bench lines at N=2 and N=4
-mkdir -p gpurun_out/final3
-timeout 1800 python -m pytest tests/test_multigpu_gpu.py -q > gpurun_out/final3/mg4_tests.txt 2>&1
+mkdir -p gpurun_out/final5
+timeout 1800 python -m pytest tests/test_multigpu_gpu.py -q > gpurun_out/final5/mg4_tests.txt 2>&1
 for N in 2 4; do
   for cfg in cfg2 cfg3 cfg4; do
-    timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port $((29600 + N * 10 + RANDOM % 9)) bench.py --gpus $N --config $cfg --steps 20 --warmup 5 2>/dev/null | grep "^{" > gpurun_out/final3/bench_${cfg}_n$N.json
+    timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port $((29600 + N * 10 + RANDOM % 9)) bench.py --gpus $N --config $cfg --steps 20 --warmup 5 2>/dev/null | grep "^{" > gpurun_out/final5/bench_${cfg}_n$N.json
   done
 done
