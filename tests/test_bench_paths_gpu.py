@@ -261,3 +261,41 @@ def test_wire_decode_keeps_step_flags(ctx):
     with pytest.raises(PsbNonFinite):
         ctx.check()
     ctx.check()
+
+
+@pytest.mark.parametrize("n,k", [(1_000_003, 100_000), (600_001, 30_001), (4096 * 50, 4096 * 5)])
+def test_dense_payload_fused_update_bitwise(ctx, n, k):
+    """rho 5-10 % at one worker through the fused P = 1 step (K1's scattered
+    theta update at a dense payload) -- bitwise the oracle's sync step over
+    several EF steps."""
+    run_ef_sequence(ctx, n, k, 4, fused=True)
+
+
+def test_dense_payload_fused_update_full_size(cuda):
+    """cfg5 rho = 10 % at 125M, fused step without mean_out, theta with -0
+    entries: theta = RN(RN(-lr * v) + theta) at the selected indices,
+    bit-for-bit untouched elsewhere."""
+    from paper_2506_17551_b200 import _lib as L
+    from paper_2506_17551_b200.engine import Context, generate
+    n = 125_000_000
+    k = n // 10
+    lr = 0.05
+    c = Context(n, k, 1)
+    g = torch.empty(n, device="cuda")
+    r = torch.zeros(n, device="cuda")
+    theta = torch.empty(n, device="cuda")
+    generate("uniform", 9, 1, 0, n, theta)
+    theta[::7] = -0.0
+    coef = torch.tensor(-lr, dtype=torch.float32, device="cuda")
+    for step in range(2):
+        generate("llmrec", 42, 0, step, n, g)
+        p = r + g
+        th0 = theta.clone()
+        c.sync_step(c.step_desc(L.PSB_COMP_TOPK, g.view(1, n), r.view(1, n), theta, lr, k, "ring"))
+        c.check()
+        sel = expected_selection(p, k)
+        assert torch.equal(bits(r), bits(torch.where(sel, torch.zeros_like(p), p))), step
+        upd = th0 + coef * p
+        assert torch.equal(bits(theta), bits(torch.where(sel, upd, th0))), step
+        del p, sel, upd, th0
+    c.close()
