@@ -12,7 +12,7 @@ are host bindings:
   parsim     reference-shaped API (same names/semantics as namespace parsim)
   dist       NCCL communicator bootstrap over torch.distributed
   train      the reference trainer around the device path (BPR producer)
-  costmodel  the reference's alpha-beta model, calibrated on measured NVLink
+  costmodel  the reference's alpha-beta model and the measured B200 step model
 """
 from ._lib import PsbError, PsbInvalidArgument, PsbNonFinite, LIB_PATH, load  # noqa: F401
 
