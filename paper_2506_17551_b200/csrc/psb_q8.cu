@@ -882,6 +882,9 @@ __global__ void __launch_bounds__(256) k_q8_apply_tma(Q8Shards ms, const float* 
   const size_t ntiles_full = n / TE;
   const size_t my_tiles = ntiles_full > blockIdx.x ? (ntiles_full - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   const size_t nbs = ms.nbs;
+  // a peer timed out in the exchange (flag 8): its shard may be stale, theta
+  // is left untouched and psb_check reports PSB_ESTATE
+  if (flags != nullptr && (__ldcg(flags) & 8u)) return;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kQ8Stages; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
