@@ -85,8 +85,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 constexpr int kSegU = 8;  // entries per thread in k_seg_offsets
 
+// With out16 != nullptr it also writes worker q's wire16 payload (u16
+// in-segment offset | value, psb_wire16_bytes layout) at out16 + q * out_stride
+// in the same pass (vbytes: 4 or 8).
 __global__ void __launch_bounds__(256) k_seg_offsets(PayloadView v, int P, uint32_t k, uint32_t nseg,
-                                                     int seg_shift, uint32_t* __restrict__ seg_off) {
+                                                     int seg_shift, uint32_t* __restrict__ seg_off,
+                                                     uint8_t* __restrict__ out16, size_t out_stride, int vbytes) {
   const int q = blockIdx.y;
   const uint32_t* idx = pl_idx(v, q);
   uint32_t* row = seg_off + (size_t)q * (nseg + 1);
@@ -97,6 +101,23 @@ __global__ void __launch_bounds__(256) k_seg_offsets(PayloadView v, int P, uint3
     const uint32_t j = base + u * blockDim.x;
     cur[u] = j < k ? idx[j] : 0u;
     prv[u] = (j && j < k) ? idx[j - 1] : 0u;
+  }
+  if (out16) {
+    const uint32_t mask = (1u << seg_shift) - 1u;
+    uint8_t* o = out16 + (size_t)q * out_stride;
+    uint16_t* lo16 = reinterpret_cast<uint16_t*>(o);
+    const uint8_t* vsrc = pl_block(v, q) + v.val_off;
+    uint8_t* vdst = o + ((2 * (size_t)k + 15) & ~(size_t)15);
+#pragma unroll
+    for (int u = 0; u < kSegU; ++u) {
+      const uint32_t j = base + u * blockDim.x;
+      if (j >= k) continue;
+      lo16[j] = (uint16_t)(cur[u] & mask);
+      if (vbytes == 8)
+        reinterpret_cast<uint64_t*>(vdst)[j] = reinterpret_cast<const uint64_t*>(vsrc)[j];
+      else
+        reinterpret_cast<uint32_t*>(vdst)[j] = reinterpret_cast<const uint32_t*>(vsrc)[j];
+    }
   }
 #pragma unroll
   for (int u = 0; u < kSegU; ++u) {
@@ -780,7 +801,8 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
   if (!tab) {
     PSB_REQUIRE(c, (size_t)P * (nseg + 1) <= c->seg_cap, "sparse apply: segment table exceeds ctx capacity");
     const unsigned gx = (unsigned)((k + 256 * kSegU - 1) / (256 * kSegU));
-    k_seg_offsets<<<dim3(gx, (unsigned)P), 256, 0, st>>>(v, P, (uint32_t)k, nseg, seg_shift, c->d_seg_off);
+    k_seg_offsets<<<dim3(gx, (unsigned)P), 256, 0, st>>>(v, P, (uint32_t)k, nseg, seg_shift, c->d_seg_off, nullptr,
+                                                         0, 0);
     c->launches += 1;
     tab = c->d_seg_off;
   }
@@ -1094,39 +1116,10 @@ psb_status psb_sparse_apply_tab(psb_ctx* c, psb_compressor comp, psb_dtype dt, i
 // (S-1) | val) -- the apply segment of S = 2^seg_shift <= 2^16 indices an
 // entry falls in is recovered from the per-segment offset rows.
 namespace {
-template <class T>
-__global__ void k_pack16(const uint32_t* __restrict__ idx, const T* __restrict__ val, size_t k, uint32_t mask,
-                         uint16_t* __restrict__ lo16, T* __restrict__ val16) {
-  for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (size_t)gridDim.x * blockDim.x) {
-    lo16[j] = (uint16_t)(idx[j] & mask);
-    val16[j] = val[j];
-  }
-}
 }  // namespace
 
 size_t psb_wire16_bytes(psb_dtype dt, size_t k) {
   return psb_align16(2 * k) + psb_align16((dt == PSB_F64 ? 8 : 4) * k);
-}
-
-psb_status psb_pack16(psb_ctx* c, psb_dtype dt, const void* payload, size_t k, int seg_shift, void* out,
-                      cudaStream_t st) {
-  const uint8_t* b = reinterpret_cast<const uint8_t*>(payload);
-  uint8_t* o = reinterpret_cast<uint8_t*>(out);
-  const uint32_t mask = (1u << seg_shift) - 1u;
-  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((k + 255) / 256, (size_t)c->num_sms * 8));
-  if (dt == PSB_F64)
-    k_pack16<double><<<grid, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(b),
-                                           reinterpret_cast<const double*>(b + psb_align16(4 * k)), k, mask,
-                                           reinterpret_cast<uint16_t*>(o),
-                                           reinterpret_cast<double*>(o + psb_align16(2 * k)));
-  else
-    k_pack16<float><<<grid, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(b),
-                                          reinterpret_cast<const float*>(b + psb_align16(4 * k)), k, mask,
-                                          reinterpret_cast<uint16_t*>(o),
-                                          reinterpret_cast<float*>(o + psb_align16(2 * k)));
-  c->launches += 1;
-  PSB_LAUNCH_CHECK(c, "wire16 pack");
-  return PSB_OK;
 }
 
 // P wire16 payloads (blocks of psb_wire16_bytes) + their offset rows -> apply.
@@ -1171,10 +1164,13 @@ psb_status psb_sparse_apply_direct(psb_ctx* c, psb_compressor comp, psb_dtype dt
 }
 
 psb_status psb_seg_offsets(psb_ctx* c, psb_compressor comp, psb_dtype dt, int nw, const void* payloads, size_t k,
-                           uint32_t nseg, int seg_shift, uint32_t* rows, cudaStream_t st) {
+                           uint32_t nseg, int seg_shift, uint32_t* rows, cudaStream_t st, void* out16,
+                           size_t out_stride) {
   const PayloadView v = make_view(comp, dt, payloads, k);
   const unsigned gx = (unsigned)((k + 256 * kSegU - 1) / (256 * kSegU));
-  k_seg_offsets<<<dim3(gx, (unsigned)nw), 256, 0, st>>>(v, nw, (uint32_t)k, nseg, seg_shift, rows);
+  k_seg_offsets<<<dim3(gx, (unsigned)nw), 256, 0, st>>>(v, nw, (uint32_t)k, nseg, seg_shift, rows,
+                                                        reinterpret_cast<uint8_t*>(out16), out_stride,
+                                                        dt == PSB_F64 ? 8 : 4);
   c->launches += 1;
   PSB_LAUNCH_CHECK(c, "segment offsets");
   return PSB_OK;

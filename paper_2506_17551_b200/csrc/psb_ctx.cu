@@ -438,7 +438,7 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
                       (c->direct_mode == 1 || (c->direct_mode == 2 && d->compressor == PSB_COMP_TOPK));
   // pull / direct mode, top-k f32/f64: the arena slots carry wire16 payloads
   // (u16 in-segment index | value: 6 instead of 8 bytes per entry on
-  // NVLink); K1 writes the standard payload into local scratch and k_pack16
+  // NVLink); K1 writes the standard payload into local scratch and k_seg_offsets
   // converts
   const bool wire16 = peer && !shard && !push && plan != nullptr && P >= 2 &&
                       d->compressor == PSB_COMP_TOPK && !c->no_wire16;
@@ -521,17 +521,11 @@ static psb_status compress_and_gather(psb_ctx* c, const psb_step_desc* d, cudaSt
   if (tabs) {
     const ShardPlan& sp = *plan;
     uint32_t* tab = reinterpret_cast<uint32_t*>(gb + sp.tab_off) + (size_t)c->rank * W * (sp.nseg + 1);
-    s = psb_seg_offsets(c, d->compressor, d->dtype, W, kb, d->k, sp.nseg, sp.seg_shift,
-                        tab, st);
+    // the offset rows and (wire16) the arena payloads in one pass over K1's output
+    s = psb_seg_offsets(c, d->compressor, d->dtype, W, kb, d->k, sp.nseg, sp.seg_shift, tab, st,
+                        wire16 ? gb + (size_t)c->rank * W * pblk : nullptr, pblk);
     if (s) return s;
-    if (wire16) {
-      for (int w = 0; w < W; ++w) {
-        const int gid = c->rank * W + w;
-        s = psb_pack16(c, d->dtype, kb + (size_t)w * blk, d->k, sp.seg_shift, gb + (size_t)gid * pblk, st);
-        if (s) return s;
-      }
-      plan->wire16 = true;
-    }
+    if (wire16) plan->wire16 = true;
     psb_mark(c, st);
   }
   if (push) {
@@ -1103,13 +1097,12 @@ static psb_status async_round_pipelined(psb_ctx* c, const psb_step_desc* d, cons
     s = psb_peer_wait_ack(c, as);
     if (s) return s;
     uint32_t* tab = reinterpret_cast<uint32_t*>(gb + tab_off) + (size_t)c->rank * W * (nseg + 1);
-    s = psb_seg_offsets(c, d->compressor, d->dtype, W, kb, d->k, nseg, seg_shift, tab, as);
+    s = psb_seg_offsets(c, d->compressor, d->dtype, W, kb, d->k, nseg, seg_shift, tab, as,
+                        wire16 ? gb + (size_t)c->rank * W * pblk : nullptr, pblk);
     if (s) return s;
-    for (int w = 0; w < W; ++w) {
+    for (int w = 0; w < W && !wire16; ++w) {
       const int gid = c->rank * W + w;
-      if (wire16) s = psb_pack16(c, d->dtype, kb + (size_t)w * blk, d->k, seg_shift, gb + (size_t)gid * pblk, as);
-      else
-        s = cudaMemcpyAsync(gb + (size_t)gid * pblk, kb + (size_t)w * blk, blk, cudaMemcpyDeviceToDevice, as) ==
+      s = cudaMemcpyAsync(gb + (size_t)gid * pblk, kb + (size_t)w * blk, blk, cudaMemcpyDeviceToDevice, as) ==
                     cudaSuccess
                 ? PSB_OK
                 : psb_set_err(c, PSB_ECUDA, "async pipeline: payload copy");

@@ -198,7 +198,8 @@ psb_status psb_shard_finish(psb_ctx* c, psb_dtype dt, size_t list_off, size_t li
                             size_t max_entries, cudaStream_t st);
 // sparse apply pieces (psb_apply.cu)
 psb_status psb_seg_offsets(psb_ctx* c, psb_compressor comp, psb_dtype dt, int nw, const void* payloads, size_t k,
-                           uint32_t nseg, int seg_shift, uint32_t* rows, cudaStream_t st);
+                           uint32_t nseg, int seg_shift, uint32_t* rows, cudaStream_t st, void* out16 = nullptr,
+                           size_t out_stride = 0);
 // P-worker sparse apply with the per-segment offset rows already computed
 // (tab: [P][nseg+1] for segments of 2^psb_apply_seg_shift(P); nullptr: compute them)
 psb_status psb_sparse_apply_tab(psb_ctx* c, psb_compressor comp, psb_dtype dt, int P, const void* payloads, size_t k,
@@ -207,8 +208,6 @@ psb_status psb_sparse_apply_tab(psb_ctx* c, psb_compressor comp, psb_dtype dt, i
                                 cudaStream_t st);
 // wire16 payloads: (u16 in-segment index | val) blocks for the NVLink exchange
 size_t psb_wire16_bytes(psb_dtype dt, size_t k);
-psb_status psb_pack16(psb_ctx* c, psb_dtype dt, const void* payload, size_t k, int seg_shift, void* out,
-                      cudaStream_t st);
 psb_status psb_sparse_apply_wire16(psb_ctx* c, psb_dtype dt, int P, const void* payloads, size_t k,
                                    const uint32_t* tab, psb_order order, const psb_topology* topo, double lr,
                                    const double* wscale, int async_mode, void* theta, size_t n, void* mean_out,
