@@ -10,7 +10,7 @@ from paper_2506_17551_b200 import _lib as L  # noqa: E402
 from paper_2506_17551_b200.engine import Context, generate, payload_bytes  # noqa: E402
 
 n = 125_000_000
-k = n // 100
+k = int(n * float(os.environ.get("PROBE_RHO", "0.01")))
 order = sys.argv[1] if len(sys.argv) > 1 else "ring"
 for P in [int(x) for x in os.environ.get("PROBE_P", "2,4,8").split(",")]:
     c = Context(n, k, P)
