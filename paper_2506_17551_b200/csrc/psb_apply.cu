@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(apply_threads(PT, TMA), apply_minb(PT, TMA))
           }
           mark(q, il, ilp, r);
         };
-        if constexpr (PT > 0 && (apply_threads(PT, TMA) / 32) % PT == 0) {
+        if constexpr (PT > 0 && (apply_threads(PT, TMA) / 32) % (PT > 0 ? PT : 1) == 0) {
           // warps own workers: warp w takes worker w % P, part w / P of its entries
           const int wid = threadIdx.x >> 5, q = wid % PT, nparts = (int)(blockDim.x >> 5) / PT;
           const uint32_t cq = vb[q + 1] - vb[q];
@@ -678,6 +678,103 @@ __global__ void __launch_bounds__(256) k_sparse_apply_light(PayloadView v, int P
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, 1u);
 }
 
+// Dense payloads (P*k a large fraction of n): fold by streaming.  One CTA per
+// segment (S <= 32 KB of accumulator) folds the workers in the reference
+// order, one pass per worker: pass s adds the s-th worker's values at its
+// indices (the first present value initialises the element).  Skipping the
+// absent workers' +0 terms only changes the sign of a zero sum, and the
+// reference's result is recovered exactly by one final RN(acc + (+0)) where
+// any worker was absent (a -0 partial sum becomes +0 at the first absent
+// worker and stays +0; any other value is unchanged by +0).  theta then
+// streams through once: theta = RN(RN(-lr * RN(acc * (1/P))) + theta) (acc =
+// +0 where no worker is present: theta + (-0) leaves theta bitwise
+// unchanged, so the host requires lr >= 0).  A segment crossing a ring chunk
+// boundary is two ranges with their own rotation.  Plain orders only (naive,
+// ring, hierarchical within one node).
+constexpr int kDenseTile = 8192;
+
+template <class T>
+__global__ void __launch_bounds__(256) k_dense_fold_apply(PayloadView v, int P, uint32_t nseg, int seg_shift,
+                                                          const uint32_t* __restrict__ seg_off, int ring, T coef,
+                                                          T* __restrict__ theta, size_t n, uint32_t* flags) {
+  constexpr uint32_t TT = kDenseTile * 4 / sizeof(T);  // 32 KB of accumulator
+  __shared__ __align__(16) T acc[TT];
+  __shared__ uint8_t cnt[TT];
+  __shared__ uint32_t lo_s[PSB_MAX_P], cnt_s[PSB_MAX_P];
+  const T inv = (T)(1.0 / (double)P);
+  const uint32_t S = 1u << seg_shift;  // <= TT (host)
+  bool bad = false;
+  if (flags != nullptr && (__ldcg(flags) & 8u)) return;
+  RingChunk rc;
+  for (uint32_t seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
+    const size_t tlo = (size_t)seg << seg_shift;
+    const size_t thi = min(tlo + S, n);
+    __syncthreads();  // the previous segment is done with shared memory
+    if (threadIdx.x < (unsigned)P) {
+      const uint32_t* row = seg_off + (size_t)threadIdx.x * (nseg + 1);
+      lo_s[threadIdx.x] = row[seg];
+      cnt_s[threadIdx.x] = row[seg + 1] - row[seg];
+    }
+    for (uint32_t e = threadIdx.x; e < S / 4; e += blockDim.x) reinterpret_cast<uint32_t*>(cnt)[e] = 0u;
+    size_t b = thi;  // first index of the second range (ring chunk boundary)
+    int rotA = 0, rotB = 0;
+    if (ring) {
+      rotA = rc.start_for(tlo, n, P);
+      if (rc.hi < thi) {
+        b = rc.hi;
+        rotB = rc.start_for(b, n, P);
+      }
+    }
+    __syncthreads();
+    for (int s = 0; s < P; ++s) {
+      for (int r = 0; r < 2; ++r) {
+        const size_t rlo = r ? b : tlo, rhi = r ? thi : b;
+        if (rlo >= rhi) continue;
+        int q = (r ? rotB : rotA) + s;
+        if (q >= P) q -= P;
+        const uint32_t l = lo_s[q], c = cnt_s[q];
+        const uint8_t* blk = pl_block(v, q);
+        for (uint32_t j = threadIdx.x; j < c; j += blockDim.x) {
+          const uint32_t jj = l + j;
+          const size_t i = v.idx16 ? (tlo + reinterpret_cast<const uint16_t*>(blk)[jj])
+                                   : (size_t)reinterpret_cast<const uint32_t*>(blk)[jj];
+          if (i < rlo || i >= rhi) continue;
+          const uint32_t e = (uint32_t)(i - tlo);
+          const T x = pl_val<T>(v, q, jj);
+          acc[e] = cnt[e] ? add_rn(acc[e], x) : x;
+          cnt[e] += 1;
+        }
+      }
+      __syncthreads();  // worker s's additions precede worker s+1's
+    }
+    const uint32_t m = (uint32_t)(thi - tlo);
+    auto fin = [&](uint32_t e) -> T {  // the reference's sum: +0 where any worker is absent
+      const T a = cnt[e] ? acc[e] : T(0);
+      return cnt[e] < (uint32_t)P ? add_rn(a, T(0)) : a;
+    };
+    if (sizeof(T) == 4 && (m & 3) == 0 && ((((uintptr_t)theta) + tlo * 4) & 15) == 0) {
+      const float cf = (float)coef, iv = (float)inv;
+      for (uint32_t e4 = threadIdx.x; e4 < m / 4; e4 += blockDim.x) {
+        float4 th = __ldcs(reinterpret_cast<const float4*>(theta + tlo) + e4);
+        const uint32_t e = e4 * 4;
+        th.x = __fadd_rn(__fmul_rn(cf, __fmul_rn((float)fin(e), iv)), th.x);
+        th.y = __fadd_rn(__fmul_rn(cf, __fmul_rn((float)fin(e + 1), iv)), th.y);
+        th.z = __fadd_rn(__fmul_rn(cf, __fmul_rn((float)fin(e + 2), iv)), th.z);
+        th.w = __fadd_rn(__fmul_rn(cf, __fmul_rn((float)fin(e + 3), iv)), th.w);
+        __stcs(reinterpret_cast<float4*>(theta + tlo) + e4, th);
+        bad |= !is_finite(th.x) || !is_finite(th.y) || !is_finite(th.z) || !is_finite(th.w);
+      }
+    } else {
+      for (uint32_t e = threadIdx.x; e < m; e += blockDim.x) {
+        const T th = add_rn(mul_rn(coef, mul_rn(fin(e), inv)), theta[tlo + e]);
+        theta[tlo + e] = th;
+        bad |= !is_finite(th);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
+}
+
 // P == 1: one payload, every touched index owned by worker 0.
 template <class T, bool ASYNC>
 __global__ void k_sparse_apply1(PayloadView v, size_t k, T coef, T* __restrict__ theta,
@@ -798,6 +895,34 @@ psb_status sparse_impl(psb_ctx* c, psb_compressor comp, int P, const void* paylo
   const int seg_shift = psb_apply_seg_shift(P);
   const uint32_t nseg = (uint32_t)((n + ((size_t)1 << seg_shift) - 1) >> seg_shift);
   PSB_REQUIRE(c, k <= 0xffffffffu, "sparse apply: k exceeds 32-bit positions");
+  // dense payloads: the streaming fold (plain orders, no mean_out / async,
+  // lr >= 0, gathered or wire16 views), over segments of at most 32 KB of
+  // accumulator (its own offset table when the apply computes the table)
+  const bool plain_order = order == PSB_ORDER_NAIVE || order == PSB_ORDER_RING ||
+                           (order == PSB_ORDER_HIER && dpn >= (uint32_t)P);
+  const int dshift = sizeof(T) == 4 ? 13 : 12;
+  // (P = 2 measured slower dense: rho 10 % 376 -> 425 us)
+  if (c->dense_fold_pct && P >= 4 && !async_mode && !mean_out && theta && plain_order && !v.q8 && !v.wpr &&
+      !(coef > T(0)) &&
+      (!tab || seg_shift <= dshift) && (double)P * (double)k * 100.0 >= (double)c->dense_fold_pct * (double)n) {
+    int sh = seg_shift;
+    uint32_t ns = nseg;
+    if (!tab) {
+      sh = std::min(seg_shift, dshift);
+      ns = (uint32_t)((n + ((size_t)1 << sh) - 1) >> sh);
+      PSB_REQUIRE(c, (size_t)P * (ns + 1) <= c->seg_cap, "dense fold: segment table exceeds ctx capacity");
+      const unsigned gx = (unsigned)((k + 256 * kSegU - 1) / (256 * kSegU));
+      k_seg_offsets<<<dim3(gx, (unsigned)P), 256, 0, st>>>(v, P, (uint32_t)k, ns, sh, c->d_seg_off, nullptr, 0, 0);
+      c->launches += 1;
+      tab = c->d_seg_off;
+    }
+    const unsigned grid = (unsigned)std::min<size_t>(ns, (size_t)c->num_sms * 8);
+    k_dense_fold_apply<T><<<grid, 256, 0, st>>>(v, P, ns, sh, tab, order == PSB_ORDER_RING ? 1 : 0, coef, theta, n,
+                                                c->d_flags);
+    c->launches += 1;
+    PSB_LAUNCH_CHECK(c, "psb_sparse_mean_sgd (dense fold)");
+    return PSB_OK;
+  }
   if (!tab) {
     PSB_REQUIRE(c, (size_t)P * (nseg + 1) <= c->seg_cap, "sparse apply: segment table exceeds ctx capacity");
     const unsigned gx = (unsigned)((k + 256 * kSegU - 1) / (256 * kSegU));

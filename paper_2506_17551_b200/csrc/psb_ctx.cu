@@ -95,6 +95,7 @@ extern "C" psb_status psb_ctx_create(psb_ctx** out, int device, size_t max_n, si
   if (const char* qs = getenv("PSB_Q8_SCALES_INPLACE")) c->q8_scales_inplace = qs[0] != '0';
   if (const char* qd = getenv("PSB_Q8_DIRECT_APPLY")) c->q8_direct_apply = qd[0] != '0';
   if (const char* nt = getenv("PSB_APPLY_NO_TMA")) c->apply_no_tma = nt[0] != '0';
+  if (const char* df = getenv("PSB_DENSE_FOLD_PCT")) c->dense_fold_pct = (uint32_t)std::max(0l, atol(df));
   if (const char* al = getenv("PSB_APPLY_LIGHT")) c->apply_light = (uint32_t)std::min(32l, std::max(0l, atol(al)));
   if (const char* tc = getenv("PSB_APPLY_TMA_CAP"))
     c->apply_tma_cap = (uint32_t)std::min(8192l, std::max(64l, atol(tc)));

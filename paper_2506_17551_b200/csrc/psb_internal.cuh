@@ -126,7 +126,10 @@ struct psb_ctx {
   // PSB_APPLY_TMA_CAP: entries per TMA stage; 1792 fits a cfg2 segment (at
   // most 1759 entries at P = 2..8) and 4 CTAs per SM
   uint32_t apply_tma_cap = 1792;
-  uint32_t apply_light = 32;  // PSB_APPLY_LIGHT: segments of <= this many entries go one warp each (0: off)
+  uint32_t apply_light = 32;
+  // PSB_DENSE_FOLD_PCT: P payloads with P*k >= pct % of n fold by streaming
+  // (k_dense_fold_apply) instead of the bitmap apply (0: off)
+  uint32_t dense_fold_pct = 20;  // PSB_APPLY_LIGHT: segments of <= this many entries go one warp each (0: off)
   int q8_no_tma = 0;   // PSB_Q8_NO_TMA=1: register double-buffer kernel for the one-worker q8 step
   int q8_unfused = 0;  // PSB_Q8_UNFUSED=1: single-rank q8 step as quant + reduce (diagnostics)
   // NVLink peer exchange (psb_peer.cu)

@@ -552,3 +552,30 @@ def test_sparse_apply_light_and_heavy_segments(ctx, P, order, dpn, npr, asynch):
         ctx.sparse_mean_sgd(pl, P, k, torch.float32, order, 0.05, theta, n, None, topo)
     ctx.check()
     assert np.array_equal(bits(tnp(theta)), bits(want))
+
+
+@pytest.mark.parametrize("P,order,dpn,npr", [(2, "ring", 0, 1), (5, "naive", 0, 1), (4, "ring", 0, 1),
+                                             (8, "ring", 0, 1), (4, "hierarchical", 8, 1), (8, "naive", 0, 1)])
+@pytest.mark.parametrize("dtype_t", [torch.float32, torch.float64])
+def test_dense_fold_apply_bitwise(ctx, P, order, dpn, npr, dtype_t):
+    """P * k >= 20 % of n: the streaming fold (k_dense_fold_apply) -- one
+    accumulator pass per worker in the reference order, +0 for absent
+    workers, ring chunks crossing tiles -- bit-exact with the oracle fold,
+    theta with +-0 entries untouched where no worker is present."""
+    dt = np.float32 if dtype_t == torch.float32 else np.float64
+    n, k = 200_003, 20_000
+    idx, val = make_payloads(P, n, k, dt, seed=P * 5 + len(order))
+    theta_h = O.generate("uniform", 4, 0, 0, n).astype(dt)
+    theta_h[::13] = -0.0
+    theta_h[1::13] = 0.0
+    dense = np.zeros((P, n), dtype=dt)
+    for p in range(P):
+        dense[p, idx[p].astype(np.int64)] = val[p]
+    mean_h = O.fold_mean(dense, order, dpn, npr)
+    want = theta_h.copy()
+    O.axpy_(-0.05, mean_h, want)
+    theta = torch.from_numpy(theta_h.copy()).cuda()
+    topo = topology(1, npr, dpn) if dpn else None
+    ctx.sparse_mean_sgd(pack_payloads(idx, val, dtype_t), P, k, dtype_t, order, 0.05, theta, n, None, topo)
+    ctx.check()
+    assert np.array_equal(bits(tnp(theta)), bits(want))
