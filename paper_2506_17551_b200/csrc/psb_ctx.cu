@@ -27,6 +27,8 @@ psb_status psb_q8_step1_launch(psb_ctx* c, const float* g, size_t gstride, float
                                double lr, float* theta, float* mean_out, cudaStream_t st);
 psb_status psb_q8_apply_tma_launch(psb_ctx* c, const Q8Shards& ms, const float* scales, size_t n, uint32_t B,
                                    double lr, float* theta, cudaStream_t st);
+long long psb_q8_reduce_tma_launch(psb_ctx* c, const Q8Workers& wv, int P, size_t blk_lo, size_t blk_hi, uint32_t B,
+                                   int8_t* mcodes, float* mscales, cudaStream_t st);
 psb_status psb_q8_apply_launch(psb_ctx* c, const Q8Shards& ms, int R, size_t n, uint32_t B, double lr,
                                float* theta, float* mean_out, cudaStream_t st);
 
@@ -662,6 +664,38 @@ static psb_status q8_step_nvlink(psb_ctx* c, const psb_step_desc* d, cudaStream_
   if (!s) s = psb_peer_wait_ready(c, st);
   if (s) return s;
   psb_mark(c, st);
+  const bool plain = d->order == PSB_ORDER_NAIVE || (d->order == PSB_ORDER_HIER && dpn >= (uint32_t)P);
+  if (!c->q8_no_tma && plain && (P == 2 || P == 4 || P == 8) && (B == 128 || B == 256 || (B == 512 && P == 2))) {
+    // the reduce reads every worker's codes and scales of our shard in place
+    // (TMA bulk copies from the peers' arenas): no pull into local memory
+    const uint8_t* regions[PSB_MAX_P];
+    psb_peer_regions(c, regions);
+    Q8Workers wr{};
+    for (int q = 0; q < P; ++q) {
+      const uint8_t* base = regions[q / W];
+      wr.codes[q] = reinterpret_cast<const int8_t*>(base + o_lc) + (size_t)(q % W) * n_pad + blk_lo * B;
+      wr.scales[q] = reinterpret_cast<const float*>(base + o_ls) + (size_t)(q % W) * R * nbs + blk_lo;
+    }
+    psb_mark(c, st);
+    long long tiles = 0;
+    if (blk_hi > blk_lo)
+      tiles = psb_q8_reduce_tma_launch(c, wr, P, blk_lo, blk_hi, B, reinterpret_cast<int8_t*>(own + o_mc),
+                                       reinterpret_cast<float*>(own + o_ms), st);
+    if (tiles < 0) return psb_set_err(c, PSB_ECUDA, "q8 TMA reduce launch");
+    const size_t done = blk_lo + (size_t)tiles * 8;
+    if (done < blk_hi) {  // ragged tail: direct loads
+      Q8Workers wt = wr;
+      for (int q = 0; q < P; ++q) {
+        wt.codes[q] += (size_t)tiles * 8 * B;
+        wt.scales[q] += (size_t)tiles * 8;
+      }
+      s = psb_q8_reduce_launch(c, wt, P, done, blk_hi, n, B, d->order, dpn, npr,
+                               reinterpret_cast<int8_t*>(own + o_mc), reinterpret_cast<float*>(own + o_ms), d->lr,
+                               nullptr, nullptr, st);
+      if (s) return s;
+    }
+    psb_mark(c, st);
+  } else {
   PeerSegs sg{};
   for (int q = 0; q < P; ++q) {
     if (q / W == c->rank || blk_hi <= blk_lo) continue;
@@ -688,6 +722,7 @@ static psb_status q8_step_nvlink(psb_ctx* c, const psb_step_desc* d, cudaStream_
                            nullptr, nullptr, st);
   if (s) return s;
   psb_mark(c, st);
+  }
   // ---- all-gather: pull every other rank's requantized shard into place
   s = psb_peer_signal(c, st);
   if (!s) s = psb_peer_wait_ready(c, st);
@@ -773,7 +808,10 @@ static psb_status q8_step(psb_ctx* c, const psb_step_desc* d, cudaStream_t st) {
   PSB_REQUIRE(c, B == 128 || B == 256 || B == 512 || B == 1024, "q8: block must be 128, 256, 512 or 1024");
   const size_t n = d->n;
   const size_t nb = (n + B - 1) / B;
-  const size_t nbs = (nb + R - 1) / R;           // blocks per shard
+  // blocks per shard, a multiple of 8 (8-block TMA tiles and 32-byte scale
+  // copies start on shard boundaries; the fold is per element, so shard
+  // boundaries never change a result)
+  const size_t nbs = (((nb + R - 1) / R) + 7) & ~(size_t)7;
   const size_t shard_elems = nbs * B;
   const size_t n_pad = (size_t)R * shard_elems;  // >= n
   // workspace: local codes W*n_pad | local scales W*R*nbs | recv codes P*shard | recv scales P*nbs

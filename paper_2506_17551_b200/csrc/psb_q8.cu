@@ -380,6 +380,92 @@ __global__ void __launch_bounds__(256) k_q8_reduce_pipe(Q8Workers wv, size_t blk
   }
 }
 
+constexpr int kQ8Stages = 4;  // TMA ring depth of the q8 kernels
+
+// The multi-rank reduce reading every worker's codes and scales of this
+// rank's shard in place (local arena or the peers' NVLink-mapped arenas) with
+// 1-D TMA bulk copies into a kQ8Stages ring of 8-block tiles, instead of a
+// pull into local memory followed by k_q8_reduce_pipe.  Same per-element
+// operations (compile-time P, plain worker-order fold).  Full tiles only; the
+// host reduces a ragged tail with k_q8_reduce*.
+template <int VPL, int PT>
+__global__ void __launch_bounds__(256) k_q8_reduce_tma(Q8Workers wv, size_t blk_lo, size_t ntiles,
+                                                       int8_t* __restrict__ mcodes, float* __restrict__ mscales) {
+  constexpr int B = VPL * 128;
+  constexpr uint32_t CB = 8 * B;        // code bytes per worker per tile
+  constexpr uint32_t SB = 8 * 4;        // scale bytes per worker per tile
+  constexpr uint32_t STG = PT * (CB + SB);
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[kQ8Stages];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t my_tiles = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kQ8Stages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](size_t i) {
+    const int s = (int)(i % kQ8Stages);
+    const size_t t = blockIdx.x + i * gridDim.x;  // tile within the shard
+    unsigned char* st = smem + (size_t)s * STG;
+    mbar_expect_tx(&full[s], STG);
+#pragma unroll
+    for (int q = 0; q < PT; ++q) {
+      tma_load_1d(st + (size_t)q * CB, wv.codes[q] + t * CB, CB, &full[s]);
+      tma_load_1d(st + (size_t)PT * CB + (size_t)q * SB, wv.scales[q] + t * 8, SB, &full[s]);
+    }
+  };
+  if (threadIdx.x == 0)
+    for (size_t i = 0; i < my_tiles && i < (size_t)kQ8Stages; ++i) issue(i);
+  const float inv = (float)(1.0 / (double)PT);
+  for (size_t i = 0; i < my_tiles; ++i) {
+    const int s = (int)(i % kQ8Stages);
+    mbar_wait(&full[s], (uint32_t)((i / kQ8Stages) & 1));
+    const unsigned char* st = smem + (size_t)s * STG;
+    const size_t blk = blk_lo + (blockIdx.x + i * gridDim.x) * 8 + wid;
+    float sc[PT];
+#pragma unroll
+    for (int q = 0; q < PT; ++q) sc[q] = reinterpret_cast<const float*>(st + (size_t)PT * CB + (size_t)q * SB)[wid];
+    float m[VPL][4];
+    float amax = 0.f;
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+      const int o = wid * B + it * 128 + lane * 4;
+      char4 cv = *reinterpret_cast<const char4*>(st + o);
+      float4 acc = make_float4(__fmul_rn((float)cv.x, sc[0]), __fmul_rn((float)cv.y, sc[0]),
+                               __fmul_rn((float)cv.z, sc[0]), __fmul_rn((float)cv.w, sc[0]));
+#pragma unroll
+      for (int q = 1; q < PT; ++q) {
+        cv = *reinterpret_cast<const char4*>(st + (size_t)q * CB + o);
+        acc.x = __fadd_rn(acc.x, __fmul_rn((float)cv.x, sc[q]));
+        acc.y = __fadd_rn(acc.y, __fmul_rn((float)cv.y, sc[q]));
+        acc.z = __fadd_rn(acc.z, __fmul_rn((float)cv.z, sc[q]));
+        acc.w = __fadd_rn(acc.w, __fmul_rn((float)cv.w, sc[q]));
+      }
+      m[it][0] = __fmul_rn(acc.x, inv);
+      m[it][1] = __fmul_rn(acc.y, inv);
+      m[it][2] = __fmul_rn(acc.z, inv);
+      m[it][3] = __fmul_rn(acc.w, inv);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) amax = fmaxf(amax, fabsf(m[it][c]));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const float scale = __fdiv_rn(amax, 127.0f);
+    const float rinv = __frcp_rn(scale);
+    if (lane == 0) mscales[blk] = scale;
+#pragma unroll
+    for (int it = 0; it < VPL; ++it) {
+      const size_t e0 = blk * B + (size_t)it * 128 + lane * 4;
+      *reinterpret_cast<char4*>(mcodes + e0) =
+          make_char4((signed char)q8_code(m[it][0], scale, rinv), (signed char)q8_code(m[it][1], scale, rinv),
+                     (signed char)q8_code(m[it][2], scale, rinv), (signed char)q8_code(m[it][3], scale, rinv));
+    }
+    __syncthreads();  // every warp is done with stage s
+    if (threadIdx.x == 0 && i + kQ8Stages < my_tiles) issue(i + kQ8Stages);
+  }
+}
+
 // Single-rank fused step (R == 1): per block of B elements, each local worker
 // q's p = r + g is quantized (codes stay in registers), r' = p - xhat written,
 // and xhat = code*scale folded in the reference order; the mean is requantized
@@ -543,7 +629,6 @@ __global__ void __launch_bounds__(256) k_q8_step1(const float* __restrict__ g, s
 // flight no longer depend on registers; each warp then quantizes one block
 // of the stage exactly as k_q8_step1 does (same per-element operations, same
 // order) and stores r' and theta' straight to global memory.
-constexpr int kQ8Stages = 4;
 
 template <int VPL>
 __global__ void __launch_bounds__(256) k_q8_step1_tma(const float* __restrict__ g, float* __restrict__ r, size_t n,
@@ -1085,6 +1170,35 @@ psb_status psb_q8_step1_launch(psb_ctx* c, const float* g, size_t gstride, float
   c->launches += 1;
   PSB_LAUNCH_CHECK(c, "q8 fused step");
   return PSB_OK;
+}
+
+// Returns the number of full 8-block tiles reduced (the caller reduces the
+// rest), or -1 when the TMA reduce does not apply (P / B combination).
+long long psb_q8_reduce_tma_launch(psb_ctx* c, const Q8Workers& wv, int P, size_t blk_lo, size_t blk_hi, uint32_t B,
+                                   int8_t* mcodes, float* mscales, cudaStream_t st) {
+  const size_t ntiles = (blk_hi - blk_lo) / 8;
+  if (ntiles == 0) return 0;
+  const unsigned grid = (unsigned)std::min<size_t>(ntiles, (size_t)c->num_sms * 2);
+#define PSB_RT(V, PP)                                                                                       \
+  do {                                                                                                      \
+    const size_t smem = (size_t)kQ8Stages * PP * (8 * V * 128 + 32);                                        \
+    cudaFuncSetAttribute(k_q8_reduce_tma<V, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
+    k_q8_reduce_tma<V, PP><<<grid, 256, smem, st>>>(wv, blk_lo, ntiles, mcodes, mscales);                  \
+  } while (0)
+  const int vpl = (int)(B / 128);
+  if (P == 2 && vpl == 1) PSB_RT(1, 2);
+  else if (P == 2 && vpl == 2) PSB_RT(2, 2);
+  else if (P == 2 && vpl == 4) PSB_RT(4, 2);
+  else if (P == 4 && vpl == 1) PSB_RT(1, 4);
+  else if (P == 4 && vpl == 2) PSB_RT(2, 4);
+  else if (P == 8 && vpl == 1) PSB_RT(1, 8);
+  else if (P == 8 && vpl == 2) PSB_RT(2, 8);
+  else return -1;
+#undef PSB_RT
+  c->launches += 1;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return -2;
+  return (long long)ntiles;
 }
 
 psb_status psb_q8_apply_tma_launch(psb_ctx* c, const Q8Shards& ms, const float* scales, size_t n, uint32_t B,
